@@ -1,0 +1,168 @@
+/*
+ * ecl_cuda.h — C-ABI of the B200 device layer (libecl_cuda.so).
+ *
+ * This is the seam that replaces the reference's per-device executor
+ *   coexec::NativePool::execute_package(const Package&, const ValidatedProgram&,
+ *       const KernelFn&, span<const vector<byte>> inputs,
+ *       span<vector<byte>> outputs, TallySlot*)
+ *   — /root/reference/proj/include/coexec/engine.hpp:120-136, selected per
+ *   device at engine.hpp:211-215 and called from drive_wall at :385 —
+ * together with the kernel plugin resolution kernel_for()/check_buffer_shapes()
+ * (workloads.hpp:170-233).  Plain C types only: no C++ or torch types cross it,
+ * no exception crosses it.
+ *
+ * One ecl_gpu = one B200: a compute stream, a copy stream, a ring of timing
+ * events, this device's replica of every read-only input and its own output
+ * partition.  Each ecl_gpu is driven by exactly one host thread.
+ *
+ * Status codes: ECL_OK (0) or the negated coexec::ErrorCode + 1 (error.hpp:11-39
+ * order), so a caller maps them 1:1 onto coexec::Error; device faults map to
+ * ECL_KERNEL_PANIC.  ecl_last_error() returns the calling thread's last message.
+ */
+#ifndef ECL_CUDA_H
+#define ECL_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum ecl_status {
+  ECL_OK = 0,
+  ECL_NON_DIVISIBLE_WORK_SIZE = -1,
+  ECL_BAD_OUT_PATTERN = -2,
+  ECL_EMPTY_PROGRAM = -3,
+  ECL_INDIVISIBLE_PACKAGE = -4,
+  ECL_TOO_FEW_WORK_GROUPS = -5,
+  ECL_BAD_SCHEDULER_CONFIG = -6,
+  ECL_SCHEDULER_ERROR = -7,
+  ECL_INPUT_SIZE_MISMATCH = -8,
+  ECL_KERNEL_PANIC = -9,
+  ECL_EMPTY_QUEUE_WITH_PENDING_WORK = -10,
+  ECL_TALLY_VIOLATION = -11,
+  ECL_EMPTY_TRACE = -12,
+  ECL_NON_POSITIVE_TIME = -13,
+  ECL_MISSING_BASELINE = -14,
+  ECL_NON_POSITIVE_REFERENCE = -15,
+  ECL_UNKNOWN_KERNEL = -16,
+  ECL_UNKNOWN_PROFILE = -17,
+  ECL_BAD_KERNEL_ARGS = -18,
+  ECL_MALFORMED_TRACE = -19,
+  ECL_CONFIG_ERROR = -20,
+  ECL_IO_ERROR = -21,
+  ECL_PENDING = 1 /* ecl_gpu_poll: package still running */
+};
+
+/* A kernel argument: coexec::ArgValue = variant<int64_t, double> (core.hpp:75). */
+typedef struct {
+  int32_t is_double;
+  int32_t reserved;
+  int64_t i;
+  double d;
+} ecl_arg;
+
+/* Buffer geometry: coexec::BufferDesc without the name (core.hpp:55-64). */
+typedef struct {
+  uint64_t element_size_bytes;
+  uint64_t element_count;
+} ecl_buffer_geom;
+
+typedef struct ecl_kernel ecl_kernel; /* resolved kernel id + args + geometry */
+typedef struct ecl_gpu ecl_gpu;       /* one device context */
+
+/* Completion callback.  Runs on CUDA's host-callback thread: it must not call
+ * CUDA; it only records (seq, status) for the owning device thread. */
+typedef void (*ecl_done_fn)(void* user, uint64_t seq, int status);
+
+/* ---- device discovery / lifetime ------------------------------------- */
+int ecl_gpu_count(int* count);
+/* queue_depth = packages that may be in flight on this device (>= 1). */
+int ecl_gpu_open(int ordinal, uint32_t queue_depth, ecl_gpu** out);
+int ecl_gpu_close(ecl_gpu* gpu);
+int ecl_gpu_sm_count(const ecl_gpu* gpu, int* sms);
+int ecl_gpu_ordinal(const ecl_gpu* gpu, int* ordinal);
+
+/* ---- kernel registry (replaces kernel_for / check_buffer_shapes) ------ */
+/* Kernel ids: "mandelbrot", "mandelbrot_f32", "vecscale",
+ * "synthetic[:constant|ramp|step]", "gaussian", "nbody", "binomial", "ray".
+ * Validates argument and buffer shapes once (ECL_UNKNOWN_KERNEL,
+ * ECL_UNKNOWN_PROFILE, ECL_BAD_KERNEL_ARGS). */
+int ecl_kernel_create(const char* kernel_id, uint64_t global_work_size, uint64_t local_work_size,
+                      const ecl_arg* args, uint32_t n_args, const ecl_buffer_geom* inputs, uint32_t n_inputs,
+                      const ecl_buffer_geom* outputs, uint32_t n_outputs, uint64_t out_indices,
+                      uint64_t out_work_items, ecl_kernel** out);
+void ecl_kernel_destroy(ecl_kernel* kernel);
+
+/* ---- buffers --------------------------------------------------------- */
+/* Allocates this device's replica of every input and its output partition
+ * (full extent, so package slices keep their global offsets).  Re-binding the
+ * same geometry reuses the allocations. */
+int ecl_gpu_bind(ecl_gpu* gpu, const ecl_kernel* kernel);
+int ecl_gpu_buffer(ecl_gpu* gpu, int is_output, uint32_t index, void** device_ptr);
+/* Swaps input i with output o in place (same byte size): iterative programs
+ * (NBody steps) ping-pong without copies. */
+int ecl_gpu_swap_io(ecl_gpu* gpu, uint32_t input_index, uint32_t output_index);
+/* Async H2D of every input (host_inputs[i] may be NULL to skip one). */
+int ecl_gpu_upload_inputs(ecl_gpu* gpu, const void* const* host_inputs);
+/* Replicates every bound input from gpus[root] to the others over NVLink
+ * (cudaMemcpyPeerAsync, binary doubling tree); ordered after root's upload. */
+int ecl_replicate_inputs(ecl_gpu* const* gpus, uint32_t n, uint32_t root);
+/* Copies output elements [elem_offset, elem_offset+elem_count) of output
+ * `index` from gpus[src] to the same range on every other device (NBody's
+ * per-step exchange of owner slices, P2P over NVLink).  Enqueued on src's
+ * compute stream. */
+int ecl_broadcast_output_slice(ecl_gpu* const* gpus, uint32_t n, uint32_t src, uint32_t index,
+                               uint64_t elem_offset, uint64_t elem_count);
+/* D2H of a slice of one output (used to gather device-resident results). */
+int ecl_gpu_download_slice(ecl_gpu* gpu, uint32_t index, uint64_t elem_offset, uint64_t elem_count,
+                           void* host_dst);
+int ecl_host_register(void* ptr, size_t bytes);
+int ecl_host_unregister(void* ptr);
+
+/* ---- packages -------------------------------------------------------- */
+/* Enqueues package `seq` = work-groups [offset_wg, offset_wg+size_wg): the
+ * kernel over its work-items on the compute stream between two timing
+ * events; then, on the copy stream, the D2H of the package's out_range_for
+ * slice of every output into host_outputs[b] (if host_outputs != NULL and
+ * host_outputs[b] != NULL) and the completion callback.  Fails with
+ * ECL_INDIVISIBLE_PACKAGE before any write when the out pattern cannot split
+ * the package (core.hpp:172-185). */
+int ecl_gpu_submit(ecl_gpu* gpu, uint64_t seq, uint64_t offset_wg, uint64_t size_wg,
+                   void* const* host_outputs, ecl_done_fn done, void* user);
+/* ECL_OK when package `seq` (and its copies) completed, ECL_PENDING while
+ * running, ECL_KERNEL_PANIC on a device fault. */
+int ecl_gpu_poll(ecl_gpu* gpu, uint64_t seq);
+/* Start/end of the package's kernel on the host steady clock (ms), mapped
+ * through the epoch set by ecl_gpu_set_epoch.  Valid after completion. */
+int ecl_gpu_package_times(ecl_gpu* gpu, uint64_t seq, double* t_start_ms, double* t_end_ms);
+/* Anchors device event time to host time: records an event, waits for it and
+ * pairs it with host_now_ms() of the caller's clock (returned). */
+int ecl_gpu_set_epoch(ecl_gpu* gpu, double (*host_now_ms)(void*), void* clock_user);
+int ecl_gpu_sync(ecl_gpu* gpu);
+/* Exactly-once tally (COEXEC_TALLY=1, engine.hpp:228-252): when enabled,
+ * every submitted package also bumps one uint32 per work-item on device. */
+int ecl_gpu_enable_tally(ecl_gpu* gpu, int enable);
+int ecl_gpu_download_tally(ecl_gpu* gpu, uint32_t* host_counts);
+
+/* ---- native baseline (overhead denominator) --------- */
+/* One launch over the whole grid on the compute stream; *kernel_ms is the
+ * CUDA-event time of that launch.  Synchronous. */
+int ecl_gpu_native_run(ecl_gpu* gpu, float* kernel_ms);
+
+/* Kernel time of the most recent submit() / native_run() launches summed
+ * since the last reset (for roofline accounting). */
+int ecl_gpu_kernel_time(ecl_gpu* gpu, double* total_ms, uint64_t* launches, int reset);
+
+/* Measured vector peaks of device `ordinal` (roofline denominators for the
+ * FP64/FP32-pipe kernels): DFMA TFLOP/s, DADD Tinstr/s, FFMA TFLOP/s. */
+int ecl_probe_vector_peaks(int ordinal, double* fp64_fma_tflops, double* fp64_add_tinstr, double* fp32_fma_tflops);
+
+const char* ecl_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ECL_CUDA_H */

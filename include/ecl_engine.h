@@ -1,0 +1,88 @@
+/*
+ * ecl_engine.h — C-ABI of the co-execution engine (libcoexec.so).
+ *
+ * The FFI surface a non-C++ caller of the reference would bind (ctypes, cgo,
+ * JNI ...): the reference's public entry Engine(EngineConfig,
+ * ValidatedProgram).run(inputs) -> RunResult{outputs, trace}
+ * (/root/reference/proj/include/coexec/engine.hpp:206-256), its scheduler
+ * strategy seam Scheduler::next/remaining_work_groups (schedulers.hpp:178-183),
+ * and the core checks validate_program / out_range_for / tiles_exactly
+ * (core.hpp:107-198) and make_report (metrics.hpp:104-117).
+ *
+ * Configuration crosses as the reference's own JSON schema 1
+ * (config.hpp:41-153: "program", "devices", "scheduler", plus "clock_mode",
+ * "seed", "exclude_init"); traces come back as trace JSON schema 1
+ * (trace_io.hpp:92-115).  Buffers cross as plain host pointers.  Status
+ * codes are those of include/ecl_cuda.h.  Functions returning int64_t
+ * return the string length (excluding NUL) or a negative status, and write
+ * the string when cap > length.
+ */
+#ifndef ECL_ENGINE_H
+#define ECL_ENGINE_H
+
+#include <stdint.h>
+
+#include "ecl_cuda.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ecl_engine ecl_engine;
+typedef struct ecl_scheduler ecl_scheduler;
+
+/* ---- engine ---------------------------------------------------------- */
+int ecl_engine_create(const char* config_json, ecl_engine** out);
+void ecl_engine_destroy(ecl_engine* engine);
+/* Wall run.  inputs[i] holds in_buffers[i]; outputs NULL (or every entry
+ * NULL) = device-resident run (see ecl_engine_gather).  Page-locked output
+ * buffers (ecl_host_register) get per-package async D2H. */
+int ecl_engine_run(ecl_engine* engine, const void* const* inputs, uint32_t n_inputs, void* const* outputs,
+                   uint32_t n_outputs);
+/* Virtual-clock run with one cost per work-item (NULL = analytic costs). */
+int ecl_engine_run_virtual(ecl_engine* engine, const double* item_costs, uint64_t n);
+int ecl_engine_gather(ecl_engine* engine, void* const* outputs, uint32_t n_outputs);
+int64_t ecl_engine_trace_json(ecl_engine* engine, char* buf, uint64_t cap);
+/* Native baseline: one launch over the whole grid on the first device. */
+int ecl_engine_native_run(ecl_engine* engine, const void* const* inputs, uint32_t n_inputs, void* const* outputs,
+                          uint32_t n_outputs, double* kernel_ms, double* total_ms);
+int ecl_engine_kernel_time(ecl_engine* engine, double* kernel_ms, uint64_t* launches, int reset);
+double ecl_engine_init_ms(const ecl_engine* engine);
+/* EngineFailure of the last failed call (the paper's get_errors()). */
+uint32_t ecl_engine_error_count(const ecl_engine* engine);
+int64_t ecl_engine_error(const ecl_engine* engine, uint32_t i, int* status, char* buf, uint64_t cap);
+
+/* ---- scheduler seam --------------------------------------------------- */
+/* {"scheduler": {...}, "devices": [...], "total_work_groups": N} */
+int ecl_scheduler_create(const char* json, ecl_scheduler** out);
+void ecl_scheduler_destroy(ecl_scheduler* s);
+/* 1 = granted (*offset_wg, *size_wg set), 0 = nothing left for this device. */
+int ecl_scheduler_next(ecl_scheduler* s, uint32_t device, uint64_t* offset_wg, uint64_t* size_wg);
+uint64_t ecl_scheduler_remaining(const ecl_scheduler* s);
+int ecl_scheduler_observe(ecl_scheduler* s, uint32_t device, uint64_t work_items, double busy_ms);
+/* HGuided only: floor(G_r * P_i / denominator) before clamping; -1 otherwise. */
+int64_t ecl_scheduler_unclamped(const ecl_scheduler* s, uint64_t pending_wg, uint32_t device);
+int64_t ecl_describe_scheduler(const char* scheduler_json, char* buf, uint64_t cap);
+/* resolve_static as JSON ({"proportions": [...], "device_order": [...]}). */
+int64_t ecl_resolve_static(const char* scheduler_json, const char* devices_json, char* buf, uint64_t cap);
+/* apply_default_min_package over a devices JSON array. */
+int64_t ecl_apply_default_min_package(const char* devices_json, char* buf, uint64_t cap);
+
+/* ---- core checks ------------------------------------------------------ */
+int ecl_validate_program(const char* program_json, uint64_t* total_work_groups);
+int ecl_out_range_for(const char* program_json, uint64_t offset_wg, uint64_t size_wg, uint64_t* offset,
+                      uint64_t* count);
+/* 1 when the packages tile [0, total_wg) exactly once, else 0. */
+int ecl_tiles_exactly(const uint64_t* offsets, const uint64_t* sizes, uint64_t n, uint64_t total_wg);
+/* make_report; reference_ms < 0 = no overhead figure. */
+int64_t ecl_metrics_report(const char* trace_json, const double* solo_ms, uint32_t n_solo, double reference_ms,
+                           char* buf, uint64_t cap);
+int64_t ecl_trace_csv(const char* trace_json, char* buf, uint64_t cap);
+
+const char* ecl_engine_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ECL_ENGINE_H */

@@ -1,0 +1,98 @@
+// engine.hpp — the co-execution engine (reference: engine.hpp:21-446).
+//
+// Same surface — Engine(EngineConfig, ValidatedProgram).run(inputs) ->
+// RunResult{outputs, trace} — with the device executor replaced: each Cuda
+// device is one B200 behind include/ecl_cuda.h, driven by one persistent
+// host thread that pulls packages from the mutex-serialized scheduler with
+// up to Backend::queue_depth packages in flight, so the next package is
+// already queued on the GPU when the current one ends.
+//
+// Additions for the B200 build:
+//   run_into()     caller-owned host outputs (the paper's program.out(v),
+//                  PAPER.md:366) — pinned buffers get async D2H per package
+//                  overlapped with the next package's kernel; nullptr
+//                  outputs keep results device-resident (gather() later).
+//   run_virtual()  the virtual-clock replay (engine.hpp:306-338) with
+//                  caller-supplied per-item costs; trace only.
+//   native_run()   one launch over the whole grid: the overhead denominator.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <vector>
+
+#include "coexec/core.hpp"
+#include "coexec/schedulers.hpp"
+
+namespace coexec {
+
+struct EngineConfig {
+  std::vector<DeviceProfile> devices;
+  SchedulerConfig scheduler;
+  ClockMode clock_mode = ClockMode::Wall;
+  std::uint64_t seed = 0;
+  bool exclude_init_from_total = false;
+  bool tally = false;  // exactly-once check (also enabled by COEXEC_TALLY=1)
+};
+
+struct RunResult {
+  std::vector<std::vector<std::byte>> outputs;
+  ExecutionTrace trace;
+};
+
+struct NativeResult {
+  double kernel_ms = 0.0;  // CUDA-event time of the single launch
+  double total_ms = 0.0;   // host wall time: first H2D -> last D2H
+};
+
+struct KernelTiming {
+  double kernel_ms = 0.0;  // summed CUDA-event time of every package launch
+  std::uint64_t launches = 0;
+};
+
+class Engine {
+ public:
+  Engine(EngineConfig cfg, ValidatedProgram prog);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  /// Reference semantics (engine.hpp:219-256): engine-allocated outputs.
+  RunResult run(std::span<const std::vector<std::byte>> inputs);
+
+  /// Caller-owned buffers; inputs[i] must hold in_buffers[i].size_bytes()
+  /// bytes.  outputs empty (or all null) = device-resident run.
+  ExecutionTrace run_into(std::span<const void* const> inputs, std::span<void* const> outputs);
+
+  /// Virtual clock (simulated devices): per-item costs, one per work-item;
+  /// empty = the analytic cost of vecscale/synthetic kernels.
+  ExecutionTrace run_virtual(std::span<const double> item_costs);
+
+  /// Copies the last device-resident run's slices to host buffers.
+  void gather(std::span<void* const> outputs);
+
+  /// One kernel launch over the whole grid on the first device, same
+  /// uploads/downloads as run_into (outputs may be empty).
+  NativeResult native_run(std::span<const void* const> inputs, std::span<void* const> outputs);
+
+  KernelTiming kernel_timing(bool reset);
+  const ExecutionTrace& last_trace() const;
+  double init_ms() const;
+  const ValidatedProgram& program() const;
+  const EngineConfig& config() const;
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+};
+
+/// Reference free function (engine.hpp:440-444).
+inline RunResult run(const EngineConfig& cfg, const ValidatedProgram& prog,
+                     std::span<const std::vector<std::byte>> inputs) {
+  Engine engine(cfg, prog);
+  return engine.run(inputs);
+}
+
+}  // namespace coexec

@@ -1,0 +1,534 @@
+// device.cu — the B200 device layer behind include/ecl_cuda.h.
+//
+// Replaces NativePool (engine.hpp:97-200): where the reference wakes W host
+// threads, splits the package contiguously and waits on a condition variable
+// (engine.hpp:120-136), a package here is one kernel launch on the device's
+// compute stream bracketed by two timing events.  The D2H of the package's
+// out_range_for slice and the completion callback go on a second (copy)
+// stream that waits on the end event, so the copy of package k overlaps the
+// kernel of package k+1 and the compute stream never blocks on the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ecl_cuda.h"
+#include "kernels.cuh"
+
+struct ecl_kernel {
+  ecl::KernelSpec spec;
+};
+
+namespace {
+
+thread_local std::string t_error;
+
+int fail(int code, const std::string& msg) {
+  t_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  t_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return ECL_KERNEL_PANIC;
+}
+
+#define ECL_CK(call)                                  \
+  do {                                                \
+    cudaError_t e_ = (call);                          \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+constexpr uint32_t kSlots = 64;  // timing-event ring; >= 2 x max queue depth
+
+struct Slot {
+  cudaEvent_t start = nullptr;  // kernel start (compute stream)
+  cudaEvent_t end = nullptr;    // kernel end (compute stream)
+  cudaEvent_t done = nullptr;   // copies + callback finished (copy stream)
+  uint64_t seq = ~0ull;
+  bool busy = false;
+  bool timed = false;
+  ecl_done_fn fn = nullptr;
+  void* user = nullptr;
+};
+
+void CUDART_CB on_package_done(void* arg) {
+  Slot* s = static_cast<Slot*>(arg);
+  if (s->fn) s->fn(s->user, s->seq, ECL_OK);
+}
+
+}  // namespace
+
+struct ecl_gpu {
+  int ordinal = 0;
+  int sms = 0;
+  uint32_t depth = 2;
+  cudaStream_t compute = nullptr;
+  cudaStream_t copy = nullptr;
+  cudaEvent_t epoch = nullptr;
+  cudaEvent_t ready = nullptr;  // last input/replication write on this device
+  double epoch_host_ms = 0.0;
+  Slot slots[kSlots];
+  const ecl::KernelSpec* spec = nullptr;
+  std::vector<void*> in, out;
+  std::vector<uint64_t> in_bytes, out_bytes;
+  unsigned* ctrl = nullptr;
+  uint32_t* tally = nullptr;
+  uint64_t tally_items = 0;
+  bool tally_on = false;
+  double kernel_ms = 0.0;
+  uint64_t launches = 0;
+  uint32_t next_slot = 0;  // per-device rotation: seqs are global across devices
+};
+
+namespace {
+
+Slot* find_slot(ecl_gpu* g, uint64_t seq) {
+  for (auto& s : g->slots)
+    if (s.busy && s.seq == seq) return &s;
+  return nullptr;
+}
+
+int set_device(const ecl_gpu* g) {
+  ECL_CK(cudaSetDevice(g->ordinal));
+  return ECL_OK;
+}
+
+ecl::LaunchEnv env_of(const ecl_gpu* g) {
+  ecl::LaunchEnv env;
+  env.stream = g->compute;
+  env.sms = g->sms;
+  env.in = g->in.data();
+  env.out = g->out.data();
+  env.ctrl = g->ctrl;
+  return env;
+}
+
+// out_range_for (core.hpp:172-185): the package's output-element range.
+int out_range(const ecl::KernelSpec& s, uint64_t offset_wg, uint64_t size_wg, uint64_t* off, uint64_t* cnt) {
+  const uint64_t items = size_wg * s.lws, first = offset_wg * s.lws;
+  if ((items * s.out_indices) % s.out_work_items != 0 || (first * s.out_indices) % s.out_work_items != 0)
+    return fail(ECL_INDIVISIBLE_PACKAGE, "package of " + std::to_string(items) + " work-items at offset " +
+                                             std::to_string(first) + " is not divisible by out pattern " +
+                                             std::to_string(s.out_indices) + ":" + std::to_string(s.out_work_items));
+  *off = first * s.out_indices / s.out_work_items;
+  *cnt = items * s.out_indices / s.out_work_items;
+  return ECL_OK;
+}
+
+void free_buffers(ecl_gpu* g) {
+  for (void* p : g->in) cudaFree(p);
+  for (void* p : g->out) cudaFree(p);
+  g->in.clear();
+  g->out.clear();
+  g->in_bytes.clear();
+  g->out_bytes.clear();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ecl_last_error(void) { return t_error.c_str(); }
+
+int ecl_gpu_count(int* count) {
+  *count = 0;
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    cudaGetLastError();
+    return fail(ECL_CONFIG_ERROR, std::string("CUDA unavailable: ") + cudaGetErrorString(e));
+  }
+  return ECL_OK;
+}
+
+int ecl_gpu_open(int ordinal, uint32_t queue_depth, ecl_gpu** out) {
+  *out = nullptr;
+  int n = 0;
+  if (ecl_gpu_count(&n) != ECL_OK) return ECL_CONFIG_ERROR;
+  if (ordinal < 0 || ordinal >= n)
+    return fail(ECL_CONFIG_ERROR, "CUDA device ordinal " + std::to_string(ordinal) + " out of range (" +
+                                      std::to_string(n) + " visible)");
+  if (queue_depth < 1 || queue_depth > kSlots / 2)
+    return fail(ECL_CONFIG_ERROR, "queue_depth must lie in [1, " + std::to_string(kSlots / 2) + "]");
+  auto* g = new ecl_gpu;
+  g->ordinal = ordinal;
+  g->depth = queue_depth;
+  auto undo = [&](int rc) {
+    ecl_gpu_close(g);
+    return rc;
+  };
+  if (int rc = set_device(g)) return undo(rc);
+  cudaError_t e = cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, ordinal);
+  if (e != cudaSuccess) return undo(cuda_fail(e, "cudaDeviceGetAttribute"));
+  if ((e = cudaStreamCreateWithFlags(&g->compute, cudaStreamNonBlocking)) != cudaSuccess)
+    return undo(cuda_fail(e, "cudaStreamCreate(compute)"));
+  if ((e = cudaStreamCreateWithFlags(&g->copy, cudaStreamNonBlocking)) != cudaSuccess)
+    return undo(cuda_fail(e, "cudaStreamCreate(copy)"));
+  if ((e = cudaEventCreate(&g->epoch)) != cudaSuccess) return undo(cuda_fail(e, "cudaEventCreate"));
+  if ((e = cudaEventCreateWithFlags(&g->ready, cudaEventDisableTiming)) != cudaSuccess)
+    return undo(cuda_fail(e, "cudaEventCreate"));
+  for (auto& s : g->slots) {
+    if ((e = cudaEventCreate(&s.start)) != cudaSuccess || (e = cudaEventCreate(&s.end)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming)) != cudaSuccess)
+      return undo(cuda_fail(e, "cudaEventCreate(slot)"));
+  }
+  if ((e = cudaMalloc(&g->ctrl, 256)) != cudaSuccess) return undo(cuda_fail(e, "cudaMalloc(ctrl)"));
+  if ((e = cudaMemset(g->ctrl, 0, 256)) != cudaSuccess) return undo(cuda_fail(e, "cudaMemset(ctrl)"));
+  *out = g;
+  return ECL_OK;
+}
+
+int ecl_gpu_close(ecl_gpu* g) {
+  if (!g) return ECL_OK;
+  cudaSetDevice(g->ordinal);
+  if (g->compute) cudaStreamSynchronize(g->compute);
+  if (g->copy) cudaStreamSynchronize(g->copy);
+  free_buffers(g);
+  if (g->ctrl) cudaFree(g->ctrl);
+  if (g->tally) cudaFree(g->tally);
+  for (auto& s : g->slots) {
+    if (s.start) cudaEventDestroy(s.start);
+    if (s.end) cudaEventDestroy(s.end);
+    if (s.done) cudaEventDestroy(s.done);
+  }
+  if (g->epoch) cudaEventDestroy(g->epoch);
+  if (g->ready) cudaEventDestroy(g->ready);
+  if (g->compute) cudaStreamDestroy(g->compute);
+  if (g->copy) cudaStreamDestroy(g->copy);
+  delete g;
+  return ECL_OK;
+}
+
+int ecl_gpu_sm_count(const ecl_gpu* g, int* sms) {
+  *sms = g->sms;
+  return ECL_OK;
+}
+
+int ecl_gpu_ordinal(const ecl_gpu* g, int* ordinal) {
+  *ordinal = g->ordinal;
+  return ECL_OK;
+}
+
+int ecl_kernel_create(const char* kernel_id, uint64_t gws, uint64_t lws, const ecl_arg* args, uint32_t n_args,
+                      const ecl_buffer_geom* inputs, uint32_t n_inputs, const ecl_buffer_geom* outputs,
+                      uint32_t n_outputs, uint64_t out_indices, uint64_t out_work_items, ecl_kernel** out) {
+  *out = nullptr;
+  if (!kernel_id) return fail(ECL_UNKNOWN_KERNEL, "null kernel id");
+  if (gws == 0 || lws == 0) return fail(ECL_CONFIG_ERROR, "global/local work size must be positive");
+  if (gws % lws != 0) return fail(ECL_NON_DIVISIBLE_WORK_SIZE, "local_work_size does not divide global_work_size");
+  if (out_indices == 0 || out_work_items == 0) return fail(ECL_BAD_OUT_PATTERN, "out_pattern components must be positive");
+  auto* k = new ecl_kernel;
+  ecl::KernelSpec& s = k->spec;
+  s.id = kernel_id;
+  s.gws = gws;
+  s.lws = lws;
+  s.out_indices = out_indices;
+  s.out_work_items = out_work_items;
+  s.args.assign(args, args + n_args);
+  s.inputs.assign(inputs, inputs + n_inputs);
+  s.outputs.assign(outputs, outputs + n_outputs);
+  std::string err;
+  const int rc = ecl::resolve_kernel(s, &err);
+  if (rc != ECL_OK) {
+    delete k;
+    return fail(rc, err);
+  }
+  *out = k;
+  return ECL_OK;
+}
+
+void ecl_kernel_destroy(ecl_kernel* k) { delete k; }
+
+int ecl_gpu_bind(ecl_gpu* g, const ecl_kernel* k) {
+  if (int rc = set_device(g)) return rc;
+  ECL_CK(cudaStreamSynchronize(g->compute));
+  ECL_CK(cudaStreamSynchronize(g->copy));
+  std::vector<uint64_t> want_in, want_out;
+  for (const auto& b : k->spec.inputs) want_in.push_back(b.element_size_bytes * b.element_count);
+  for (const auto& b : k->spec.outputs) want_out.push_back(b.element_size_bytes * b.element_count);
+  if (want_in != g->in_bytes || want_out != g->out_bytes) {
+    free_buffers(g);
+    for (uint64_t bytes : want_in) {
+      void* p = nullptr;
+      ECL_CK(cudaMalloc(&p, std::max<uint64_t>(bytes, 16)));
+      g->in.push_back(p);
+    }
+    for (uint64_t bytes : want_out) {
+      void* p = nullptr;
+      ECL_CK(cudaMalloc(&p, std::max<uint64_t>(bytes, 16)));
+      g->out.push_back(p);
+    }
+    g->in_bytes = want_in;
+    g->out_bytes = want_out;
+  }
+  g->spec = &k->spec;
+  ECL_CK(cudaMemsetAsync(g->ctrl, 0, 256, g->compute));
+  return ECL_OK;
+}
+
+int ecl_gpu_buffer(ecl_gpu* g, int is_output, uint32_t index, void** ptr) {
+  const auto& v = is_output ? g->out : g->in;
+  if (index >= v.size()) return fail(ECL_CONFIG_ERROR, "buffer index out of range");
+  *ptr = v[index];
+  return ECL_OK;
+}
+
+int ecl_gpu_swap_io(ecl_gpu* g, uint32_t i, uint32_t o) {
+  if (i >= g->in.size() || o >= g->out.size()) return fail(ECL_CONFIG_ERROR, "buffer index out of range");
+  if (g->in_bytes[i] != g->out_bytes[o]) return fail(ECL_CONFIG_ERROR, "swap_io needs equal buffer sizes");
+  std::swap(g->in[i], g->out[o]);
+  return ECL_OK;
+}
+
+int ecl_gpu_upload_inputs(ecl_gpu* g, const void* const* host_inputs) {
+  if (int rc = set_device(g)) return rc;
+  for (size_t i = 0; i < g->in.size(); ++i) {
+    if (!host_inputs || !host_inputs[i]) continue;
+    ECL_CK(cudaMemcpyAsync(g->in[i], host_inputs[i], g->in_bytes[i], cudaMemcpyHostToDevice, g->compute));
+  }
+  ECL_CK(cudaEventRecord(g->ready, g->compute));
+  return ECL_OK;
+}
+
+int ecl_replicate_inputs(ecl_gpu* const* gpus, uint32_t n, uint32_t root) {
+  if (root >= n) return fail(ECL_CONFIG_ERROR, "replicate: root out of range");
+  std::vector<ecl_gpu*> order;
+  order.push_back(gpus[root]);
+  for (uint32_t i = 0; i < n; ++i)
+    if (i != root) order.push_back(gpus[i]);
+  // Binary doubling: in round r the first 2^r holders each feed one more.
+  for (size_t have = 1; have < order.size(); have *= 2) {
+    for (size_t i = 0; i < have && have + i < order.size(); ++i) {
+      ecl_gpu* src = order[i];
+      ecl_gpu* dst = order[have + i];
+      if (src->in_bytes != dst->in_bytes) return fail(ECL_CONFIG_ERROR, "replicate: devices bound differently");
+      if (src->ordinal != dst->ordinal) {
+        cudaSetDevice(dst->ordinal);
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, dst->ordinal, src->ordinal);
+        if (can) {
+          cudaError_t e = cudaDeviceEnablePeerAccess(src->ordinal, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "EnablePeerAccess");
+          cudaGetLastError();
+        }
+      }
+      if (int rc = set_device(dst)) return rc;
+      ECL_CK(cudaStreamWaitEvent(dst->compute, src->ready, 0));
+      for (size_t b = 0; b < dst->in.size(); ++b)
+        ECL_CK(cudaMemcpyPeerAsync(dst->in[b], dst->ordinal, src->in[b], src->ordinal, dst->in_bytes[b],
+                                   dst->compute));
+      ECL_CK(cudaEventRecord(dst->ready, dst->compute));
+    }
+  }
+  return ECL_OK;
+}
+
+int ecl_broadcast_output_slice(ecl_gpu* const* gpus, uint32_t n, uint32_t src_i, uint32_t index,
+                               uint64_t elem_offset, uint64_t elem_count) {
+  if (src_i >= n) return fail(ECL_CONFIG_ERROR, "broadcast: source out of range");
+  ecl_gpu* src = gpus[src_i];
+  if (index >= src->out.size()) return fail(ECL_CONFIG_ERROR, "broadcast: output index out of range");
+  const uint64_t esz = src->spec->outputs[index].element_size_bytes;
+  if ((elem_offset + elem_count) * esz > src->out_bytes[index])
+    return fail(ECL_CONFIG_ERROR, "broadcast: slice out of range");
+  if (int rc = set_device(src)) return rc;
+  for (uint32_t d = 0; d < n; ++d) {
+    ecl_gpu* dst = gpus[d];
+    if (d == src_i || dst->out.size() <= index) continue;
+    char* to = static_cast<char*>(dst->out[index]) + elem_offset * esz;
+    const char* from = static_cast<const char*>(src->out[index]) + elem_offset * esz;
+    if (dst->ordinal == src->ordinal)
+      ECL_CK(cudaMemcpyAsync(to, from, elem_count * esz, cudaMemcpyDeviceToDevice, src->compute));
+    else
+      ECL_CK(cudaMemcpyPeerAsync(to, dst->ordinal, from, src->ordinal, elem_count * esz, src->compute));
+  }
+  ECL_CK(cudaEventRecord(src->ready, src->compute));
+  for (uint32_t d = 0; d < n; ++d) {
+    if (d == src_i) continue;
+    if (int rc = set_device(gpus[d])) return rc;
+    ECL_CK(cudaStreamWaitEvent(gpus[d]->compute, src->ready, 0));
+  }
+  return ECL_OK;
+}
+
+int ecl_gpu_download_slice(ecl_gpu* g, uint32_t index, uint64_t elem_offset, uint64_t elem_count, void* host) {
+  if (index >= g->out.size()) return fail(ECL_CONFIG_ERROR, "download: output index out of range");
+  const uint64_t esz = g->spec->outputs[index].element_size_bytes;
+  if ((elem_offset + elem_count) * esz > g->out_bytes[index])
+    return fail(ECL_CONFIG_ERROR, "download: slice out of range");
+  if (int rc = set_device(g)) return rc;
+  ECL_CK(cudaStreamSynchronize(g->compute));
+  ECL_CK(cudaMemcpyAsync(host, static_cast<const char*>(g->out[index]) + elem_offset * esz, elem_count * esz,
+                         cudaMemcpyDeviceToHost, g->copy));
+  ECL_CK(cudaStreamSynchronize(g->copy));
+  return ECL_OK;
+}
+
+int ecl_host_register(void* ptr, size_t bytes) {
+  cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterPortable);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) {
+    cudaGetLastError();
+    return ECL_OK;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaHostRegister");
+  return ECL_OK;
+}
+
+int ecl_host_unregister(void* ptr) {
+  cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess && e != cudaErrorHostMemoryNotRegistered) return cuda_fail(e, "cudaHostUnregister");
+  cudaGetLastError();
+  return ECL_OK;
+}
+
+int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_wg, void* const* host_outputs,
+                   ecl_done_fn done, void* user) {
+  if (!g->spec) return fail(ECL_CONFIG_ERROR, "submit before bind");
+  const ecl::KernelSpec& s = *g->spec;
+  if (size_wg == 0 || (offset_wg + size_wg) * s.lws > s.gws)
+    return fail(ECL_SCHEDULER_ERROR, "package outside the work-group range");
+  uint64_t o_off = 0, o_cnt = 0;
+  if (int rc = out_range(s, offset_wg, size_wg, &o_off, &o_cnt)) return rc;
+  if (int rc = set_device(g)) return rc;
+  if (find_slot(g, seq)) return fail(ECL_SCHEDULER_ERROR, "package seq submitted twice");
+  Slot& slot = g->slots[g->next_slot];
+  g->next_slot = (g->next_slot + 1) % (kSlots - 1);  // the last slot is reserved for native_run
+  if (slot.busy) ECL_CK(cudaEventSynchronize(slot.done));  // ring wrapped: oldest must be retired
+  slot.seq = seq;
+  slot.busy = true;
+  slot.timed = false;
+  slot.fn = done;
+  slot.user = user;
+
+  const uint64_t first = offset_wg * s.lws, count = size_wg * s.lws;
+  ECL_CK(cudaEventRecord(slot.start, g->compute));
+  cudaError_t e = ecl::launch_kernel(s, env_of(g), first, count);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  if (g->tally_on) {
+    e = ecl::launch_tally(g->tally, first, count, g->compute);
+    if (e != cudaSuccess) return cuda_fail(e, "tally launch");
+  }
+  ECL_CK(cudaEventRecord(slot.end, g->compute));
+
+  ECL_CK(cudaStreamWaitEvent(g->copy, slot.end, 0));
+  if (host_outputs) {
+    for (size_t b = 0; b < g->out.size(); ++b) {
+      if (!host_outputs[b]) continue;
+      const uint64_t esz = s.outputs[b].element_size_bytes;
+      ECL_CK(cudaMemcpyAsync(static_cast<char*>(host_outputs[b]) + o_off * esz,
+                             static_cast<const char*>(g->out[b]) + o_off * esz, o_cnt * esz,
+                             cudaMemcpyDeviceToHost, g->copy));
+    }
+  }
+  if (done) ECL_CK(cudaLaunchHostFunc(g->copy, on_package_done, &slot));
+  ECL_CK(cudaEventRecord(slot.done, g->copy));
+  return ECL_OK;
+}
+
+int ecl_gpu_poll(ecl_gpu* g, uint64_t seq) {
+  Slot* sp = find_slot(g, seq);
+  if (!sp) return fail(ECL_CONFIG_ERROR, "poll: unknown package");
+  Slot& slot = *sp;
+  cudaSetDevice(g->ordinal);
+  cudaError_t e = cudaEventQuery(slot.done);
+  if (e == cudaSuccess) return ECL_OK;
+  if (e == cudaErrorNotReady) {
+    cudaGetLastError();
+    return ECL_PENDING;
+  }
+  return cuda_fail(e, "package completion");
+}
+
+int ecl_gpu_package_times(ecl_gpu* g, uint64_t seq, double* t_start, double* t_end) {
+  Slot* sp = find_slot(g, seq);
+  if (!sp) return fail(ECL_CONFIG_ERROR, "package_times: unknown package");
+  Slot& slot = *sp;
+  if (int rc = set_device(g)) return rc;
+  ECL_CK(cudaEventSynchronize(slot.done));
+  float a = 0.f, b = 0.f, k = 0.f;
+  ECL_CK(cudaEventElapsedTime(&a, g->epoch, slot.start));
+  ECL_CK(cudaEventElapsedTime(&b, g->epoch, slot.end));
+  ECL_CK(cudaEventElapsedTime(&k, slot.start, slot.end));
+  *t_start = g->epoch_host_ms + a;
+  *t_end = g->epoch_host_ms + b;
+  if (!slot.timed) {
+    g->kernel_ms += k;
+    g->launches += 1;
+    slot.timed = true;
+  }
+  slot.busy = false;
+  return ECL_OK;
+}
+
+int ecl_gpu_set_epoch(ecl_gpu* g, double (*host_now_ms)(void*), void* clock_user) {
+  if (int rc = set_device(g)) return rc;
+  ECL_CK(cudaEventRecord(g->epoch, g->compute));
+  ECL_CK(cudaEventSynchronize(g->epoch));
+  g->epoch_host_ms = host_now_ms ? host_now_ms(clock_user) : 0.0;
+  return ECL_OK;
+}
+
+int ecl_gpu_sync(ecl_gpu* g) {
+  if (int rc = set_device(g)) return rc;
+  ECL_CK(cudaStreamSynchronize(g->compute));
+  ECL_CK(cudaStreamSynchronize(g->copy));
+  return ECL_OK;
+}
+
+int ecl_gpu_enable_tally(ecl_gpu* g, int enable) {
+  if (int rc = set_device(g)) return rc;
+  g->tally_on = enable != 0;
+  if (!g->tally_on) return ECL_OK;
+  if (!g->spec) return fail(ECL_CONFIG_ERROR, "tally before bind");
+  if (g->tally_items != g->spec->gws) {
+    if (g->tally) cudaFree(g->tally);
+    g->tally = nullptr;
+    ECL_CK(cudaMalloc(&g->tally, g->spec->gws * sizeof(uint32_t)));
+    g->tally_items = g->spec->gws;
+  }
+  ECL_CK(cudaMemsetAsync(g->tally, 0, g->tally_items * sizeof(uint32_t), g->compute));
+  return ECL_OK;
+}
+
+int ecl_gpu_download_tally(ecl_gpu* g, uint32_t* host) {
+  if (!g->tally) return fail(ECL_CONFIG_ERROR, "tally not enabled");
+  if (int rc = set_device(g)) return rc;
+  ECL_CK(cudaStreamSynchronize(g->compute));
+  ECL_CK(cudaMemcpy(host, g->tally, g->tally_items * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return ECL_OK;
+}
+
+int ecl_gpu_native_run(ecl_gpu* g, float* kernel_ms) {
+  if (!g->spec) return fail(ECL_CONFIG_ERROR, "native run before bind");
+  if (int rc = set_device(g)) return rc;
+  Slot& slot = g->slots[kSlots - 1];
+  if (slot.busy) ECL_CK(cudaEventSynchronize(slot.done));
+  ECL_CK(cudaEventRecord(slot.start, g->compute));
+  cudaError_t e = ecl::launch_kernel(*g->spec, env_of(g), 0, g->spec->gws);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  ECL_CK(cudaEventRecord(slot.end, g->compute));
+  ECL_CK(cudaEventSynchronize(slot.end));
+  float ms = 0.f;
+  ECL_CK(cudaEventElapsedTime(&ms, slot.start, slot.end));
+  *kernel_ms = ms;
+  g->kernel_ms += ms;
+  g->launches += 1;
+  return ECL_OK;
+}
+
+int ecl_gpu_kernel_time(ecl_gpu* g, double* total_ms, uint64_t* launches, int reset) {
+  *total_ms = g->kernel_ms;
+  *launches = g->launches;
+  if (reset) {
+    g->kernel_ms = 0.0;
+    g->launches = 0;
+  }
+  return ECL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// kernels.cuh — the sm_100a kernel registry shared by the device layer.
+//
+// Every kernel is a pure function of (global work-item index, args, read-only
+// inputs) that writes only the out_range_for slice of the items it is given —
+// the contract of the reference's KernelFn (workloads.hpp:42-44) — launched
+// over one package [first_item, first_item + item_count).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "ecl_cuda.h"
+
+namespace ecl {
+
+enum class KernelKind { VecScale, Mandelbrot, MandelbrotF32, Synthetic, Gaussian, NBody, Binomial, Ray };
+
+enum class SyntheticProfile { Constant = 0, Ramp = 1, Step = 2 };
+
+// Mandelbrot args [W, H, max_iter, x0, y0, x1, y1] (workloads.hpp:102-120).
+struct MandelParams {
+  uint64_t width = 0, height = 0;
+  uint32_t max_iterations = 1;
+  double x0 = -2.5, y0 = -1.25, x1 = 1.0, y1 = 1.25;
+};
+
+struct GaussianParams {
+  uint32_t width = 0, height = 0, filter = 0;
+};
+
+struct NBodyParams {
+  uint64_t bodies = 0;
+  float dt = 0.005f, eps2 = 500.0f;
+};
+
+struct BinomialParams {
+  uint32_t steps = 254;
+  uint64_t options = 0;  // scalar options (4 per work-group)
+};
+
+struct RayParams {
+  uint32_t width = 0, height = 0, spheres = 0, max_depth = 0;
+};
+
+// Resolved kernel: the device-independent half of ecl_kernel.
+struct KernelSpec {
+  KernelKind kind = KernelKind::VecScale;
+  SyntheticProfile profile = SyntheticProfile::Constant;
+  std::string id;
+  uint64_t gws = 0, lws = 1, out_indices = 1, out_work_items = 1;
+  std::vector<ecl_arg> args;
+  std::vector<ecl_buffer_geom> inputs, outputs;
+  // parsed arguments
+  MandelParams mandel;
+  double a = 0.0, b = 0.0;  // vecscale
+  double synth_param = 1.0;
+  bool synth_has_param = false;
+  GaussianParams gauss;
+  NBodyParams nbody;
+  BinomialParams binom;
+  RayParams ray;
+};
+
+// Everything a launcher needs from the device context.
+struct LaunchEnv {
+  cudaStream_t stream = nullptr;
+  int sms = 148;
+  void* const* in = nullptr;   // device pointers of the bound inputs
+  void* const* out = nullptr;  // device pointers of the bound outputs
+  unsigned* ctrl = nullptr;    // zeroed per-device control words (work counters)
+};
+
+// Parses and validates (kernel_for + check_buffer_shapes semantics).
+// Returns ECL_OK or a negative status with *err filled.
+int resolve_kernel(KernelSpec& spec, std::string* err);
+
+// Launches the kernel over work-items [first, first + count) on env.stream.
+cudaError_t launch_kernel(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
+
+// Per-kind launchers (one translation unit each).
+cudaError_t launch_mandelbrot(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
+cudaError_t launch_vecscale(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
+cudaError_t launch_synthetic(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
+cudaError_t launch_gaussian(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
+cudaError_t launch_nbody(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
+cudaError_t launch_binomial(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
+cudaError_t launch_ray(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
+
+// Exactly-once tally: tally[i] += 1 for i in [first, first + count).
+cudaError_t launch_tally(uint32_t* tally, uint64_t first, uint64_t count, cudaStream_t stream);
+
+}  // namespace ecl

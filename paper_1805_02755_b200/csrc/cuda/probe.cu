@@ -1,0 +1,80 @@
+// probe.cu — measured FP64/FP32 vector peaks for the roofline denominators.
+//
+// MEASURED_PEAKS.json carries HBM and bf16 tensor peaks only; the
+// Mandelbrot/NBody/Binomial kernels are bound by the FP64/FP32 vector pipes,
+// so bench.py measures those here on the same device it times: independent
+// FMA chains (8 per thread, full occupancy) for FLOP/s, and DADD chains for
+// the non-fused FP64 instruction rate.
+#include "ecl_cuda.h"
+#include "kernels.cuh"
+
+namespace {
+
+template <int MODE>  // 0 = DFMA, 1 = DADD, 2 = FFMA
+__global__ void __launch_bounds__(256) pipe_chain(double* sink, int iters) {
+  double d[8];
+  float f[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    d[k] = threadIdx.x * 1e-9 + k;
+    f[k] = threadIdx.x * 1e-6f + k;
+  }
+  const double a = 0.999999, b = 1e-7;
+  const float af = 0.999999f, bf = 1e-7f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (MODE == 0) d[k] = __fma_rn(d[k], a, b);
+        else if (MODE == 1) d[k] = __dadd_rn(d[k], b);
+        else f[k] = __fmaf_rn(f[k], af, bf);
+      }
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += d[k] + f[k];
+  if (s == 12345.678) sink[0] = s;  // keep the chains live
+}
+
+template <int MODE>
+float time_chain(int sms, int iters, cudaStream_t st, double* sink) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0, st);
+    pipe_chain<MODE><<<sms * 8, 256, 0, st>>>(sink, iters);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0 && ms < best) best = ms;  // first launch is warm-up
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return best;
+}
+
+}  // namespace
+
+extern "C" int ecl_probe_vector_peaks(int ordinal, double* fp64_fma_tflops, double* fp64_add_tinstr,
+                                      double* fp32_fma_tflops) {
+  if (cudaSetDevice(ordinal) != cudaSuccess) return ECL_CONFIG_ERROR;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ordinal);
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  double* sink = nullptr;
+  cudaMalloc(&sink, 64);
+  const int iters = 2048;
+  const double ops = double(sms) * 8 * 256 * iters * 64;
+  *fp64_fma_tflops = 2.0 * ops / (time_chain<0>(sms, iters, st, sink) * 1e-3) / 1e12;
+  *fp64_add_tinstr = ops / (time_chain<1>(sms, iters, st, sink) * 1e-3) / 1e12;
+  *fp32_fma_tflops = 2.0 * ops / (time_chain<2>(sms, iters, st, sink) * 1e-3) / 1e12;
+  cudaFree(sink);
+  cudaStreamDestroy(st);
+  return cudaGetLastError() == cudaSuccess ? ECL_OK : ECL_KERNEL_PANIC;
+}

@@ -1,0 +1,600 @@
+// engine.cpp — coexec::Engine over the B200 device layer (include/ecl_cuda.h).
+//
+// Wall mode (the hot path).  Reference: drive_wall (engine.hpp:354-405)
+// spawns one std::thread per device per run; each locks the coordinator,
+// asks the scheduler for a package, runs it on a NativePool and records
+// timestamps.  Here the device threads are created once with the engine
+// (the paper's initialization optimization) and each keeps up
+// to queue_depth packages in flight on its GPU: package k+1 is submitted
+// before package k ends, so the per-package dispatch (scheduler call +
+// kernel launch + event records) hides under the running kernel.
+// Completion is event driven: the device layer's host callback marks the
+// package done and wakes the owning thread.
+//
+// Virtual mode.  The discrete-event replay of drive_virtual
+// (engine.hpp:306-338) with the same cost model (simulate_package_ms,
+// :37-58) and tie-break (time, device, seq) (:60-90); costs come from the
+// caller, so the product never evaluates kernels on the CPU.
+#include "coexec/engine.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstdlib>
+#include <cstring>
+#include <deque>
+#include <mutex>
+#include <optional>
+#include <queue>
+#include <set>
+#include <string>
+#include <thread>
+
+#include "ecl_cuda.h"
+
+namespace coexec {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+[[noreturn]] void throw_status(int status, const std::string& what) {
+  throw Error(code_of_status(status), what + ": " + ecl_last_error());
+}
+
+void check(int status, const std::string& what) {
+  if (status != ECL_OK) throw_status(status, what);
+}
+
+bool tally_from_env() {
+  const char* v = std::getenv("COEXEC_TALLY");
+  return v && std::string_view(v) == "1";
+}
+
+struct RunState;
+
+struct Device {
+  std::uint32_t index = 0;
+  ecl_gpu* gpu = nullptr;
+  std::uint32_t depth = 2;
+  std::thread thread;
+  // completion mailbox, written by the CUDA callback thread
+  std::mutex mailbox_m;
+  std::condition_variable mailbox_cv;
+  std::set<std::uint64_t> finished;
+};
+
+void on_done(void* user, std::uint64_t seq, int /*status*/) {
+  auto* d = static_cast<Device*>(user);
+  {
+    std::lock_guard lock(d->mailbox_m);
+    d->finished.insert(seq);
+  }
+  d->mailbox_cv.notify_one();
+}
+
+struct RunState {
+  Scheduler* scheduler = nullptr;
+  std::mutex coordinator;  // serializes scheduler access and seq (engine.hpp:357,370)
+  std::uint64_t next_seq = 0;
+  std::vector<void*> host_out;  // empty = device-resident
+  std::mutex completion;
+  std::vector<Package> completed;
+  std::vector<Error> errors;
+  std::atomic<bool> abort{false};
+};
+
+}  // namespace
+
+struct Engine::Impl {
+  EngineConfig cfg;
+  ValidatedProgram prog;
+  Clock::time_point epoch;  // reset at the start of every run
+  double init_ms = 0.0;
+  bool init_charged = false;
+  ecl_kernel* kernel = nullptr;
+  std::vector<std::unique_ptr<Device>> devices;
+  ExecutionTrace last;
+  std::vector<Package> last_packages;  // packages of the last wall run (for gather)
+  bool last_resident = false;
+
+  // device-thread run protocol
+  std::mutex run_m;
+  std::condition_variable run_cv, idle_cv;
+  std::uint64_t generation = 0;
+  std::uint32_t busy = 0;
+  bool stop = false;
+  RunState* current = nullptr;
+
+  Impl(EngineConfig c, ValidatedProgram p) : cfg(std::move(c)), prog(std::move(p)) {}
+
+  double now_ms() const { return std::chrono::duration<double, std::milli>(Clock::now() - epoch).count(); }
+  static double clock_cb(void* self) { return static_cast<Impl*>(self)->now_ms(); }
+
+  bool wall() const { return cfg.clock_mode == ClockMode::Wall; }
+
+  void validate_config() const {
+    if (cfg.devices.empty()) throw Error(ErrorCode::ConfigError, "engine needs at least one device");
+    for (std::size_t i = 0; i < cfg.devices.size(); ++i) {
+      const DeviceProfile& d = cfg.devices[i];
+      validate_device(d);
+      for (std::size_t j = i + 1; j < cfg.devices.size(); ++j)
+        if (cfg.devices[j].id == d.id) throw Error(ErrorCode::ConfigError, "duplicate device id '" + d.id + "'");
+      const bool sim = d.backend.kind == BackendKind::Simulated;
+      if (!wall() && !sim) throw Error(ErrorCode::ConfigError, "virtual clock mode requires simulated backends");
+      if (wall() && sim) throw Error(ErrorCode::ConfigError, "wall clock mode requires cuda backends");
+    }
+  }
+
+  void make_kernel() {
+    const ProgramSpec& s = prog.spec();
+    std::vector<ecl_arg> args;
+    for (const ArgValue& a : s.args) {
+      ecl_arg x{};
+      if (const auto* i = std::get_if<std::int64_t>(&a)) x.i = *i;
+      else {
+        x.is_double = 1;
+        x.d = std::get<double>(a);
+      }
+      args.push_back(x);
+    }
+    std::vector<ecl_buffer_geom> ins, outs;
+    for (const BufferDesc& b : s.in_buffers) ins.push_back({b.element_size_bytes, b.element_count});
+    for (const BufferDesc& b : s.out_buffers) outs.push_back({b.element_size_bytes, b.element_count});
+    check(ecl_kernel_create(s.kernel.c_str(), s.global_work_size, s.local_work_size, args.data(),
+                            static_cast<std::uint32_t>(args.size()), ins.data(), static_cast<std::uint32_t>(ins.size()),
+                            outs.data(), static_cast<std::uint32_t>(outs.size()), s.out_pattern.out_indices,
+                            s.out_pattern.work_items, &kernel),
+          "kernel '" + s.kernel + "'");
+  }
+
+  void open_devices() {
+    for (std::uint32_t i = 0; i < cfg.devices.size(); ++i) {
+      auto d = std::make_unique<Device>();
+      d->index = i;
+      d->depth = cfg.devices[i].backend.queue_depth;
+      check(ecl_gpu_open(cfg.devices[i].backend.ordinal, d->depth, &d->gpu), "device '" + cfg.devices[i].id + "'");
+      devices.push_back(std::move(d));
+      check(ecl_gpu_bind(devices.back()->gpu, kernel), "bind '" + cfg.devices[i].id + "'");
+    }
+    for (auto& d : devices) d->thread = std::thread([this, dev = d.get()] { device_loop(*dev); });
+  }
+
+  void shutdown() {
+    {
+      std::lock_guard lock(run_m);
+      stop = true;
+    }
+    run_cv.notify_all();
+    for (auto& d : devices)
+      if (d->thread.joinable()) d->thread.join();
+    for (auto& d : devices) ecl_gpu_close(d->gpu);
+    devices.clear();
+    if (kernel) ecl_kernel_destroy(kernel);
+    kernel = nullptr;
+  }
+
+  // ---- wall mode ---------------------------------------------------------
+
+  void device_loop(Device& dev) {
+    std::uint64_t seen = 0;
+    for (;;) {
+      RunState* rs;
+      {
+        std::unique_lock lock(run_m);
+        run_cv.wait(lock, [&] { return stop || generation != seen; });
+        if (stop) return;
+        seen = generation;
+        rs = current;
+      }
+      drive(dev, *rs);
+      {
+        std::lock_guard lock(run_m);
+        if (--busy == 0) idle_cv.notify_all();
+      }
+    }
+  }
+
+  void fail(RunState& rs, Error e) {
+    std::lock_guard lock(rs.completion);
+    rs.errors.push_back(std::move(e));
+    rs.abort.store(true);
+  }
+
+  // Waits for package `seq`; false on a device fault (already recorded).
+  bool await(Device& dev, RunState& rs, std::uint64_t seq) {
+    std::unique_lock lock(dev.mailbox_m);
+    while (!dev.finished.count(seq)) {
+      if (dev.mailbox_cv.wait_for(lock, std::chrono::milliseconds(50)) == std::cv_status::timeout) {
+        lock.unlock();
+        const int rc = ecl_gpu_poll(dev.gpu, seq);
+        lock.lock();
+        if (rc == ECL_OK) break;
+        if (rc != ECL_PENDING) {
+          lock.unlock();
+          fail(rs, Error(code_of_status(rc), std::string("device '") + cfg.devices[dev.index].id + "': " + ecl_last_error()));
+          return false;
+        }
+      }
+    }
+    dev.finished.erase(seq);
+    return true;
+  }
+
+  void drive(Device& dev, RunState& rs) {
+    const DeviceProfile& profile = cfg.devices[dev.index];
+    {
+      std::lock_guard lock(dev.mailbox_m);
+      dev.finished.clear();  // seqs restart at 0 every run
+    }
+    std::deque<Package> inflight;
+    bool drained = false;
+    void* const* host_out = rs.host_out.empty() ? nullptr : rs.host_out.data();
+
+    auto pull = [&]() -> bool {
+      std::optional<PackageRange> range;
+      Package pkg;
+      {
+        std::lock_guard lock(rs.coordinator);
+        if (rs.abort.load()) return false;
+        range = rs.scheduler->next(dev.index);
+        if (!range) return false;
+        pkg.seq = rs.next_seq++;
+        pkg.t_enqueue_ms = now_ms();
+      }
+      pkg.device_index = dev.index;
+      pkg.device_id = profile.id;
+      pkg.offset_wg = range->offset_wg;
+      pkg.size_wg = range->size_wg;
+      pkg.t_start_ms = pkg.t_enqueue_ms;
+      if (profile.launch_overhead_ms > 0.0)
+        std::this_thread::sleep_for(std::chrono::duration<double, std::milli>(profile.launch_overhead_ms));
+      const int rc = ecl_gpu_submit(dev.gpu, pkg.seq, pkg.offset_wg, pkg.size_wg, host_out, on_done, &dev);
+      if (rc != ECL_OK) {
+        fail(rs, Error(code_of_status(rc), std::string("device '") + profile.id + "': " + ecl_last_error()));
+        return false;
+      }
+      inflight.push_back(std::move(pkg));
+      return true;
+    };
+
+    for (;;) {
+      while (!drained && inflight.size() < dev.depth) {
+        if (!pull()) drained = true;
+      }
+      if (inflight.empty()) break;
+      Package pkg = std::move(inflight.front());
+      inflight.pop_front();
+      if (!await(dev, rs, pkg.seq)) {
+        drained = true;
+        continue;
+      }
+      double t0 = 0.0, t1 = 0.0;
+      const int rc = ecl_gpu_package_times(dev.gpu, pkg.seq, &t0, &t1);
+      if (rc != ECL_OK) {
+        fail(rs, Error(code_of_status(rc), ecl_last_error()));
+        drained = true;
+        continue;
+      }
+      pkg.t_start_ms = t0;
+      pkg.t_end_ms = t1;
+      {
+        std::lock_guard lock(rs.coordinator);
+        rs.scheduler->observe(dev.index, pkg.size_wg * prog.local_work_size(), t1 - t0);
+      }
+      std::lock_guard lock(rs.completion);
+      rs.completed.push_back(std::move(pkg));
+    }
+  }
+
+  ExecutionTrace run_wall(std::span<const void* const> inputs, std::span<void* const> outputs) {
+    const ProgramSpec& s = prog.spec();
+    if (inputs.size() != s.in_buffers.size())
+      throw Error(ErrorCode::InputSizeMismatch, "expected " + std::to_string(s.in_buffers.size()) +
+                                                    " input buffers, got " + std::to_string(inputs.size()));
+    for (std::size_t i = 0; i < inputs.size(); ++i)
+      if (!inputs[i]) throw Error(ErrorCode::InputSizeMismatch, "input '" + s.in_buffers[i].name + "' is null");
+    bool resident = true;
+    for (void* p : outputs) resident = resident && p == nullptr;
+    if (!outputs.empty() && outputs.size() != s.out_buffers.size())
+      throw Error(ErrorCode::ConfigError, "expected " + std::to_string(s.out_buffers.size()) + " output buffers");
+
+    epoch = Clock::now();
+    const bool tally = cfg.tally || tally_from_env();
+    std::vector<ecl_gpu*> gpus;
+    for (auto& d : devices) gpus.push_back(d->gpu);
+    for (auto& d : devices) {
+      check(ecl_gpu_enable_tally(d->gpu, tally ? 1 : 0), "tally");
+      check(ecl_gpu_set_epoch(d->gpu, &Impl::clock_cb, this), "epoch");
+    }
+    if (!inputs.empty()) {
+      // One H2D into the first device, then an NVLink doubling tree.
+      check(ecl_gpu_upload_inputs(gpus[0], const_cast<const void* const*>(inputs.data())), "upload");
+      if (gpus.size() > 1)
+        check(ecl_replicate_inputs(gpus.data(), static_cast<std::uint32_t>(gpus.size()), 0), "replicate");
+    }
+
+    auto scheduler = make_scheduler(cfg.scheduler, prog.total_work_groups(), cfg.devices);
+    RunState rs;
+    rs.scheduler = scheduler.get();
+    if (!resident) rs.host_out.assign(outputs.begin(), outputs.end());
+    {
+      std::lock_guard lock(run_m);
+      current = &rs;
+      busy = static_cast<std::uint32_t>(devices.size());
+      ++generation;
+    }
+    run_cv.notify_all();
+    {
+      std::unique_lock lock(run_m);
+      idle_cv.wait(lock, [&] { return busy == 0; });
+      current = nullptr;
+    }
+
+    std::sort(rs.completed.begin(), rs.completed.end(), [](const Package& a, const Package& b) { return a.seq < b.seq; });
+    std::vector<Error> errors = std::move(rs.errors);
+    if (errors.empty()) {
+      if (!tiles_exactly(rs.completed, prog.total_work_groups()))
+        errors.emplace_back(ErrorCode::SchedulerError, "packages do not tile the work-group range exactly once");
+      if (tally) check_tally(errors);
+    }
+    if (!errors.empty()) throw EngineFailure(std::move(errors));
+    last_resident = resident;
+    last_packages = rs.completed;
+    ExecutionTrace t = assemble(std::move(rs.completed));
+    last = t;
+    return t;
+  }
+
+  void check_tally(std::vector<Error>& errors) {
+    const std::uint64_t n = prog.global_work_size();
+    std::vector<std::uint32_t> sum(n, 0), part(n);
+    for (auto& d : devices) {
+      check(ecl_gpu_download_tally(d->gpu, part.data()), "tally download");
+      for (std::uint64_t i = 0; i < n; ++i) sum[i] += part[i];
+    }
+    for (std::uint64_t i = 0; i < n; ++i)
+      if (sum[i] != 1) {
+        errors.emplace_back(ErrorCode::TallyViolation,
+                            "work-item " + std::to_string(i) + " executed " + std::to_string(sum[i]) + " times");
+        return;
+      }
+  }
+
+  ExecutionTrace assemble(std::vector<Package> completed) {
+    ExecutionTrace t;
+    t.program = summarize(prog);
+    t.devices = cfg.devices;
+    t.scheduler = describe(cfg.scheduler);
+    t.clock_mode = cfg.clock_mode;
+    t.seed = cfg.seed;
+    t.init_ms = wall() ? init_ms : 0.0;
+    t.init_in_total = !cfg.exclude_init_from_total;
+    double last_end = 0.0;
+    std::map<std::string, std::pair<double, double>> spans;
+    for (const Package& p : completed) {
+      last_end = std::max(last_end, p.t_end_ms);
+      auto [it, fresh] = spans.try_emplace(p.device_id, p.t_enqueue_ms, p.t_end_ms);
+      if (!fresh) {
+        it->second.first = std::min(it->second.first, p.t_enqueue_ms);
+        it->second.second = std::max(it->second.second, p.t_end_ms);
+      }
+    }
+    for (const auto& [id, sp] : spans) t.per_device_time_ms[id] = sp.second - sp.first;
+    // Timestamps are relative to the run's start; engine construction (init)
+    // is charged once, to the first run, unless excluded.
+    double total = last_end;
+    if (wall() && t.init_in_total && !init_charged) total += init_ms;
+    if (wall()) init_charged = true;
+    t.t_total_ms = total;
+    t.packages = std::move(completed);
+    return t;
+  }
+
+  // ---- virtual mode ------------------------------------------------------
+
+  ExecutionTrace run_virtual(std::span<const double> item_costs) {
+    if (wall()) throw Error(ErrorCode::ConfigError, "run_virtual needs clock_mode virtual");
+    const ProgramSpec& s = prog.spec();
+    const std::uint64_t gws = prog.global_work_size(), lws = prog.local_work_size();
+    std::vector<double> analytic;
+    if (item_costs.empty()) {
+      analytic.assign(gws, 1.0);
+      if (s.kernel.rfind("synthetic", 0) == 0) {
+        const std::string prof = s.kernel == "synthetic" ? "constant" : s.kernel.substr(10);
+        const bool has = !s.args.empty();
+        const double param = has ? std::visit([](auto v) { return static_cast<double>(v); }, s.args[0]) : 0.0;
+        for (std::uint64_t i = 0; i < gws; ++i) {
+          if (prof == "constant") analytic[i] = has ? param : 1.0;
+          else if (prof == "ramp") analytic[i] = 1.0 + static_cast<double>(i) / static_cast<double>(gws);
+          else if (prof == "step") analytic[i] = i < gws / 2 ? 1.0 : (has ? param : 10.0);
+          else throw Error(ErrorCode::UnknownProfile, "no synthetic cost profile named '" + prof + "'");
+        }
+      } else if (s.kernel != "vecscale") {
+        throw Error(ErrorCode::BadKernelArgs, "run_virtual: kernel '" + s.kernel + "' needs per-item costs");
+      }
+      item_costs = analytic;
+    }
+    if (item_costs.size() != gws) throw Error(ErrorCode::InputSizeMismatch, "one cost per work-item expected");
+
+    auto duration = [&](const DeviceProfile& dev, const Package& pkg) {
+      const std::uint64_t first = pkg.offset_wg * lws, count = pkg.size_wg * lws;
+      double work = 0.0;
+      for (std::uint64_t i = first; i < first + count; ++i) work += item_costs[i];
+      const double share = static_cast<double>(count) / static_cast<double>(gws);
+      double in_bytes = 0.0, out_bytes = 0.0;
+      for (const BufferDesc& b : s.in_buffers) in_bytes += static_cast<double>(b.size_bytes()) * share;
+      const OutRange r = out_range_for(pkg, prog);
+      for (const BufferDesc& b : s.out_buffers) out_bytes += static_cast<double>(r.count * b.element_size_bytes);
+      return dev.launch_overhead_ms + in_bytes / dev.bandwidth_bytes_per_ms + work / dev.computing_power +
+             out_bytes / dev.bandwidth_bytes_per_ms;
+    };
+
+    struct Event {
+      double t;
+      std::uint32_t dev;
+      std::uint64_t seq;
+      bool operator>(const Event& o) const {
+        if (t != o.t) return t > o.t;
+        if (dev != o.dev) return dev > o.dev;
+        return seq > o.seq;
+      }
+    };
+    auto scheduler = make_scheduler(cfg.scheduler, prog.total_work_groups(), cfg.devices);
+    std::priority_queue<Event, std::vector<Event>, std::greater<Event>> events;
+    std::vector<Package> inflight(cfg.devices.size()), completed;
+    double clock = 0.0;
+    std::uint64_t seq = 0;
+    auto request = [&](std::uint32_t d) {
+      const auto range = scheduler->next(d);
+      if (!range) return;
+      Package p;
+      p.seq = seq++;
+      p.device_index = d;
+      p.device_id = cfg.devices[d].id;
+      p.offset_wg = range->offset_wg;
+      p.size_wg = range->size_wg;
+      p.t_enqueue_ms = p.t_start_ms = clock;
+      events.push(Event{clock + duration(cfg.devices[d], p), d, p.seq});
+      inflight[d] = std::move(p);
+    };
+    for (std::uint32_t d = 0; d < cfg.devices.size(); ++d) request(d);
+    while (!events.empty()) {
+      const Event e = events.top();
+      events.pop();
+      clock = e.t;
+      Package p = std::move(inflight[e.dev]);
+      p.t_end_ms = e.t;
+      completed.push_back(std::move(p));
+      request(e.dev);
+    }
+    if (scheduler->remaining_work_groups() != 0)
+      throw Error(ErrorCode::EmptyQueueWithPendingWork,
+                  std::to_string(scheduler->remaining_work_groups()) + " work-groups were never dispatched");
+    std::sort(completed.begin(), completed.end(), [](const Package& a, const Package& b) { return a.seq < b.seq; });
+    if (!tiles_exactly(completed, prog.total_work_groups()))
+      throw EngineFailure({Error(ErrorCode::SchedulerError, "packages do not tile the work-group range exactly once")});
+    ExecutionTrace t = assemble(std::move(completed));
+    last = t;
+    return t;
+  }
+
+  // ---- gather / native ----------------------------------------------------
+
+  void gather(std::span<void* const> outputs) {
+    const ProgramSpec& s = prog.spec();
+    if (outputs.size() != s.out_buffers.size()) throw Error(ErrorCode::ConfigError, "gather: output count mismatch");
+    for (const Package& p : last_packages) {
+      const OutRange r = out_range_for(p, prog);
+      for (std::uint32_t b = 0; b < outputs.size(); ++b) {
+        if (!outputs[b]) continue;
+        char* dst = static_cast<char*>(outputs[b]) + r.offset * s.out_buffers[b].element_size_bytes;
+        check(ecl_gpu_download_slice(devices[p.device_index]->gpu, b, r.offset, r.count, dst), "gather");
+      }
+    }
+  }
+
+  NativeResult native_run(std::span<const void* const> inputs, std::span<void* const> outputs) {
+    if (!wall()) throw Error(ErrorCode::ConfigError, "native_run needs cuda devices");
+    const ProgramSpec& s = prog.spec();
+    if (inputs.size() != s.in_buffers.size()) throw Error(ErrorCode::InputSizeMismatch, "native_run: input count");
+    ecl_gpu* g = devices[0]->gpu;
+    check(ecl_gpu_sync(g), "sync");
+    const auto t0 = Clock::now();
+    if (!inputs.empty()) check(ecl_gpu_upload_inputs(g, const_cast<const void* const*>(inputs.data())), "upload");
+    float kms = 0.f;
+    check(ecl_gpu_native_run(g, &kms), "native run");
+    for (std::uint32_t b = 0; b < outputs.size(); ++b)
+      if (outputs[b]) check(ecl_gpu_download_slice(g, b, 0, s.out_buffers[b].element_count, outputs[b]), "download");
+    NativeResult r;
+    r.kernel_ms = kms;
+    r.total_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+    return r;
+  }
+};
+
+Engine::Engine(EngineConfig cfg, ValidatedProgram prog) : impl_(std::make_unique<Impl>(std::move(cfg), std::move(prog))) {
+  const auto t0 = Clock::now();
+  impl_->epoch = t0;
+  impl_->validate_config();
+  if (impl_->wall()) {
+    try {
+      impl_->make_kernel();
+      impl_->open_devices();
+    } catch (...) {
+      impl_->shutdown();
+      throw;
+    }
+    impl_->init_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+  }
+}
+
+Engine::~Engine() {
+  if (impl_) impl_->shutdown();
+}
+
+RunResult Engine::run(std::span<const std::vector<std::byte>> inputs) {
+  const ProgramSpec& s = impl_->prog.spec();
+  if (inputs.size() != s.in_buffers.size())
+    throw Error(ErrorCode::InputSizeMismatch,
+                "expected " + std::to_string(s.in_buffers.size()) + " input buffers, got " + std::to_string(inputs.size()));
+  for (std::size_t i = 0; i < inputs.size(); ++i)
+    if (inputs[i].size() != s.in_buffers[i].size_bytes())
+      throw Error(ErrorCode::InputSizeMismatch, "input '" + s.in_buffers[i].name + "' is " +
+                                                    std::to_string(inputs[i].size()) + " bytes, descriptor says " +
+                                                    std::to_string(s.in_buffers[i].size_bytes()));
+  RunResult r;
+  for (const BufferDesc& b : s.out_buffers) r.outputs.emplace_back(b.size_bytes());
+  if (!impl_->wall()) {
+    r.trace = run_virtual({});
+    return r;
+  }
+  std::vector<const void*> in;
+  for (const auto& v : inputs) in.push_back(v.data());
+  std::vector<void*> out;
+  for (auto& v : r.outputs) {
+    out.push_back(v.data());
+    ecl_host_register(v.data(), v.size());
+  }
+  try {
+    r.trace = run_into(in, out);
+  } catch (...) {
+    for (void* p : out) ecl_host_unregister(p);
+    throw;
+  }
+  for (void* p : out) ecl_host_unregister(p);
+  return r;
+}
+
+ExecutionTrace Engine::run_into(std::span<const void* const> inputs, std::span<void* const> outputs) {
+  if (!impl_->wall()) throw Error(ErrorCode::ConfigError, "run_into needs clock_mode wall");
+  return impl_->run_wall(inputs, outputs);
+}
+
+ExecutionTrace Engine::run_virtual(std::span<const double> item_costs) { return impl_->run_virtual(item_costs); }
+
+void Engine::gather(std::span<void* const> outputs) { impl_->gather(outputs); }
+
+NativeResult Engine::native_run(std::span<const void* const> inputs, std::span<void* const> outputs) {
+  return impl_->native_run(inputs, outputs);
+}
+
+KernelTiming Engine::kernel_timing(bool reset) {
+  KernelTiming t;
+  for (auto& d : impl_->devices) {
+    double ms = 0.0;
+    std::uint64_t n = 0;
+    ecl_gpu_kernel_time(d->gpu, &ms, &n, reset ? 1 : 0);
+    t.kernel_ms += ms;
+    t.launches += n;
+  }
+  return t;
+}
+
+const ExecutionTrace& Engine::last_trace() const { return impl_->last; }
+double Engine::init_ms() const { return impl_->init_ms; }
+const ValidatedProgram& Engine::program() const { return impl_->prog; }
+const EngineConfig& Engine::config() const { return impl_->cfg; }
+
+}  // namespace coexec
