@@ -151,6 +151,11 @@ int ecl_gpu_download_tally(ecl_gpu* gpu, uint32_t* host_counts);
  * CUDA-event time of that launch.  Synchronous. */
 int ecl_gpu_native_run(ecl_gpu* gpu, float* kernel_ms);
 
+/* Work-items per sub-launch when a package copies to host buffers (default
+ * 2^23; 0 = one launch per package): bounds how much compute precedes the
+ * first D2H of a package. */
+int ecl_gpu_set_copy_split(ecl_gpu* gpu, uint64_t items);
+
 /* Kernel time of the most recent submit() / native_run() launches summed
  * since the last reset (for roofline accounting). */
 int ecl_gpu_kernel_time(ecl_gpu* gpu, double* total_ms, uint64_t* launches, int reset);

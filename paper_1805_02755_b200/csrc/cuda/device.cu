@@ -71,6 +71,7 @@ struct ecl_gpu {
   cudaStream_t copy = nullptr;
   cudaEvent_t epoch = nullptr;
   cudaEvent_t ready = nullptr;  // last input/replication write on this device
+  cudaEvent_t piece = nullptr;  // end of a sub-launch whose slice the copy stream drains
   double epoch_host_ms = 0.0;
   Slot slots[kSlots];
   const ecl::KernelSpec* spec = nullptr;
@@ -83,6 +84,10 @@ struct ecl_gpu {
   double kernel_ms = 0.0;
   uint64_t launches = 0;
   uint32_t next_slot = 0;  // per-device rotation: seqs are global across devices
+  void* scratch = nullptr;
+  uint64_t scratch_cap = 0;
+  bool scratch_ready = false;
+  uint64_t d2h_split_items = 1ull << 23;  // sub-launch size when copies are pipelined
 };
 
 namespace {
@@ -105,6 +110,8 @@ ecl::LaunchEnv env_of(const ecl_gpu* g) {
   env.in = g->in.data();
   env.out = g->out.data();
   env.ctrl = g->ctrl;
+  env.scratch = g->scratch;
+  env.scratch_ready = const_cast<bool*>(&g->scratch_ready);
   return env;
 }
 
@@ -170,6 +177,8 @@ int ecl_gpu_open(int ordinal, uint32_t queue_depth, ecl_gpu** out) {
   if ((e = cudaStreamCreateWithFlags(&g->copy, cudaStreamNonBlocking)) != cudaSuccess)
     return undo(cuda_fail(e, "cudaStreamCreate(copy)"));
   if ((e = cudaEventCreate(&g->epoch)) != cudaSuccess) return undo(cuda_fail(e, "cudaEventCreate"));
+  if ((e = cudaEventCreateWithFlags(&g->piece, cudaEventDisableTiming)) != cudaSuccess)
+    return undo(cuda_fail(e, "cudaEventCreate"));
   if ((e = cudaEventCreateWithFlags(&g->ready, cudaEventDisableTiming)) != cudaSuccess)
     return undo(cuda_fail(e, "cudaEventCreate"));
   for (auto& s : g->slots) {
@@ -189,6 +198,7 @@ int ecl_gpu_close(ecl_gpu* g) {
   if (g->compute) cudaStreamSynchronize(g->compute);
   if (g->copy) cudaStreamSynchronize(g->copy);
   free_buffers(g);
+  if (g->scratch) cudaFree(g->scratch);
   if (g->ctrl) cudaFree(g->ctrl);
   if (g->tally) cudaFree(g->tally);
   for (auto& s : g->slots) {
@@ -198,6 +208,7 @@ int ecl_gpu_close(ecl_gpu* g) {
   }
   if (g->epoch) cudaEventDestroy(g->epoch);
   if (g->ready) cudaEventDestroy(g->ready);
+  if (g->piece) cudaEventDestroy(g->piece);
   if (g->compute) cudaStreamDestroy(g->compute);
   if (g->copy) cudaStreamDestroy(g->copy);
   delete g;
@@ -267,6 +278,15 @@ int ecl_gpu_bind(ecl_gpu* g, const ecl_kernel* k) {
     g->out_bytes = want_out;
   }
   g->spec = &k->spec;
+  const uint64_t scratch = ecl::scratch_bytes(k->spec);
+  if (scratch > g->scratch_cap) {
+    if (g->scratch) cudaFree(g->scratch);
+    g->scratch = nullptr;
+    g->scratch_cap = 0;
+    ECL_CK(cudaMalloc(&g->scratch, scratch));
+    g->scratch_cap = scratch;
+  }
+  g->scratch_ready = false;
   ECL_CK(cudaMemsetAsync(g->ctrl, 0, 256, g->compute));
   return ECL_OK;
 }
@@ -405,26 +425,44 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
   slot.fn = done;
   slot.user = user;
 
-  const uint64_t first = offset_wg * s.lws, count = size_wg * s.lws;
-  ECL_CK(cudaEventRecord(slot.start, g->compute));
-  cudaError_t e = ecl::launch_kernel(s, env_of(g), first, count);
-  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
-  if (g->tally_on) {
-    e = ecl::launch_tally(g->tally, first, count, g->compute);
-    if (e != cudaSuccess) return cuda_fail(e, "tally launch");
-  }
-  ECL_CK(cudaEventRecord(slot.end, g->compute));
+  bool copies = false;
+  for (size_t b = 0; host_outputs && b < g->out.size(); ++b) copies = copies || host_outputs[b] != nullptr;
 
-  ECL_CK(cudaStreamWaitEvent(g->copy, slot.end, 0));
-  if (host_outputs) {
+  // With host outputs the package runs as sub-launches of ~d2h_split_items
+  // work-items, each followed on the copy stream by the D2H of its own
+  // slice, so the PCIe copy of piece i overlaps the kernel of piece i+1
+  // (the package's timing events still bracket the whole package).
+  uint64_t piece_wg = size_wg;
+  if (copies && g->d2h_split_items > 0) {
+    piece_wg = std::max<uint64_t>(1, g->d2h_split_items / s.lws);
+    uint64_t po = 0, pc = 0;
+    if (out_range(s, offset_wg, std::min(piece_wg, size_wg), &po, &pc) != ECL_OK) piece_wg = size_wg;
+  }
+  ECL_CK(cudaEventRecord(slot.start, g->compute));
+  for (uint64_t wg = offset_wg; wg < offset_wg + size_wg; wg += piece_wg) {
+    const uint64_t n_wg = std::min(piece_wg, offset_wg + size_wg - wg);
+    const uint64_t first = wg * s.lws, count = n_wg * s.lws;
+    cudaError_t e = ecl::launch_kernel(s, env_of(g), first, count);
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+    if (g->tally_on) {
+      e = ecl::launch_tally(g->tally, first, count, g->compute);
+      if (e != cudaSuccess) return cuda_fail(e, "tally launch");
+    }
+    if (!copies) continue;
+    uint64_t p_off = o_off, p_cnt = o_cnt;
+    if (piece_wg != size_wg && out_range(s, wg, n_wg, &p_off, &p_cnt) != ECL_OK) return ECL_INDIVISIBLE_PACKAGE;
+    ECL_CK(cudaEventRecord(g->piece, g->compute));
+    ECL_CK(cudaStreamWaitEvent(g->copy, g->piece, 0));  // waits on this recording only
     for (size_t b = 0; b < g->out.size(); ++b) {
       if (!host_outputs[b]) continue;
       const uint64_t esz = s.outputs[b].element_size_bytes;
-      ECL_CK(cudaMemcpyAsync(static_cast<char*>(host_outputs[b]) + o_off * esz,
-                             static_cast<const char*>(g->out[b]) + o_off * esz, o_cnt * esz,
+      ECL_CK(cudaMemcpyAsync(static_cast<char*>(host_outputs[b]) + p_off * esz,
+                             static_cast<const char*>(g->out[b]) + p_off * esz, p_cnt * esz,
                              cudaMemcpyDeviceToHost, g->copy));
     }
   }
+  ECL_CK(cudaEventRecord(slot.end, g->compute));
+  ECL_CK(cudaStreamWaitEvent(g->copy, slot.end, 0));
   if (done) ECL_CK(cudaLaunchHostFunc(g->copy, on_package_done, &slot));
   ECL_CK(cudaEventRecord(slot.done, g->copy));
   return ECL_OK;
@@ -532,3 +570,8 @@ int ecl_gpu_kernel_time(ecl_gpu* g, double* total_ms, uint64_t* launches, int re
 }
 
 }  // extern "C"
+
+extern "C" int ecl_gpu_set_copy_split(ecl_gpu* g, uint64_t items) {
+  g->d2h_split_items = items;
+  return ECL_OK;
+}

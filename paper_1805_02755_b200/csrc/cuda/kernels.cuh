@@ -71,7 +71,13 @@ struct LaunchEnv {
   void* const* in = nullptr;   // device pointers of the bound inputs
   void* const* out = nullptr;  // device pointers of the bound outputs
   unsigned* ctrl = nullptr;    // zeroed per-device control words (work counters)
+  void* scratch = nullptr;     // per-device, per-binding kernel scratch (scratch_bytes())
+  bool* scratch_ready = nullptr;  // false after bind: the kernel (re)initializes scratch
 };
+
+// Device scratch a kernel needs per binding (e.g. Mandelbrot coordinate tables).
+uint64_t scratch_bytes(const KernelSpec& spec);
+uint64_t mandelbrot_scratch_bytes(const KernelSpec& spec);
 
 // Parses and validates (kernel_for + check_buffer_shapes semantics).
 // Returns ECL_OK or a negative status with *err filled.

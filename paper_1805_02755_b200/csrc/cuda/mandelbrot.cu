@@ -7,48 +7,64 @@
 //   cx = x0 + ((px * (x1 - x0)) / W)          workloads.hpp:97
 //   xx = zx*zx; yy = zy*zy; escape if xx+yy > 4   :82-84
 //   zy = (2*zx)*zy + cy;  zx = (xx - yy) + cx      :85-86
-// One exact rewrite is used: (2*zx)*zy rounds to exactly 2*round(zx*zy)
-// (scaling by two is exact away from overflow/subnormals), and
-// round(2*t + cy) is one fma(t, 2, cy) because 2*t is exact — 7 FP64 pipe
-// ops per iteration instead of 8, same bits.
+// Exact rewrites (same bits, fewer FP64-pipe instructions):
+//  * (2*zx)*zy rounds to exactly 2*round(zx*zy) (scaling by two is exact
+//    away from overflow/subnormals) and round(2*t + cy) is one
+//    fma(t, 2, cy) because 2*t is exact.
+//  * xx + yy is a sum of squares, so it is >= +0 and its IEEE bit pattern
+//    orders like an unsigned integer: "xx + yy > 4.0" is one 64-bit integer
+//    compare on the ALU pipe instead of a DSETP on the FP64 pipe.
+//  * cx/cy depend on the column/row only: they are computed once per image
+//    by coord_tables with the reference formula and looked up per pixel, so
+//    the refill path has no IEEE double division.
+// 7 FP64-pipe instructions per iteration (3 DMUL, 3 DADD, 1 DFMA).
 //
 // Layout.  One persistent grid per package; each warp claims chunks of
-// kChunk consecutive pixels from a device-wide counter and keeps all 32
-// lanes busy by refilling a lane with the next pixel of the chunk as soon as
-// its pixel escapes (checked every R iterations), so the divergence of the
-// irregular set costs at most R-1 idle iterations per pixel instead of the
-// warp-wide max.  Results are written as one uint4 per pixel: the four
-// identical counts of the reference's 4:1 out pattern (workloads.hpp:217-222).
+// consecutive pixels from a device-wide counter (256-pixel chunks for the
+// first 7/8 of the package, 32-pixel chunks for the tail so a launch drains
+// evenly) and keeps all 32 lanes busy by refilling a lane with the next pixel
+// of the chunk as soon as its pixel finishes (checked every R iterations):
+// the divergence of the irregular set costs at most R-1 idle iterations per
+// pixel instead of the warp-wide maximum.  Results are one uint4 per pixel:
+// the four identical counts of the reference's 4:1 pattern (:217-222).
 #include "kernels.cuh"
 
 namespace ecl {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr uint64_t kChunk = 256;  // pixels per warp claim
+constexpr uint64_t kBigChunk = 256;   // pixels per claim, bulk of the package
+constexpr uint64_t kTailChunk = 32;   // pixels per claim, last 1/8
 constexpr int kThreads = 256;
+constexpr int kMinBlocks = 8;         // 64 resident warps per SM (<= 32 registers)
 
 template <typename Real>
 struct Arith;
 
 template <>
 struct Arith<double> {
+  using Bits = unsigned long long;
   static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
   static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
   static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
   static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
   static __device__ __forceinline__ double twice_plus(double t, double c) { return __fma_rn(t, 2.0, c); }
   static __device__ __forceinline__ double from_u64(uint64_t v) { return __ull2double_rn(v); }
+  static __device__ __forceinline__ Bits bits(double v) { return static_cast<Bits>(__double_as_longlong(v)); }
+  static constexpr Bits kFourBits = 0x4010000000000000ull;  // 4.0
 };
 
 template <>
 struct Arith<float> {
+  using Bits = unsigned;
   static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
   static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
   static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
   static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
   static __device__ __forceinline__ float twice_plus(float t, float c) { return __fmaf_rn(t, 2.0f, c); }
   static __device__ __forceinline__ float from_u64(uint64_t v) { return __ull2float_rn(v); }
+  static __device__ __forceinline__ Bits bits(float v) { return __float_as_uint(v); }
+  static constexpr Bits kFourBits = 0x40800000u;  // 4.0f
 };
 
 template <typename Real>
@@ -58,29 +74,51 @@ struct Viewport {
   Real x0, y0, span_x, span_y, fw, fh;  // span = x1 - x0 rounded in Real
 };
 
-template <typename Real, int R>
-__global__ void __launch_bounds__(kThreads)
-    mandel_persistent(const Viewport<Real> vp, uint64_t first, uint64_t count, uint4* __restrict__ out,
-                      unsigned* __restrict__ ctrl) {
+// cx[px] for px < W, then cy[py] for py < H: the reference's coordinate map.
+template <typename Real>
+__global__ void coord_tables(const Viewport<Real> vp, Real* __restrict__ tab) {
   using A = Arith<Real>;
+  const uint64_t n = vp.width + vp.height;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    tab[i] = i < vp.width ? A::add(vp.x0, A::div(A::mul(A::from_u64(i), vp.span_x), vp.fw))
+                          : A::add(vp.y0, A::div(A::mul(A::from_u64(i - vp.width), vp.span_y), vp.fh));
+  }
+}
+
+template <typename Real, int R>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    mandel_persistent(const Viewport<Real> vp, const Real* __restrict__ tab, uint64_t first, uint64_t count,
+                      uint4* __restrict__ out, unsigned* __restrict__ ctrl) {
+  using A = Arith<Real>;
+  using Bits = typename A::Bits;
   const unsigned lane = threadIdx.x & 31u;
   const unsigned below = (1u << lane) - 1u;
-  const uint64_t nchunks = (count + kChunk - 1) / kChunk;
+  const uint64_t big = (count - count / 8) / kBigChunk;  // claims 0..big-1 are 256-pixel chunks
+  const uint64_t tail_start = big * kBigChunk;
+  const uint64_t nclaims = big + (count - tail_start + kTailChunk - 1) / kTailChunk;
+  const Real* __restrict__ cxs = tab;
+  const Real* __restrict__ cys = tab + vp.width;
 
-  // Warp-uniform cursor over the claimed chunk: [next, end) relative to first.
-  uint64_t next = 0, end = 0;
+  // Warp-uniform cursor over the claimed chunk: [next, end) relative to
+  // first, with (px0, py0) the column/row of `next`.
+  uint64_t next = 0, end = 0, px0 = 0, py0 = 0;
   bool more = true;
   auto claim = [&]() {
     unsigned c = 0;
     if (lane == 0) c = atomicAdd(ctrl, 1u);
     c = __shfl_sync(kFull, c, 0);
-    if (c >= nchunks) {
+    if (c >= nclaims) {
       more = false;
       next = end = 0;
-    } else {
-      next = static_cast<uint64_t>(c) * kChunk;
-      end = next + kChunk < count ? next + kChunk : count;
+      return;
     }
+    next = c < big ? c * kBigChunk : tail_start + (c - big) * kTailChunk;
+    const uint64_t size = c < big ? kBigChunk : kTailChunk;
+    end = next + size < count ? next + size : count;
+    const uint64_t g = first + next;
+    py0 = g / vp.width;
+    px0 = g - py0 * vp.width;
   };
   claim();
 
@@ -98,17 +136,26 @@ __global__ void __launch_bounds__(kThreads)
       const uint64_t avail = end - next;
       if (!valid && rank < avail) {
         idx = first + next + rank;
-        const uint64_t px = idx % vp.width, py = idx / vp.width;
-        cx = A::add(vp.x0, A::div(A::mul(A::from_u64(px), vp.span_x), vp.fw));
-        cy = A::add(vp.y0, A::div(A::mul(A::from_u64(py), vp.span_y), vp.fh));
+        uint64_t px = px0 + rank, py = py0;
+        while (px >= vp.width) {  // at most once when W >= chunk size
+          px -= vp.width;
+          ++py;
+        }
+        cx = cxs[px];
+        cy = cys[py];
         zx = 0;
         zy = 0;
         n = 0;
         valid = true;
         alive = true;
       }
-      const uint64_t want = __popc(need);
-      next += want < avail ? want : avail;
+      const uint64_t take = __popc(need) < avail ? __popc(need) : avail;
+      next += take;
+      px0 += take;
+      while (px0 >= vp.width) {
+        px0 -= vp.width;
+        ++py0;
+      }
       if (next >= end) claim();
       need = __ballot_sync(kFull, !valid);
     }
@@ -118,7 +165,8 @@ __global__ void __launch_bounds__(kThreads)
     for (int r = 0; r < R; ++r) {
       const Real xx = A::mul(zx, zx);
       const Real yy = A::mul(zy, zy);
-      alive = alive && !(A::add(xx, yy) > Real(4));
+      const Bits s = A::bits(A::add(xx, yy));  // >= +0: integer order == FP order
+      alive = alive && s <= A::kFourBits;
       const Real t = A::mul(zx, zy);
       zy = A::twice_plus(t, cy);
       zx = A::add(A::sub(xx, yy), cx);
@@ -153,8 +201,8 @@ Viewport<Real> make_viewport(const MandelParams& p) {
   const Real x1 = static_cast<Real>(p.x1), y1 = static_cast<Real>(p.y1);
   vp.x0 = x0;
   vp.y0 = y0;
-  // x1 - x0 rounded once in Real, the same value the reference recomputes
-  // per pixel (host subtraction is IEEE round-to-nearest, no contraction).
+  // x1 - x0 rounded once in Real: the value the reference recomputes per
+  // pixel (host subtraction is IEEE round-to-nearest, no contraction).
   volatile Real sx = x1 - x0, sy = y1 - y0;
   vp.span_x = sx;
   vp.span_y = sy;
@@ -172,17 +220,31 @@ cudaError_t launch_real(const MandelParams& p, const LaunchEnv& env, uint64_t fi
     if (e != cudaSuccess) return e;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
-  const uint64_t warps_needed = (count + kChunk - 1) / kChunk;
-  const uint64_t blocks_needed = (warps_needed + kThreads / 32 - 1) / (kThreads / 32);
+  const Viewport<Real> vp = make_viewport<Real>(p);
+  Real* tab = static_cast<Real*>(env.scratch);
+  if (!env.scratch_ready) {
+    const uint64_t n = p.width + p.height;
+    coord_tables<Real><<<static_cast<unsigned>((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0,
+                         env.stream>>>(vp, tab);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    *env.scratch_ready = true;
+  }
+  const uint64_t claims = (count + kTailChunk - 1) / kTailChunk;
+  const uint64_t blocks_needed = (claims + kThreads / 32 - 1) / (kThreads / 32);
   uint64_t grid = static_cast<uint64_t>(env.sms) * static_cast<uint64_t>(blocks_per_sm);
   if (blocks_needed < grid) grid = blocks_needed;
   if (grid == 0) return cudaSuccess;
   mandel_persistent<Real, R><<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
-      make_viewport<Real>(p), first, count, static_cast<uint4*>(env.out[0]), env.ctrl);
+      vp, tab, first, count, static_cast<uint4*>(env.out[0]), env.ctrl);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+uint64_t mandelbrot_scratch_bytes(const KernelSpec& spec) {
+  return (spec.mandel.width + spec.mandel.height) * sizeof(double);
+}
 
 cudaError_t launch_mandelbrot(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
   if (count == 0) return cudaSuccess;

@@ -182,6 +182,14 @@ int resolve_kernel(KernelSpec& s, std::string* err) {
   return ECL_UNKNOWN_KERNEL;
 }
 
+uint64_t scratch_bytes(const KernelSpec& spec) {
+  switch (spec.kind) {
+    case KernelKind::Mandelbrot:
+    case KernelKind::MandelbrotF32: return mandelbrot_scratch_bytes(spec);
+    default: return 0;
+  }
+}
+
 cudaError_t launch_kernel(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
   switch (spec.kind) {
     case KernelKind::VecScale: return launch_vecscale(spec, env, first, count);

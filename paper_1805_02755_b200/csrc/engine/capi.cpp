@@ -42,8 +42,7 @@ int guarded(ecl_engine* e, F&& body) {
     if (e) e->errors = f.errors();
     return f.errors().empty() ? ECL_KERNEL_PANIC : status_of(f.errors().front().code());
   } catch (const Error& err) {
-    t_error = err.what();
-    if (e) e->errors = {err};
+    t_error = err.what();  // a single Error, not an EngineFailure aggregate
     return status_of(err.code());
   } catch (const json::exception& je) {
     t_error = std::string("ConfigError: ") + je.what();
