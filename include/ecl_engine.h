@@ -39,6 +39,13 @@ void ecl_engine_destroy(ecl_engine* engine);
  * buffers (ecl_host_register) get per-package async D2H. */
 int ecl_engine_run(ecl_engine* engine, const void* const* inputs, uint32_t n_inputs, void* const* outputs,
                    uint32_t n_outputs);
+/* Iterative run (e.g. NBody timesteps): `steps` passes; between passes the
+ * pairs (swap_in[k], swap_out[k]) are exchanged across devices (each owner
+ * GPU's package slices over NVLink) and swapped in place; outputs are
+ * gathered after the last pass (NULL = keep device-resident). */
+int ecl_engine_run_steps(ecl_engine* engine, const void* const* inputs, uint32_t n_inputs, void* const* outputs,
+                         uint32_t n_outputs, uint32_t steps, const uint32_t* swap_in, const uint32_t* swap_out,
+                         uint32_t n_swaps);
 /* Virtual-clock run with one cost per work-item (NULL = analytic costs). */
 int ecl_engine_run_virtual(ecl_engine* engine, const double* item_costs, uint64_t n);
 int ecl_engine_gather(ecl_engine* engine, void* const* outputs, uint32_t n_outputs);

@@ -43,6 +43,8 @@ _sig("ecl_engine_create", c_int, c_char_p, ctypes.POINTER(c_void_p))
 _sig("ecl_engine_destroy", None, c_void_p)
 _sig("ecl_engine_run", c_int, c_void_p, PVOID, c_u32, PVOID, c_u32)
 _sig("ecl_engine_run_virtual", c_int, c_void_p, ctypes.POINTER(c_dbl), c_u64)
+_sig("ecl_engine_run_steps", c_int, c_void_p, PVOID, c_u32, PVOID, c_u32, c_u32, ctypes.POINTER(c_u32),
+     ctypes.POINTER(c_u32), c_u32)
 _sig("ecl_engine_gather", c_int, c_void_p, PVOID, c_u32)
 _sig("ecl_engine_trace_json", c_i64, c_void_p, c_char_p, c_u64)
 _sig("ecl_engine_native_run", c_int, c_void_p, PVOID, c_u32, PVOID, c_u32, ctypes.POINTER(c_dbl),
@@ -72,6 +74,8 @@ _sig("ecl_engine_last_error", c_char_p)
 _sig("ecl_gpu_count", c_int, ctypes.POINTER(c_int))
 _sig("ecl_host_register", c_int, c_void_p, ctypes.c_size_t)
 _sig("ecl_host_unregister", c_int, c_void_p)
+_sig("ecl_host_alloc", c_int, ctypes.c_size_t, ctypes.POINTER(c_void_p))
+_sig("ecl_host_free", c_int, c_void_p)
 _sig("ecl_last_error", c_char_p)
 _sig("ecl_probe_vector_peaks", c_int, c_int, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl))
 

@@ -504,8 +504,10 @@ class Engine:
     def allocate_outputs(self) -> List[np.ndarray]:
         return [np.zeros(b.size_bytes(), dtype=np.uint8) for b in self._prog.spec().out_buffers]
 
-    def run_into(self, inputs: Sequence, outputs: Optional[Sequence[np.ndarray]]) -> ExecutionTrace:
-        """Caller-owned buffers; outputs=None keeps the results device-resident."""
+    def run_into(self, inputs: Sequence, outputs: Optional[Sequence[np.ndarray]],
+                 want_trace: bool = True) -> Optional[ExecutionTrace]:
+        """Caller-owned buffers; outputs=None keeps the results device-resident.
+        want_trace=False skips serializing the trace (last_trace() has it)."""
         in_ptrs = self._check_inputs(inputs)
         in_arr = N.pointer_array(in_ptrs)
         if outputs is None:
@@ -523,7 +525,22 @@ class Engine:
             rc = N.lib.ecl_engine_run(self._h, in_arr, len(in_ptrs), N.pointer_array(out_ptrs), len(out_ptrs))
         if rc != 0:
             self._fail(rc)
-        return self.last_trace()
+        return self.last_trace() if want_trace else None
+
+    def run_steps(self, inputs: Sequence, outputs: Optional[Sequence[np.ndarray]], steps: int,
+                  swaps: Sequence[Tuple[int, int]], want_trace: bool = True) -> Optional[ExecutionTrace]:
+        """Iterative program: `steps` passes; between passes each (input i,
+        output o) pair is exchanged across devices and swapped in place."""
+        in_ptrs = self._check_inputs(inputs)
+        out_ptrs = [_as_buffer(a)[0] for a in outputs] if outputs is not None else []
+        si = (ctypes.c_uint32 * max(1, len(swaps)))(*[a for a, _ in swaps])
+        so = (ctypes.c_uint32 * max(1, len(swaps)))(*[b for _, b in swaps])
+        rc = N.lib.ecl_engine_run_steps(self._h, N.pointer_array(in_ptrs), len(in_ptrs),
+                                        N.pointer_array(out_ptrs) if out_ptrs else None, len(out_ptrs), steps, si, so,
+                                        len(swaps))
+        if rc != 0:
+            self._fail(rc)
+        return self.last_trace() if want_trace else None
 
     def run(self, inputs: Sequence = ()) -> RunResult:
         """Reference semantics: engine-allocated outputs (engine.hpp:219-256)."""
@@ -589,6 +606,28 @@ def host_register(a: np.ndarray) -> None:
 def host_unregister(a: np.ndarray) -> None:
     p, _ = _as_buffer(a)
     N.lib.ecl_host_unregister(p)
+
+
+class PinnedBuffer:
+    """Page-locked host memory (cudaHostAlloc) viewed as a numpy array."""
+
+    def __init__(self, nbytes: int, dtype=np.uint8):
+        p = ctypes.c_void_p()
+        rc = N.lib.ecl_host_alloc(nbytes, ctypes.byref(p))
+        if rc != 0:
+            raise Error(ErrorCode[N.code_name(rc)], N.device_last_error())
+        self._ptr = p
+        raw = (ctypes.c_uint8 * nbytes).from_address(p.value)
+        self.array = np.frombuffer(raw, dtype=np.uint8).view(dtype)
+
+    def free(self):
+        if getattr(self, "_ptr", None):
+            self.array = None
+            N.lib.ecl_host_free(self._ptr)
+            self._ptr = None
+
+    def __del__(self):
+        self.free()
 
 
 def gpu_count() -> int:

@@ -21,6 +21,7 @@
 #include <cstdint>
 #include <memory>
 #include <span>
+#include <utility>
 #include <vector>
 
 #include "coexec/core.hpp"
@@ -65,6 +66,12 @@ class Engine {
   /// Caller-owned buffers; inputs[i] must hold in_buffers[i].size_bytes()
   /// bytes.  outputs empty (or all null) = device-resident run.
   ExecutionTrace run_into(std::span<const void* const> inputs, std::span<void* const> outputs);
+
+  /// Iterative program: `steps` passes; between passes every (input i,
+  /// output o) pair in `swaps` is exchanged across devices (owner slices over
+  /// NVLink) and swapped in place.  Outputs gathered after the last pass.
+  ExecutionTrace run_steps(std::span<const void* const> inputs, std::span<void* const> outputs, std::uint32_t steps,
+                           std::span<const std::pair<std::uint32_t, std::uint32_t>> swaps);
 
   /// Virtual clock (simulated devices): per-item costs, one per work-item;
   /// empty = the analytic cost of vecscale/synthetic kernels.

@@ -2,17 +2,24 @@
 //
 // Replaces NativePool (engine.hpp:97-200): where the reference wakes W host
 // threads, splits the package contiguously and waits on a condition variable
-// (engine.hpp:120-136), a package here is one kernel launch on the device's
-// compute stream bracketed by two timing events.  The D2H of the package's
-// out_range_for slice and the completion callback go on a second (copy)
-// stream that waits on the end event, so the copy of package k overlaps the
-// kernel of package k+1 and the compute stream never blocks on the host.
+// (engine.hpp:120-136), a package here is one kernel launch bracketed by two
+// timing events on one of the device's compute lanes (streams).
+//
+// Streams per device:
+//   lane[0], lane[1]  compute.  Consecutive packages alternate lanes (queue
+//                     depth >= 2), so package k+1's CTAs fill the SMs that
+//                     package k's drain tail leaves idle; each lane has its
+//                     own work-claim counters.  Depth 1 uses lane[0] only,
+//                     the reference's strictly serial device.
+//   copy              D2H of every package's out_range_for slice, waiting on
+//                     the kernel (piece) events: copies of package k overlap
+//                     the kernels of k+1.
+//   notify            completion callbacks, after the copies; kept off the
+//                     copy stream so a host callback never stalls a DMA.
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <atomic>
 #include <cstring>
-#include <mutex>
 #include <string>
 #include <vector>
 
@@ -37,18 +44,20 @@ int cuda_fail(cudaError_t e, const char* what) {
   return ECL_KERNEL_PANIC;
 }
 
-#define ECL_CK(call)                                  \
-  do {                                                \
-    cudaError_t e_ = (call);                          \
+#define ECL_CK(call)                                    \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
     if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
   } while (0)
 
 constexpr uint32_t kSlots = 64;  // timing-event ring; >= 2 x max queue depth
+constexpr int kLanes = 2;
+constexpr size_t kCtrlWordsPerLane = 16;
 
 struct Slot {
-  cudaEvent_t start = nullptr;  // kernel start (compute stream)
-  cudaEvent_t end = nullptr;    // kernel end (compute stream)
-  cudaEvent_t done = nullptr;   // copies + callback finished (copy stream)
+  cudaEvent_t start = nullptr;  // kernel start (its lane)
+  cudaEvent_t end = nullptr;    // kernel end (its lane)
+  cudaEvent_t done = nullptr;   // copies + callback finished (notify stream)
   uint64_t seq = ~0ull;
   bool busy = false;
   bool timed = false;
@@ -67,26 +76,29 @@ struct ecl_gpu {
   int ordinal = 0;
   int sms = 0;
   uint32_t depth = 2;
-  cudaStream_t compute = nullptr;
+  int lanes = 1;
+  cudaStream_t lane[kLanes] = {nullptr, nullptr};
   cudaStream_t copy = nullptr;
+  cudaStream_t notify = nullptr;
   cudaEvent_t epoch = nullptr;
-  cudaEvent_t ready = nullptr;  // last input/replication write on this device
-  cudaEvent_t piece = nullptr;  // end of a sub-launch whose slice the copy stream drains
+  cudaEvent_t ready = nullptr;             // last input/replication write on lane 0
+  cudaEvent_t piece[kLanes] = {nullptr, nullptr};  // end of a sub-launch the copy stream drains
+  cudaEvent_t copied = nullptr;            // copies of the latest package queued on `copy`
   double epoch_host_ms = 0.0;
   Slot slots[kSlots];
+  uint32_t next_slot = 0;  // per-device rotation: seqs are global across devices
+  uint32_t next_lane = 0;
   const ecl::KernelSpec* spec = nullptr;
   std::vector<void*> in, out;
   std::vector<uint64_t> in_bytes, out_bytes;
-  unsigned* ctrl = nullptr;
+  unsigned* ctrl = nullptr;  // kLanes x kCtrlWordsPerLane words
+  void* scratch = nullptr;
+  uint64_t scratch_cap = 0;
   uint32_t* tally = nullptr;
   uint64_t tally_items = 0;
   bool tally_on = false;
   double kernel_ms = 0.0;
   uint64_t launches = 0;
-  uint32_t next_slot = 0;  // per-device rotation: seqs are global across devices
-  void* scratch = nullptr;
-  uint64_t scratch_cap = 0;
-  bool scratch_ready = false;
   uint64_t d2h_split_items = 1ull << 23;  // sub-launch size when copies are pipelined
 };
 
@@ -103,16 +115,38 @@ int set_device(const ecl_gpu* g) {
   return ECL_OK;
 }
 
-ecl::LaunchEnv env_of(const ecl_gpu* g) {
+ecl::LaunchEnv env_of(const ecl_gpu* g, int lane) {
   ecl::LaunchEnv env;
-  env.stream = g->compute;
+  env.stream = g->lane[lane];
   env.sms = g->sms;
   env.in = g->in.data();
   env.out = g->out.data();
-  env.ctrl = g->ctrl;
+  env.ctrl = g->ctrl + lane * kCtrlWordsPerLane;
   env.scratch = g->scratch;
-  env.scratch_ready = const_cast<bool*>(&g->scratch_ready);
   return env;
+}
+
+// Makes every lane of g wait for the work queued so far on lane 0.
+int fan_out_lane0(ecl_gpu* g) {
+  ECL_CK(cudaEventRecord(g->ready, g->lane[0]));
+  for (int l = 1; l < g->lanes; ++l) ECL_CK(cudaStreamWaitEvent(g->lane[l], g->ready, 0));
+  return ECL_OK;
+}
+
+// Makes lane 0 wait for everything queued on the other lanes.
+int join_lanes(ecl_gpu* g) {
+  for (int l = 1; l < g->lanes; ++l) {
+    ECL_CK(cudaEventRecord(g->piece[l], g->lane[l]));
+    ECL_CK(cudaStreamWaitEvent(g->lane[0], g->piece[l], 0));
+  }
+  return ECL_OK;
+}
+
+int sync_all(ecl_gpu* g) {
+  for (int l = 0; l < g->lanes; ++l) ECL_CK(cudaStreamSynchronize(g->lane[l]));
+  ECL_CK(cudaStreamSynchronize(g->copy));
+  ECL_CK(cudaStreamSynchronize(g->notify));
+  return ECL_OK;
 }
 
 // out_range_for (core.hpp:172-185): the package's output-element range.
@@ -134,6 +168,15 @@ void free_buffers(ecl_gpu* g) {
   g->out.clear();
   g->in_bytes.clear();
   g->out_bytes.clear();
+}
+
+void enable_peer(int dst, int src) {
+  if (dst == src) return;
+  cudaSetDevice(dst);
+  int can = 0;
+  cudaDeviceCanAccessPeer(&can, dst, src);
+  if (can) cudaDeviceEnablePeerAccess(src, 0);  // AlreadyEnabled is fine
+  cudaGetLastError();
 }
 
 }  // namespace
@@ -165,6 +208,7 @@ int ecl_gpu_open(int ordinal, uint32_t queue_depth, ecl_gpu** out) {
   auto* g = new ecl_gpu;
   g->ordinal = ordinal;
   g->depth = queue_depth;
+  g->lanes = queue_depth >= 2 ? kLanes : 1;
   auto undo = [&](int rc) {
     ecl_gpu_close(g);
     return rc;
@@ -172,22 +216,25 @@ int ecl_gpu_open(int ordinal, uint32_t queue_depth, ecl_gpu** out) {
   if (int rc = set_device(g)) return undo(rc);
   cudaError_t e = cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, ordinal);
   if (e != cudaSuccess) return undo(cuda_fail(e, "cudaDeviceGetAttribute"));
-  if ((e = cudaStreamCreateWithFlags(&g->compute, cudaStreamNonBlocking)) != cudaSuccess)
-    return undo(cuda_fail(e, "cudaStreamCreate(compute)"));
+  for (int l = 0; l < kLanes; ++l)
+    if ((e = cudaStreamCreateWithFlags(&g->lane[l], cudaStreamNonBlocking)) != cudaSuccess)
+      return undo(cuda_fail(e, "cudaStreamCreate(lane)"));
   if ((e = cudaStreamCreateWithFlags(&g->copy, cudaStreamNonBlocking)) != cudaSuccess)
     return undo(cuda_fail(e, "cudaStreamCreate(copy)"));
+  if ((e = cudaStreamCreateWithFlags(&g->notify, cudaStreamNonBlocking)) != cudaSuccess)
+    return undo(cuda_fail(e, "cudaStreamCreate(notify)"));
   if ((e = cudaEventCreate(&g->epoch)) != cudaSuccess) return undo(cuda_fail(e, "cudaEventCreate"));
-  if ((e = cudaEventCreateWithFlags(&g->piece, cudaEventDisableTiming)) != cudaSuccess)
-    return undo(cuda_fail(e, "cudaEventCreate"));
-  if ((e = cudaEventCreateWithFlags(&g->ready, cudaEventDisableTiming)) != cudaSuccess)
-    return undo(cuda_fail(e, "cudaEventCreate"));
+  for (cudaEvent_t* ev : {&g->ready, &g->piece[0], &g->piece[1], &g->copied})
+    if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess)
+      return undo(cuda_fail(e, "cudaEventCreate"));
   for (auto& s : g->slots) {
     if ((e = cudaEventCreate(&s.start)) != cudaSuccess || (e = cudaEventCreate(&s.end)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming)) != cudaSuccess)
       return undo(cuda_fail(e, "cudaEventCreate(slot)"));
   }
-  if ((e = cudaMalloc(&g->ctrl, 256)) != cudaSuccess) return undo(cuda_fail(e, "cudaMalloc(ctrl)"));
-  if ((e = cudaMemset(g->ctrl, 0, 256)) != cudaSuccess) return undo(cuda_fail(e, "cudaMemset(ctrl)"));
+  const size_t ctrl_bytes = kLanes * kCtrlWordsPerLane * sizeof(unsigned);
+  if ((e = cudaMalloc(&g->ctrl, ctrl_bytes)) != cudaSuccess) return undo(cuda_fail(e, "cudaMalloc(ctrl)"));
+  if ((e = cudaMemset(g->ctrl, 0, ctrl_bytes)) != cudaSuccess) return undo(cuda_fail(e, "cudaMemset(ctrl)"));
   *out = g;
   return ECL_OK;
 }
@@ -195,8 +242,10 @@ int ecl_gpu_open(int ordinal, uint32_t queue_depth, ecl_gpu** out) {
 int ecl_gpu_close(ecl_gpu* g) {
   if (!g) return ECL_OK;
   cudaSetDevice(g->ordinal);
-  if (g->compute) cudaStreamSynchronize(g->compute);
+  for (int l = 0; l < kLanes; ++l)
+    if (g->lane[l]) cudaStreamSynchronize(g->lane[l]);
   if (g->copy) cudaStreamSynchronize(g->copy);
+  if (g->notify) cudaStreamSynchronize(g->notify);
   free_buffers(g);
   if (g->scratch) cudaFree(g->scratch);
   if (g->ctrl) cudaFree(g->ctrl);
@@ -206,12 +255,14 @@ int ecl_gpu_close(ecl_gpu* g) {
     if (s.end) cudaEventDestroy(s.end);
     if (s.done) cudaEventDestroy(s.done);
   }
-  if (g->epoch) cudaEventDestroy(g->epoch);
-  if (g->ready) cudaEventDestroy(g->ready);
-  if (g->piece) cudaEventDestroy(g->piece);
-  if (g->compute) cudaStreamDestroy(g->compute);
+  for (cudaEvent_t ev : {g->epoch, g->ready, g->piece[0], g->piece[1], g->copied})
+    if (ev) cudaEventDestroy(ev);
+  for (int l = 0; l < kLanes; ++l)
+    if (g->lane[l]) cudaStreamDestroy(g->lane[l]);
   if (g->copy) cudaStreamDestroy(g->copy);
+  if (g->notify) cudaStreamDestroy(g->notify);
   delete g;
+  cudaGetLastError();
   return ECL_OK;
 }
 
@@ -232,7 +283,8 @@ int ecl_kernel_create(const char* kernel_id, uint64_t gws, uint64_t lws, const e
   if (!kernel_id) return fail(ECL_UNKNOWN_KERNEL, "null kernel id");
   if (gws == 0 || lws == 0) return fail(ECL_CONFIG_ERROR, "global/local work size must be positive");
   if (gws % lws != 0) return fail(ECL_NON_DIVISIBLE_WORK_SIZE, "local_work_size does not divide global_work_size");
-  if (out_indices == 0 || out_work_items == 0) return fail(ECL_BAD_OUT_PATTERN, "out_pattern components must be positive");
+  if (out_indices == 0 || out_work_items == 0)
+    return fail(ECL_BAD_OUT_PATTERN, "out_pattern components must be positive");
   auto* k = new ecl_kernel;
   ecl::KernelSpec& s = k->spec;
   s.id = kernel_id;
@@ -257,8 +309,7 @@ void ecl_kernel_destroy(ecl_kernel* k) { delete k; }
 
 int ecl_gpu_bind(ecl_gpu* g, const ecl_kernel* k) {
   if (int rc = set_device(g)) return rc;
-  ECL_CK(cudaStreamSynchronize(g->compute));
-  ECL_CK(cudaStreamSynchronize(g->copy));
+  if (int rc = sync_all(g)) return rc;
   std::vector<uint64_t> want_in, want_out;
   for (const auto& b : k->spec.inputs) want_in.push_back(b.element_size_bytes * b.element_count);
   for (const auto& b : k->spec.outputs) want_out.push_back(b.element_size_bytes * b.element_count);
@@ -286,8 +337,10 @@ int ecl_gpu_bind(ecl_gpu* g, const ecl_kernel* k) {
     ECL_CK(cudaMalloc(&g->scratch, scratch));
     g->scratch_cap = scratch;
   }
-  g->scratch_ready = false;
-  ECL_CK(cudaMemsetAsync(g->ctrl, 0, 256, g->compute));
+  ECL_CK(cudaMemsetAsync(g->ctrl, 0, kLanes * kCtrlWordsPerLane * sizeof(unsigned), g->lane[0]));
+  const cudaError_t e = ecl::prepare_kernel(k->spec, env_of(g, 0));
+  if (e != cudaSuccess) return cuda_fail(e, "kernel prepare");
+  ECL_CK(cudaStreamSynchronize(g->lane[0]));
   return ECL_OK;
 }
 
@@ -301,18 +354,20 @@ int ecl_gpu_buffer(ecl_gpu* g, int is_output, uint32_t index, void** ptr) {
 int ecl_gpu_swap_io(ecl_gpu* g, uint32_t i, uint32_t o) {
   if (i >= g->in.size() || o >= g->out.size()) return fail(ECL_CONFIG_ERROR, "buffer index out of range");
   if (g->in_bytes[i] != g->out_bytes[o]) return fail(ECL_CONFIG_ERROR, "swap_io needs equal buffer sizes");
+  if (int rc = set_device(g)) return rc;
+  if (int rc = sync_all(g)) return rc;
   std::swap(g->in[i], g->out[o]);
   return ECL_OK;
 }
 
 int ecl_gpu_upload_inputs(ecl_gpu* g, const void* const* host_inputs) {
   if (int rc = set_device(g)) return rc;
+  if (int rc = join_lanes(g)) return rc;  // no kernel of an earlier run still reads the inputs
   for (size_t i = 0; i < g->in.size(); ++i) {
     if (!host_inputs || !host_inputs[i]) continue;
-    ECL_CK(cudaMemcpyAsync(g->in[i], host_inputs[i], g->in_bytes[i], cudaMemcpyHostToDevice, g->compute));
+    ECL_CK(cudaMemcpyAsync(g->in[i], host_inputs[i], g->in_bytes[i], cudaMemcpyHostToDevice, g->lane[0]));
   }
-  ECL_CK(cudaEventRecord(g->ready, g->compute));
-  return ECL_OK;
+  return fan_out_lane0(g);
 }
 
 int ecl_replicate_inputs(ecl_gpu* const* gpus, uint32_t n, uint32_t root) {
@@ -321,28 +376,20 @@ int ecl_replicate_inputs(ecl_gpu* const* gpus, uint32_t n, uint32_t root) {
   order.push_back(gpus[root]);
   for (uint32_t i = 0; i < n; ++i)
     if (i != root) order.push_back(gpus[i]);
-  // Binary doubling: in round r the first 2^r holders each feed one more.
+  // Binary doubling over NVLink: in round r the first 2^r holders each feed one more.
   for (size_t have = 1; have < order.size(); have *= 2) {
     for (size_t i = 0; i < have && have + i < order.size(); ++i) {
       ecl_gpu* src = order[i];
       ecl_gpu* dst = order[have + i];
       if (src->in_bytes != dst->in_bytes) return fail(ECL_CONFIG_ERROR, "replicate: devices bound differently");
-      if (src->ordinal != dst->ordinal) {
-        cudaSetDevice(dst->ordinal);
-        int can = 0;
-        cudaDeviceCanAccessPeer(&can, dst->ordinal, src->ordinal);
-        if (can) {
-          cudaError_t e = cudaDeviceEnablePeerAccess(src->ordinal, 0);
-          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "EnablePeerAccess");
-          cudaGetLastError();
-        }
-      }
+      enable_peer(dst->ordinal, src->ordinal);
       if (int rc = set_device(dst)) return rc;
-      ECL_CK(cudaStreamWaitEvent(dst->compute, src->ready, 0));
+      if (int rc = join_lanes(dst)) return rc;
+      ECL_CK(cudaStreamWaitEvent(dst->lane[0], src->ready, 0));
       for (size_t b = 0; b < dst->in.size(); ++b)
         ECL_CK(cudaMemcpyPeerAsync(dst->in[b], dst->ordinal, src->in[b], src->ordinal, dst->in_bytes[b],
-                                   dst->compute));
-      ECL_CK(cudaEventRecord(dst->ready, dst->compute));
+                                   dst->lane[0]));
+      if (int rc = fan_out_lane0(dst)) return rc;
     }
   }
   return ECL_OK;
@@ -356,22 +403,24 @@ int ecl_broadcast_output_slice(ecl_gpu* const* gpus, uint32_t n, uint32_t src_i,
   const uint64_t esz = src->spec->outputs[index].element_size_bytes;
   if ((elem_offset + elem_count) * esz > src->out_bytes[index])
     return fail(ECL_CONFIG_ERROR, "broadcast: slice out of range");
+  for (uint32_t d = 0; d < n; ++d) enable_peer(gpus[d]->ordinal, src->ordinal);
   if (int rc = set_device(src)) return rc;
+  if (int rc = join_lanes(src)) return rc;
   for (uint32_t d = 0; d < n; ++d) {
     ecl_gpu* dst = gpus[d];
     if (d == src_i || dst->out.size() <= index) continue;
     char* to = static_cast<char*>(dst->out[index]) + elem_offset * esz;
     const char* from = static_cast<const char*>(src->out[index]) + elem_offset * esz;
     if (dst->ordinal == src->ordinal)
-      ECL_CK(cudaMemcpyAsync(to, from, elem_count * esz, cudaMemcpyDeviceToDevice, src->compute));
+      ECL_CK(cudaMemcpyAsync(to, from, elem_count * esz, cudaMemcpyDeviceToDevice, src->lane[0]));
     else
-      ECL_CK(cudaMemcpyPeerAsync(to, dst->ordinal, from, src->ordinal, elem_count * esz, src->compute));
+      ECL_CK(cudaMemcpyPeerAsync(to, dst->ordinal, from, src->ordinal, elem_count * esz, src->lane[0]));
   }
-  ECL_CK(cudaEventRecord(src->ready, src->compute));
+  if (int rc = fan_out_lane0(src)) return rc;
   for (uint32_t d = 0; d < n; ++d) {
     if (d == src_i) continue;
     if (int rc = set_device(gpus[d])) return rc;
-    ECL_CK(cudaStreamWaitEvent(gpus[d]->compute, src->ready, 0));
+    for (int l = 0; l < gpus[d]->lanes; ++l) ECL_CK(cudaStreamWaitEvent(gpus[d]->lane[l], src->ready, 0));
   }
   return ECL_OK;
 }
@@ -382,7 +431,7 @@ int ecl_gpu_download_slice(ecl_gpu* g, uint32_t index, uint64_t elem_offset, uin
   if ((elem_offset + elem_count) * esz > g->out_bytes[index])
     return fail(ECL_CONFIG_ERROR, "download: slice out of range");
   if (int rc = set_device(g)) return rc;
-  ECL_CK(cudaStreamSynchronize(g->compute));
+  if (int rc = sync_all(g)) return rc;
   ECL_CK(cudaMemcpyAsync(host, static_cast<const char*>(g->out[index]) + elem_offset * esz, elem_count * esz,
                          cudaMemcpyDeviceToHost, g->copy));
   ECL_CK(cudaStreamSynchronize(g->copy));
@@ -406,6 +455,17 @@ int ecl_host_unregister(void* ptr) {
   return ECL_OK;
 }
 
+int ecl_host_alloc(size_t bytes, void** ptr) {
+  *ptr = nullptr;
+  ECL_CK(cudaHostAlloc(ptr, bytes, cudaHostAllocPortable));
+  return ECL_OK;
+}
+
+int ecl_host_free(void* ptr) {
+  ECL_CK(cudaFreeHost(ptr));
+  return ECL_OK;
+}
+
 int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_wg, void* const* host_outputs,
                    ecl_done_fn done, void* user) {
   if (!g->spec) return fail(ECL_CONFIG_ERROR, "submit before bind");
@@ -417,13 +477,16 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
   if (int rc = set_device(g)) return rc;
   if (find_slot(g, seq)) return fail(ECL_SCHEDULER_ERROR, "package seq submitted twice");
   Slot& slot = g->slots[g->next_slot];
-  g->next_slot = (g->next_slot + 1) % (kSlots - 1);  // the last slot is reserved for native_run
+  g->next_slot = (g->next_slot + 1) % (kSlots - 1);        // the last slot is reserved for native_run
   if (slot.busy) ECL_CK(cudaEventSynchronize(slot.done));  // ring wrapped: oldest must be retired
   slot.seq = seq;
   slot.busy = true;
   slot.timed = false;
   slot.fn = done;
   slot.user = user;
+  const int lane = static_cast<int>(g->next_lane);
+  g->next_lane = (g->next_lane + 1) % static_cast<uint32_t>(g->lanes);
+  cudaStream_t st = g->lane[lane];
 
   bool copies = false;
   for (size_t b = 0; host_outputs && b < g->out.size(); ++b) copies = copies || host_outputs[b] != nullptr;
@@ -438,21 +501,22 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
     uint64_t po = 0, pc = 0;
     if (out_range(s, offset_wg, std::min(piece_wg, size_wg), &po, &pc) != ECL_OK) piece_wg = size_wg;
   }
-  ECL_CK(cudaEventRecord(slot.start, g->compute));
+  const ecl::LaunchEnv env = env_of(g, lane);
+  ECL_CK(cudaEventRecord(slot.start, st));
   for (uint64_t wg = offset_wg; wg < offset_wg + size_wg; wg += piece_wg) {
     const uint64_t n_wg = std::min(piece_wg, offset_wg + size_wg - wg);
     const uint64_t first = wg * s.lws, count = n_wg * s.lws;
-    cudaError_t e = ecl::launch_kernel(s, env_of(g), first, count);
+    cudaError_t e = ecl::launch_kernel(s, env, first, count);
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     if (g->tally_on) {
-      e = ecl::launch_tally(g->tally, first, count, g->compute);
+      e = ecl::launch_tally(g->tally, first, count, st);
       if (e != cudaSuccess) return cuda_fail(e, "tally launch");
     }
     if (!copies) continue;
     uint64_t p_off = o_off, p_cnt = o_cnt;
     if (piece_wg != size_wg && out_range(s, wg, n_wg, &p_off, &p_cnt) != ECL_OK) return ECL_INDIVISIBLE_PACKAGE;
-    ECL_CK(cudaEventRecord(g->piece, g->compute));
-    ECL_CK(cudaStreamWaitEvent(g->copy, g->piece, 0));  // waits on this recording only
+    ECL_CK(cudaEventRecord(g->piece[lane], st));
+    ECL_CK(cudaStreamWaitEvent(g->copy, g->piece[lane], 0));  // captures this recording
     for (size_t b = 0; b < g->out.size(); ++b) {
       if (!host_outputs[b]) continue;
       const uint64_t esz = s.outputs[b].element_size_bytes;
@@ -461,19 +525,22 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
                              cudaMemcpyDeviceToHost, g->copy));
     }
   }
-  ECL_CK(cudaEventRecord(slot.end, g->compute));
-  ECL_CK(cudaStreamWaitEvent(g->copy, slot.end, 0));
-  if (done) ECL_CK(cudaLaunchHostFunc(g->copy, on_package_done, &slot));
-  ECL_CK(cudaEventRecord(slot.done, g->copy));
+  ECL_CK(cudaEventRecord(slot.end, st));
+  ECL_CK(cudaStreamWaitEvent(g->notify, slot.end, 0));
+  if (copies) {
+    ECL_CK(cudaEventRecord(g->copied, g->copy));
+    ECL_CK(cudaStreamWaitEvent(g->notify, g->copied, 0));
+  }
+  if (done) ECL_CK(cudaLaunchHostFunc(g->notify, on_package_done, &slot));
+  ECL_CK(cudaEventRecord(slot.done, g->notify));
   return ECL_OK;
 }
 
 int ecl_gpu_poll(ecl_gpu* g, uint64_t seq) {
   Slot* sp = find_slot(g, seq);
   if (!sp) return fail(ECL_CONFIG_ERROR, "poll: unknown package");
-  Slot& slot = *sp;
   cudaSetDevice(g->ordinal);
-  cudaError_t e = cudaEventQuery(slot.done);
+  cudaError_t e = cudaEventQuery(sp->done);
   if (e == cudaSuccess) return ECL_OK;
   if (e == cudaErrorNotReady) {
     cudaGetLastError();
@@ -505,7 +572,7 @@ int ecl_gpu_package_times(ecl_gpu* g, uint64_t seq, double* t_start, double* t_e
 
 int ecl_gpu_set_epoch(ecl_gpu* g, double (*host_now_ms)(void*), void* clock_user) {
   if (int rc = set_device(g)) return rc;
-  ECL_CK(cudaEventRecord(g->epoch, g->compute));
+  ECL_CK(cudaEventRecord(g->epoch, g->lane[0]));
   ECL_CK(cudaEventSynchronize(g->epoch));
   g->epoch_host_ms = host_now_ms ? host_now_ms(clock_user) : 0.0;
   return ECL_OK;
@@ -513,9 +580,7 @@ int ecl_gpu_set_epoch(ecl_gpu* g, double (*host_now_ms)(void*), void* clock_user
 
 int ecl_gpu_sync(ecl_gpu* g) {
   if (int rc = set_device(g)) return rc;
-  ECL_CK(cudaStreamSynchronize(g->compute));
-  ECL_CK(cudaStreamSynchronize(g->copy));
-  return ECL_OK;
+  return sync_all(g);
 }
 
 int ecl_gpu_enable_tally(ecl_gpu* g, int enable) {
@@ -523,20 +588,21 @@ int ecl_gpu_enable_tally(ecl_gpu* g, int enable) {
   g->tally_on = enable != 0;
   if (!g->tally_on) return ECL_OK;
   if (!g->spec) return fail(ECL_CONFIG_ERROR, "tally before bind");
+  if (int rc = join_lanes(g)) return rc;
   if (g->tally_items != g->spec->gws) {
     if (g->tally) cudaFree(g->tally);
     g->tally = nullptr;
     ECL_CK(cudaMalloc(&g->tally, g->spec->gws * sizeof(uint32_t)));
     g->tally_items = g->spec->gws;
   }
-  ECL_CK(cudaMemsetAsync(g->tally, 0, g->tally_items * sizeof(uint32_t), g->compute));
-  return ECL_OK;
+  ECL_CK(cudaMemsetAsync(g->tally, 0, g->tally_items * sizeof(uint32_t), g->lane[0]));
+  return fan_out_lane0(g);
 }
 
 int ecl_gpu_download_tally(ecl_gpu* g, uint32_t* host) {
   if (!g->tally) return fail(ECL_CONFIG_ERROR, "tally not enabled");
   if (int rc = set_device(g)) return rc;
-  ECL_CK(cudaStreamSynchronize(g->compute));
+  if (int rc = sync_all(g)) return rc;
   ECL_CK(cudaMemcpy(host, g->tally, g->tally_items * sizeof(uint32_t), cudaMemcpyDeviceToHost));
   return ECL_OK;
 }
@@ -544,19 +610,19 @@ int ecl_gpu_download_tally(ecl_gpu* g, uint32_t* host) {
 int ecl_gpu_native_run(ecl_gpu* g, float* kernel_ms) {
   if (!g->spec) return fail(ECL_CONFIG_ERROR, "native run before bind");
   if (int rc = set_device(g)) return rc;
+  if (int rc = join_lanes(g)) return rc;
   Slot& slot = g->slots[kSlots - 1];
-  if (slot.busy) ECL_CK(cudaEventSynchronize(slot.done));
-  ECL_CK(cudaEventRecord(slot.start, g->compute));
-  cudaError_t e = ecl::launch_kernel(*g->spec, env_of(g), 0, g->spec->gws);
+  ECL_CK(cudaEventRecord(slot.start, g->lane[0]));
+  cudaError_t e = ecl::launch_kernel(*g->spec, env_of(g, 0), 0, g->spec->gws);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
-  ECL_CK(cudaEventRecord(slot.end, g->compute));
+  ECL_CK(cudaEventRecord(slot.end, g->lane[0]));
   ECL_CK(cudaEventSynchronize(slot.end));
   float ms = 0.f;
   ECL_CK(cudaEventElapsedTime(&ms, slot.start, slot.end));
   *kernel_ms = ms;
   g->kernel_ms += ms;
   g->launches += 1;
-  return ECL_OK;
+  return fan_out_lane0(g);
 }
 
 int ecl_gpu_kernel_time(ecl_gpu* g, double* total_ms, uint64_t* launches, int reset) {
@@ -569,9 +635,9 @@ int ecl_gpu_kernel_time(ecl_gpu* g, double* total_ms, uint64_t* launches, int re
   return ECL_OK;
 }
 
-}  // extern "C"
-
-extern "C" int ecl_gpu_set_copy_split(ecl_gpu* g, uint64_t items) {
+int ecl_gpu_set_copy_split(ecl_gpu* g, uint64_t items) {
   g->d2h_split_items = items;
   return ECL_OK;
 }
+
+}  // extern "C"

@@ -1,0 +1,210 @@
+// gaussian.cu — direct FxF convolution with clamp-to-edge (the paper's
+// Gaussian blur benchmark; absent from the reference, definition in
+// SURVEY.md Appendix B and oracle/oracle.c:orc_gaussian).
+//
+//   out[y*W+x] = sum_{i<F} sum_{j<F} filt[i*F+j] * img[cl(y+i-F/2)*W + cl(x+j-F/2)]
+//
+// Layout (one CTA = a 64x32 output tile, 256 threads, 8 outputs per thread):
+//  * the (32+F-1) x (64+F-1) input tile is staged in shared memory with a
+//    row pitch of 100 floats (= 4 mod 32 banks).  Interior tiles are staged
+//    by the TMA engine: one cp.async.bulk (global -> shared, mbarrier
+//    complete_tx) per tile row, 16-byte aligned 384-byte rows; tiles that
+//    touch the image border use clamped LDG loads instead;
+//  * thread (tx, ty) owns outputs (ty, 8tx..8tx+7); lanes are laid out so
+//    the 8 lanes of an LDS.128 phase read 8 different rows -> the 100-float
+//    pitch spreads them over all 32 banks (conflict-free);
+//  * the filter lives in __constant__ memory (copied from the device input
+//    on the launch stream), so every FFMA takes its weight from a uniform
+//    register: per filter row i a thread loads 10 float4 of the input row
+//    and issues 8*F FFMAs (i outer, j inner, the oracle's order);
+//  * results leave as two float4 stores per thread.
+// Packages are arbitrary work-item ranges: tiles cover the rows the range
+// touches and only pixels inside [first, first+count) are written.
+#include <algorithm>
+
+#include "kernels.cuh"
+
+namespace ecl {
+namespace {
+
+constexpr int kTileW = 64, kTileH = 32, kThreads = 256, kPitch = 100;
+constexpr int kMaxF = 31;
+__constant__ float c_filter[63 * 63];
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+               "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(phase)
+      : "memory");
+}
+
+// TMA bulk copy of `bytes` (multiple of 16, 16-byte aligned) into shared memory.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+      "l"(src), "r"(bytes), "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+
+template <int F>
+__global__ void __launch_bounds__(kThreads)
+    gaussian_tiled(const float* __restrict__ img, float* __restrict__ out, int W, int H, uint64_t first, uint64_t count,
+                   int row0) {
+  constexpr int R = F / 2;
+  constexpr int TH = kTileH + F - 1;  // staged rows
+  constexpr int NV = 8 + F - 1;       // input values per thread row
+  constexpr int SHIFT = (4 - R % 4) % 4;  // first value's offset inside its float4
+  constexpr int NL = (SHIFT + NV + 3) / 4;  // float4 loads per filter row
+  __shared__ __align__(128) float tile[TH * kPitch];
+  __shared__ __align__(8) uint64_t bar;
+
+  const int tile_x = blockIdx.x * kTileW;
+  const int tile_y = row0 + blockIdx.y * kTileH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tx = (warp >> 2) * 4 + (lane >> 3);  // 0..7
+  const int ty = (warp & 3) * 8 + (lane & 7);    // 0..31
+
+  // Stage columns tile_x-16 .. tile_x+79 (96 floats) of rows tile_y-R .. ;
+  // smem column c holds global column tile_x - 16 + c.
+  const bool interior = tile_x >= 16 && tile_x + kTileW + 16 <= W && tile_y - R >= 0 && tile_y + kTileH + R <= H &&
+                        (W & 3) == 0;
+  if (interior) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) mbar_expect_tx(&bar, TH * 96 * 4);
+    __syncthreads();
+    if (threadIdx.x < TH) {
+      const int gy = tile_y - R + threadIdx.x;
+      bulk_g2s(&tile[threadIdx.x * kPitch], img + static_cast<int64_t>(gy) * W + (tile_x - 16), 96 * 4, &bar);
+    }
+    mbar_wait(&bar, 0);
+  } else {
+    for (int k = threadIdx.x; k < TH * 96; k += kThreads) {
+      const int r = k / 96, c = k - r * 96;
+      const int gy = clampi(tile_y - R + r, 0, H - 1), gx = clampi(tile_x - 16 + c, 0, W - 1);
+      tile[r * kPitch + c] = img[static_cast<int64_t>(gy) * W + gx];
+    }
+    __syncthreads();
+  }
+
+  float acc[8];
+#pragma unroll
+  for (int b = 0; b < 8; ++b) acc[b] = 0.0f;
+  // thread's first input column in smem: output col 8tx needs global col 8tx - R
+  const float* row = tile + ty * kPitch + (16 + 8 * tx - R - SHIFT);  // 16-byte aligned
+#pragma unroll 1
+  for (int i = 0; i < F; ++i) {
+    float v[NL * 4];
+    const float4* src = reinterpret_cast<const float4*>(row + i * kPitch);
+#pragma unroll
+    for (int m = 0; m < NL; ++m) {
+      const float4 q = src[m];
+      v[4 * m] = q.x;
+      v[4 * m + 1] = q.y;
+      v[4 * m + 2] = q.z;
+      v[4 * m + 3] = q.w;
+    }
+    const float* w = c_filter + i * F;
+#pragma unroll
+    for (int j = 0; j < F; ++j) {
+      const float wj = w[j];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) acc[b] = fmaf(wj, v[SHIFT + b + j], acc[b]);
+    }
+  }
+
+  // Masked float4 stores of the 8 outputs (pixels outside the package skipped).
+  const int gy = tile_y + ty, gx = tile_x + 8 * tx;
+  if (gy >= H || gx >= W) return;
+  const uint64_t base = static_cast<uint64_t>(gy) * W + gx;
+  float* dst = out + base;
+  if (base >= first && base + 8 <= first + count && gx + 8 <= W && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    reinterpret_cast<float4*>(dst)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    reinterpret_cast<float4*>(dst)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  } else {
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+      if (gx + b < W && base + b >= first && base + b < first + count) dst[b] = acc[b];
+  }
+}
+
+// Any odd F up to 63: one thread per output, filter from constant memory.
+__global__ void __launch_bounds__(kThreads)
+    gaussian_generic(const float* __restrict__ img, float* __restrict__ out, int W, int H, int F, uint64_t first,
+                     uint64_t count) {
+  const int R = F / 2;
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < count;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t idx = first + k;
+    const int x = static_cast<int>(idx % W), y = static_cast<int>(idx / W);
+    float acc = 0.0f;
+    for (int i = 0; i < F; ++i) {
+      const float* src = img + static_cast<int64_t>(clampi(y + i - R, 0, H - 1)) * W;
+      for (int j = 0; j < F; ++j) acc = fmaf(c_filter[i * F + j], src[clampi(x + j - R, 0, W - 1)], acc);
+    }
+    out[idx] = acc;
+  }
+}
+
+template <int F>
+cudaError_t launch_tiled(const GaussianParams& g, const LaunchEnv& env, uint64_t first, uint64_t count) {
+  const int row0 = static_cast<int>(first / g.width);
+  const int row1 = static_cast<int>((first + count - 1) / g.width);
+  const dim3 grid((g.width + kTileW - 1) / kTileW, (row1 - row0 + kTileH) / kTileH);
+  gaussian_tiled<F><<<grid, kThreads, 0, env.stream>>>(static_cast<const float*>(env.in[0]),
+                                                       static_cast<float*>(env.out[0]), static_cast<int>(g.width),
+                                                       static_cast<int>(g.height), first, count, row0);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_gaussian(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
+  if (count == 0) return cudaSuccess;
+  const GaussianParams& g = spec.gauss;
+  // The filter (input 1) goes to constant memory on the launch stream, so the
+  // kernels that follow on this stream see this program's filter.
+  cudaError_t e = cudaMemcpyToSymbolAsync(c_filter, env.in[1], sizeof(float) * g.filter * g.filter, 0,
+                                          cudaMemcpyDeviceToDevice, env.stream);
+  if (e != cudaSuccess) return e;
+  switch (g.filter) {
+    case 3: return launch_tiled<3>(g, env, first, count);
+    case 5: return launch_tiled<5>(g, env, first, count);
+    case 7: return launch_tiled<7>(g, env, first, count);
+    case 9: return launch_tiled<9>(g, env, first, count);
+    case 15: return launch_tiled<15>(g, env, first, count);
+    case 31: return launch_tiled<31>(g, env, first, count);
+    default: break;
+  }
+  const uint64_t blocks = std::min<uint64_t>((count + kThreads - 1) / kThreads, static_cast<uint64_t>(env.sms) * 16);
+  gaussian_generic<<<static_cast<unsigned>(blocks), kThreads, 0, env.stream>>>(
+      static_cast<const float*>(env.in[0]), static_cast<float*>(env.out[0]), static_cast<int>(g.width),
+      static_cast<int>(g.height), static_cast<int>(g.filter), first, count);
+  return cudaGetLastError();
+}
+
+}  // namespace ecl

@@ -72,12 +72,14 @@ struct LaunchEnv {
   void* const* out = nullptr;  // device pointers of the bound outputs
   unsigned* ctrl = nullptr;    // zeroed per-device control words (work counters)
   void* scratch = nullptr;     // per-device, per-binding kernel scratch (scratch_bytes())
-  bool* scratch_ready = nullptr;  // false after bind: the kernel (re)initializes scratch
 };
 
-// Device scratch a kernel needs per binding (e.g. Mandelbrot coordinate tables).
+// Device scratch a kernel needs per binding (e.g. Mandelbrot coordinate tables),
+// filled once by prepare_kernel when the program is bound to a device.
 uint64_t scratch_bytes(const KernelSpec& spec);
+cudaError_t prepare_kernel(const KernelSpec& spec, const LaunchEnv& env);
 uint64_t mandelbrot_scratch_bytes(const KernelSpec& spec);
+cudaError_t prepare_mandelbrot(const KernelSpec& spec, const LaunchEnv& env);
 
 // Parses and validates (kernel_for + check_buffer_shapes semantics).
 // Returns ECL_OK or a negative status with *err filled.

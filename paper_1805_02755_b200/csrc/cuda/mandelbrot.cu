@@ -221,15 +221,7 @@ cudaError_t launch_real(const MandelParams& p, const LaunchEnv& env, uint64_t fi
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   const Viewport<Real> vp = make_viewport<Real>(p);
-  Real* tab = static_cast<Real*>(env.scratch);
-  if (!env.scratch_ready) {
-    const uint64_t n = p.width + p.height;
-    coord_tables<Real><<<static_cast<unsigned>((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0,
-                         env.stream>>>(vp, tab);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    *env.scratch_ready = true;
-  }
+  const Real* tab = static_cast<const Real*>(env.scratch);
   const uint64_t claims = (count + kTailChunk - 1) / kTailChunk;
   const uint64_t blocks_needed = (claims + kThreads / 32 - 1) / (kThreads / 32);
   uint64_t grid = static_cast<uint64_t>(env.sms) * static_cast<uint64_t>(blocks_per_sm);
@@ -240,10 +232,22 @@ cudaError_t launch_real(const MandelParams& p, const LaunchEnv& env, uint64_t fi
   return cudaGetLastError();
 }
 
+template <typename Real>
+cudaError_t tables(const MandelParams& p, const LaunchEnv& env) {
+  const uint64_t n = p.width + p.height;
+  const unsigned grid = static_cast<unsigned>((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+  coord_tables<Real><<<grid, 256, 0, env.stream>>>(make_viewport<Real>(p), static_cast<Real*>(env.scratch));
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 uint64_t mandelbrot_scratch_bytes(const KernelSpec& spec) {
   return (spec.mandel.width + spec.mandel.height) * sizeof(double);
+}
+
+cudaError_t prepare_mandelbrot(const KernelSpec& spec, const LaunchEnv& env) {
+  return spec.kind == KernelKind::MandelbrotF32 ? tables<float>(spec.mandel, env) : tables<double>(spec.mandel, env);
 }
 
 cudaError_t launch_mandelbrot(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {

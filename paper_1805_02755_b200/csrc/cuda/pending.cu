@@ -6,8 +6,5 @@
 namespace ecl {
 
 cudaError_t launch_ray(const KernelSpec&, const LaunchEnv&, uint64_t, uint64_t) { return cudaErrorNotSupported; }
-cudaError_t launch_gaussian(const KernelSpec&, const LaunchEnv&, uint64_t, uint64_t) { return cudaErrorNotSupported; }
-cudaError_t launch_nbody(const KernelSpec&, const LaunchEnv&, uint64_t, uint64_t) { return cudaErrorNotSupported; }
-cudaError_t launch_binomial(const KernelSpec&, const LaunchEnv&, uint64_t, uint64_t) { return cudaErrorNotSupported; }
 
 }  // namespace ecl

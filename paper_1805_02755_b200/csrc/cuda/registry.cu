@@ -150,7 +150,7 @@ int resolve_kernel(KernelSpec& s, std::string* err) {
       // args [steps]; lws = steps + 1; one float4 of options per work-group.
       uint64_t steps;
       if (!arg_u64(s, 0, &steps, err)) return ECL_BAD_KERNEL_ARGS;
-      if (steps < 1 || steps > 1023) return bad(err, "binomial: steps must lie in [1, 1023]");
+      if (steps < 1 || steps > 255) return bad(err, "binomial: steps must lie in [1, 255]");
       if (s.lws != steps + 1) return bad(err, "binomial: local_work_size must be steps + 1");
       if (s.out_indices != 1 || s.out_work_items != s.lws) return bad(err, "binomial writes with a 1:lws out pattern");
       const uint64_t groups = s.gws / s.lws;
@@ -187,6 +187,14 @@ uint64_t scratch_bytes(const KernelSpec& spec) {
     case KernelKind::Mandelbrot:
     case KernelKind::MandelbrotF32: return mandelbrot_scratch_bytes(spec);
     default: return 0;
+  }
+}
+
+cudaError_t prepare_kernel(const KernelSpec& spec, const LaunchEnv& env) {
+  switch (spec.kind) {
+    case KernelKind::Mandelbrot:
+    case KernelKind::MandelbrotF32: return prepare_mandelbrot(spec, env);
+    default: return cudaSuccess;
   }
 }
 

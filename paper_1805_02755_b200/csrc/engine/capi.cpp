@@ -102,6 +102,17 @@ int ecl_engine_run(ecl_engine* e, const void* const* inputs, uint32_t n_in, void
   });
 }
 
+int ecl_engine_run_steps(ecl_engine* e, const void* const* inputs, uint32_t n_in, void* const* outputs,
+                         uint32_t n_out, uint32_t steps, const uint32_t* swap_in, const uint32_t* swap_out,
+                         uint32_t n_swaps) {
+  return guarded(e, [&] {
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> swaps;
+    for (uint32_t k = 0; k < n_swaps; ++k) swaps.emplace_back(swap_in[k], swap_out[k]);
+    e->engine->run_steps(std::span<const void* const>(inputs, inputs ? n_in : 0),
+                         std::span<void* const>(outputs, outputs ? n_out : 0), steps, swaps);
+  });
+}
+
 int ecl_engine_run_virtual(ecl_engine* e, const double* costs, uint64_t n) {
   return guarded(e, [&] { e->engine->run_virtual(std::span<const double>(costs, costs ? n : 0)); });
 }

@@ -300,25 +300,47 @@ struct Engine::Impl {
     if (!outputs.empty() && outputs.size() != s.out_buffers.size())
       throw Error(ErrorCode::ConfigError, "expected " + std::to_string(s.out_buffers.size()) + " output buffers");
 
+    const bool tally = begin_run(inputs);
+    std::vector<Package> done = co_execute(resident ? std::span<void* const>() : outputs, 0, tally);
+    last_resident = resident;
+    last_packages = done;
+    ExecutionTrace t = assemble(std::move(done));
+    last = t;
+    return t;
+  }
+
+  std::vector<ecl_gpu*> gpus() const {
+    std::vector<ecl_gpu*> g;
+    for (auto& d : devices) g.push_back(d->gpu);
+    return g;
+  }
+
+  // Run start: clock epoch, tally reset, one H2D into the first device and an
+  // NVLink doubling tree to the others (ecl_replicate_inputs).
+  bool begin_run(std::span<const void* const> inputs) {
     epoch = Clock::now();
     const bool tally = cfg.tally || tally_from_env();
-    std::vector<ecl_gpu*> gpus;
-    for (auto& d : devices) gpus.push_back(d->gpu);
+    std::vector<ecl_gpu*> g = gpus();
     for (auto& d : devices) {
       check(ecl_gpu_enable_tally(d->gpu, tally ? 1 : 0), "tally");
       check(ecl_gpu_set_epoch(d->gpu, &Impl::clock_cb, this), "epoch");
     }
     if (!inputs.empty()) {
-      // One H2D into the first device, then an NVLink doubling tree.
-      check(ecl_gpu_upload_inputs(gpus[0], const_cast<const void* const*>(inputs.data())), "upload");
-      if (gpus.size() > 1)
-        check(ecl_replicate_inputs(gpus.data(), static_cast<std::uint32_t>(gpus.size()), 0), "replicate");
+      check(ecl_gpu_upload_inputs(g[0], const_cast<const void* const*>(inputs.data())), "upload");
+      if (g.size() > 1) check(ecl_replicate_inputs(g.data(), static_cast<std::uint32_t>(g.size()), 0), "replicate");
     }
+    return tally;
+  }
 
+  // One pass over the whole index space: the device threads pull packages
+  // from a fresh scheduler until it is drained.  Returns the packages in
+  // seq order; throws EngineFailure on any device/tiling/tally error.
+  std::vector<Package> co_execute(std::span<void* const> host_out, std::uint64_t first_seq, bool tally) {
     auto scheduler = make_scheduler(cfg.scheduler, prog.total_work_groups(), cfg.devices);
     RunState rs;
     rs.scheduler = scheduler.get();
-    if (!resident) rs.host_out.assign(outputs.begin(), outputs.end());
+    rs.next_seq = first_seq;
+    rs.host_out.assign(host_out.begin(), host_out.end());
     {
       std::lock_guard lock(run_m);
       current = &rs;
@@ -331,7 +353,6 @@ struct Engine::Impl {
       idle_cv.wait(lock, [&] { return busy == 0; });
       current = nullptr;
     }
-
     std::sort(rs.completed.begin(), rs.completed.end(), [](const Package& a, const Package& b) { return a.seq < b.seq; });
     std::vector<Error> errors = std::move(rs.errors);
     if (errors.empty()) {
@@ -340,9 +361,52 @@ struct Engine::Impl {
       if (tally) check_tally(errors);
     }
     if (!errors.empty()) throw EngineFailure(std::move(errors));
-    last_resident = resident;
-    last_packages = rs.completed;
-    ExecutionTrace t = assemble(std::move(rs.completed));
+    return std::move(rs.completed);
+  }
+
+  // Iterative program (NBody timesteps):
+  // inputs are uploaded once; after every step but the last, each package's
+  // slices of the swapped outputs are copied from their owner GPU to every
+  // other GPU over NVLink (the per-step allgatherv of the new state) and each
+  // device swaps input i with output o in place.  Final outputs are gathered
+  // from the owners of the last step's packages.
+  ExecutionTrace run_steps(std::span<const void* const> inputs, std::span<void* const> outputs, std::uint32_t steps,
+                           std::span<const std::pair<std::uint32_t, std::uint32_t>> swaps) {
+    const ProgramSpec& s = prog.spec();
+    if (steps == 0) throw Error(ErrorCode::ConfigError, "run_steps needs at least one step");
+    if (inputs.size() != s.in_buffers.size())
+      throw Error(ErrorCode::InputSizeMismatch, "expected " + std::to_string(s.in_buffers.size()) + " input buffers");
+    for (const auto& [i, o] : swaps)
+      if (i >= s.in_buffers.size() || o >= s.out_buffers.size() ||
+          s.in_buffers[i].size_bytes() != s.out_buffers[o].size_bytes())
+        throw Error(ErrorCode::ConfigError, "run_steps: swap pairs need equal-size input/output buffers");
+    const bool tally = begin_run(inputs);
+    std::vector<ecl_gpu*> g = gpus();
+    std::vector<Package> all, step;
+    for (std::uint32_t k = 0; k < steps; ++k) {
+      if (tally && k > 0)
+        for (auto& d : devices) check(ecl_gpu_enable_tally(d->gpu, 1), "tally");
+      step = co_execute({}, all.size(), tally);
+      if (k + 1 < steps) {
+        if (g.size() > 1)
+          for (const Package& p : step) {
+            const OutRange r = out_range_for(p, prog);
+            for (const auto& [i, o] : swaps)
+              check(ecl_broadcast_output_slice(g.data(), static_cast<std::uint32_t>(g.size()), p.device_index, o,
+                                               r.offset, r.count),
+                    "exchange");
+          }
+        for (auto& d : devices)
+          for (const auto& [i, o] : swaps) check(ecl_gpu_swap_io(d->gpu, i, o), "swap");
+      }
+      all.insert(all.end(), step.begin(), step.end());
+    }
+    last_packages = step;
+    last_resident = true;
+    bool any_out = false;
+    for (void* p : outputs) any_out = any_out || p != nullptr;
+    if (any_out) gather(outputs);
+    ExecutionTrace t = assemble(std::move(all));
     last = t;
     return t;
   }
@@ -573,6 +637,12 @@ ExecutionTrace Engine::run_into(std::span<const void* const> inputs, std::span<v
 }
 
 ExecutionTrace Engine::run_virtual(std::span<const double> item_costs) { return impl_->run_virtual(item_costs); }
+
+ExecutionTrace Engine::run_steps(std::span<const void* const> inputs, std::span<void* const> outputs,
+                                 std::uint32_t steps, std::span<const std::pair<std::uint32_t, std::uint32_t>> swaps) {
+  if (!impl_->wall()) throw Error(ErrorCode::ConfigError, "run_steps needs clock_mode wall");
+  return impl_->run_steps(inputs, outputs, steps, swaps);
+}
 
 void Engine::gather(std::span<void* const> outputs) { impl_->gather(outputs); }
 
