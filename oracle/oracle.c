@@ -308,3 +308,159 @@ int orc_num_threads(void) {
   return 1;
 #endif
 }
+
+/* ------------------------------------------------------------------------ */
+/* Ray tracing (ABSENT in the reference; Table 2; this      */
+/* repo's definition).  Whitted-style: nearest hit     */
+/* over `ns` spheres and the ground plane y = 0, Phong shading with hard     */
+/* shadows from 3 point lights, mirror reflection up to `max_depth` bounces. */
+/* Every float operation is a single IEEE op in a fixed order (the oracle   */
+/* is built with -ffp-contract=off and the device uses _rn intrinsics), the */
+/* specular power is x^16 by four squarings, so the device can match the    */
+/* oracle bit for bit.  Scene buffer (float4): spheres[ns] (cx,cy,cz,r),    */
+/* materials[ns] (r,g,b,refl), then camera (ox,oy,oz,tan_half_fov),        */
+/* lights[3] (x,y,z,intensity), plane material (r,g,b,refl), shading        */
+/* (ambient, spec_k, 0, 0), sky (r,g,b,0).  Output float4 (r,g,b,bounces). */
+
+typedef struct { float x, y, z; } v3;
+
+static inline v3 v3sub(v3 a, v3 b) { v3 r = {a.x - b.x, a.y - b.y, a.z - b.z}; return r; }
+static inline float v3dot(v3 a, v3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+static inline v3 v3scale(v3 a, float s) { v3 r = {a.x * s, a.y * s, a.z * s}; return r; }
+static inline v3 v3norm(v3 a) {
+  const float len = sqrtf(v3dot(a, a));
+  v3 r = {a.x / len, a.y / len, a.z / len};
+  return r;
+}
+
+/* distance along (o,d) to sphere s (cx,cy,cz,r); < 0 = miss */
+static inline float ray_sphere(v3 o, v3 d, const float* s) {
+  const v3 c = {s[0], s[1], s[2]};
+  const v3 oc = v3sub(o, c);
+  const float b = v3dot(oc, d);
+  const float cc = v3dot(oc, oc) - s[3] * s[3];
+  const float disc = b * b - cc;
+  if (disc < 0.0f) return -1.0f;
+  const float sq = sqrtf(disc);
+  float t = -b - sq;
+  if (t > 1e-3f) return t;
+  t = -b + sq;
+  return t > 1e-3f ? t : -1.0f;
+}
+
+typedef struct { uint64_t sphere_tests, plane_tests, shades; } RayCounts;
+
+static void trace_pixel(const float* scene, uint32_t ns, uint32_t w, uint32_t h, uint32_t max_depth, uint64_t idx,
+                        float* out4, RayCounts* cnt) {
+  const float* sph = scene;
+  const float* mat = scene + 4 * ns;
+  const float* cam = scene + 8 * ns;
+  const float* lights = cam + 4;
+  const float* pmat = cam + 16;
+  const float* shading = cam + 20;
+  const float* sky = cam + 24;
+  const uint32_t px = (uint32_t)(idx % w), py = (uint32_t)(idx / w);
+  const float tanf_ = cam[3];
+  const float aspect = (float)w / (float)h;
+  const float u = ((2.0f * ((float)px + 0.5f)) / (float)w - 1.0f) * aspect * tanf_;
+  const float v = (1.0f - (2.0f * ((float)py + 0.5f)) / (float)h) * tanf_;
+  v3 d0 = {u, v, 1.0f};
+  v3 d = v3norm(d0);
+  v3 o = {cam[0], cam[1], cam[2]};
+  float r = 0.0f, g = 0.0f, b = 0.0f, weight = 1.0f;
+  uint32_t bounces = 0;
+  for (uint32_t depth = 0; depth <= max_depth; ++depth) {
+    float tmin = 1e30f;
+    int hit = -1;
+    for (uint32_t s = 0; s < ns; ++s) {
+      const float t = ray_sphere(o, d, sph + 4 * s);
+      if (t > 0.0f && t < tmin) { tmin = t; hit = (int)s; }
+    }
+    cnt->sphere_tests += ns;
+    cnt->plane_tests += 1;
+    if (d.y < 0.0f) {
+      const float tp = -o.y / d.y;
+      if (tp > 1e-3f && tp < tmin) { tmin = tp; hit = (int)ns; }
+    }
+    if (hit < 0) {
+      r += weight * sky[0];
+      g += weight * sky[1];
+      b += weight * sky[2];
+      break;
+    }
+    const v3 p = {o.x + tmin * d.x, o.y + tmin * d.y, o.z + tmin * d.z};
+    v3 n;
+    float cr, cg, cb, refl;
+    if (hit < (int)ns) {
+      const v3 c = {sph[4 * hit], sph[4 * hit + 1], sph[4 * hit + 2]};
+      n = v3norm(v3sub(p, c));
+      cr = mat[4 * hit]; cg = mat[4 * hit + 1]; cb = mat[4 * hit + 2]; refl = mat[4 * hit + 3];
+    } else {
+      n.x = 0.0f; n.y = 1.0f; n.z = 0.0f;
+      const int check = ((int)floorf(p.x) + (int)floorf(p.z)) & 1;
+      const float k = check ? 1.0f : 0.35f;
+      cr = pmat[0] * k; cg = pmat[1] * k; cb = pmat[2] * k; refl = pmat[3];
+    }
+    const float amb = shading[0], spec_k = shading[1];
+    float lr = amb * cr, lg = amb * cg, lb = amb * cb;
+    for (int l = 0; l < 3; ++l) {
+      const v3 lp = {lights[4 * l], lights[4 * l + 1], lights[4 * l + 2]};
+      const v3 L = v3sub(lp, p);
+      const float dist = sqrtf(v3dot(L, L));
+      const v3 ln = {L.x / dist, L.y / dist, L.z / dist};
+      const float ndl = v3dot(n, ln);
+      cnt->shades += 1;
+      if (ndl <= 0.0f) continue;
+      int shadow = 0;
+      for (uint32_t s = 0; s < ns; ++s) {
+        const float t = ray_sphere(p, ln, sph + 4 * s);
+        if (t > 0.0f && t < dist) { shadow = 1; break; }
+      }
+      cnt->sphere_tests += ns; /* counted as a full pass (the device has no early exit per lane) */
+      if (shadow) continue;
+      /* specular: reflect -ln about n, dot with -d, ^16 */
+      const float two_ndl = 2.0f * ndl;
+      const v3 rl = {two_ndl * n.x - ln.x, two_ndl * n.y - ln.y, two_ndl * n.z - ln.z};
+      float sp = -(rl.x * d.x + rl.y * d.y + rl.z * d.z);
+      sp = sp > 0.0f ? sp : 0.0f;
+      sp = sp * sp; sp = sp * sp; sp = sp * sp; sp = sp * sp;
+      const float I = lights[4 * l + 3];
+      lr += I * (cr * ndl + spec_k * sp);
+      lg += I * (cg * ndl + spec_k * sp);
+      lb += I * (cb * ndl + spec_k * sp);
+    }
+    const float keep = weight * (1.0f - refl);
+    r += keep * lr;
+    g += keep * lg;
+    b += keep * lb;
+    bounces = depth + 1;
+    weight = weight * refl;
+    if (!(refl > 0.0f) || weight < 1e-3f) break;
+    const float two_dn = 2.0f * v3dot(d, n);
+    const v3 nd = {d.x - two_dn * n.x, d.y - two_dn * n.y, d.z - two_dn * n.z};
+    d = nd;
+    o = p;
+  }
+  out4[0] = r; out4[1] = g; out4[2] = b; out4[3] = (float)bounces;
+}
+
+/* Renders pixels [first, first+count) into out4 (float4 per pixel, indexed
+ * globally) and returns the instrumented operation counts. */
+void orc_ray(const float* scene, uint32_t ns, uint32_t w, uint32_t h, uint32_t max_depth, float* out4,
+             uint64_t first, uint64_t count, uint64_t* counts3) {
+  uint64_t st = 0, pt = 0, sh = 0;
+#pragma omp parallel for schedule(dynamic, 256) reduction(+ : st, pt, sh)
+  for (int64_t k = 0; k < (int64_t)count; ++k) {
+    RayCounts c = {0, 0, 0};
+    const uint64_t idx = first + (uint64_t)k;
+    trace_pixel(scene, ns, w, h, max_depth, idx, out4 + 4 * idx, &c);
+    st += c.sphere_tests;
+    pt += c.plane_tests;
+    sh += c.shades;
+  }
+  if (counts3) {
+    counts3[0] = st;
+    counts3[1] = pt;
+    counts3[2] = sh;
+  }
+}

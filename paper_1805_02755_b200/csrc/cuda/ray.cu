@@ -1,0 +1,254 @@
+// ray.cu — Whitted ray tracer (the paper's Ray benchmark, Table 2
+// PAPER.md:506-511; absent from the reference, definition frozen in
+// oracle/oracle.c:orc_ray — SURVEY.md Appendix B).
+//
+// Parity: every float operation is an IEEE-rounded intrinsic (_rn) in the
+// oracle's order and the specular power is x^16 by four squarings, so the
+// device reproduces the oracle's pixels bit for bit (no FMA contraction,
+// correctly rounded sqrt and division).
+//
+// Layout: the sphere and material arrays (2 x ns float4) are staged in
+// shared memory once per CTA and read as warp-wide broadcasts.  Work is
+// irregular (0..max_depth+1 bounces per pixel, shadow tests that stop at the
+// first occluder), so warps are persistent and refill lanes per bounce:
+// each warp claims 32-pixel chunks from a device counter and, after every
+// bounce, lanes whose pixel finished store it and take the next pixel — a
+// warp stays full until the package is exhausted instead of idling on its
+// deepest reflection.
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace ecl {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kThreads = 128;  // Table 2: lws 128
+constexpr uint64_t kChunk = 32;
+constexpr int kMaxSpheres = 256;
+
+struct V3 {
+  float x, y, z;
+};
+
+__device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float dvd(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ V3 vsub(V3 a, V3 b) { return {sub(a.x, b.x), sub(a.y, b.y), sub(a.z, b.z)}; }
+__device__ __forceinline__ float vdot(V3 a, V3 b) { return add(add(mul(a.x, b.x), mul(a.y, b.y)), mul(a.z, b.z)); }
+__device__ __forceinline__ V3 vnorm(V3 a) {
+  const float len = __fsqrt_rn(vdot(a, a));
+  return {dvd(a.x, len), dvd(a.y, len), dvd(a.z, len)};
+}
+
+// distance along (o, d) to sphere s; < 0 = miss (oracle: ray_sphere)
+__device__ __forceinline__ float ray_sphere(V3 o, V3 d, float4 s) {
+  const V3 oc = vsub(o, V3{s.x, s.y, s.z});
+  const float b = vdot(oc, d);
+  const float cc = sub(vdot(oc, oc), mul(s.w, s.w));
+  const float disc = sub(mul(b, b), cc);
+  if (disc < 0.0f) return -1.0f;
+  const float sq = __fsqrt_rn(disc);
+  float t = sub(-b, sq);
+  if (t > 1e-3f) return t;
+  t = add(-b, sq);
+  return t > 1e-3f ? t : -1.0f;
+}
+
+struct Lane {
+  V3 o, d;
+  float r, g, b, weight;
+  uint32_t depth, bounces;
+};
+
+__global__ void __launch_bounds__(kThreads)
+    ray_persistent(const float4* __restrict__ scene, uint32_t ns, uint32_t w, uint32_t h, uint32_t max_depth,
+                   float4* __restrict__ out, uint64_t first, uint64_t count, unsigned* __restrict__ ctrl) {
+  __shared__ float4 sph[kMaxSpheres], mat[kMaxSpheres];
+  for (uint32_t i = threadIdx.x; i < ns; i += kThreads) {
+    sph[i] = scene[i];
+    mat[i] = scene[ns + i];
+  }
+  const float4* cam4 = scene + 2 * ns;
+  const float4 cam = cam4[0];
+  const float4 lights[3] = {cam4[1], cam4[2], cam4[3]};
+  const float4 pmat = cam4[4], shading = cam4[5], sky = cam4[6];
+  __syncthreads();
+
+  const unsigned lane_id = threadIdx.x & 31u;
+  const unsigned below = (1u << lane_id) - 1u;
+  const uint64_t nchunks = (count + kChunk - 1) / kChunk;
+  uint64_t next = 0, end = 0;
+  bool more = true;
+  auto claim = [&]() {
+    unsigned c = 0;
+    if (lane_id == 0) c = atomicAdd(ctrl, 1u);
+    c = __shfl_sync(kFull, c, 0);
+    if (c >= nchunks) {
+      more = false;
+      next = end = 0;
+    } else {
+      next = static_cast<uint64_t>(c) * kChunk;
+      end = next + kChunk < count ? next + kChunk : count;
+    }
+  };
+  claim();
+
+  const float aspect = dvd(static_cast<float>(w), static_cast<float>(h));
+  bool valid = false;
+  uint64_t idx = 0;
+  Lane L{};
+  for (;;) {
+    unsigned need = __ballot_sync(kFull, !valid);
+    while (need && more) {
+      const unsigned rank = __popc(need & below);
+      const uint64_t avail = end - next;
+      if (!valid && rank < avail) {
+        idx = first + next + rank;
+        const uint32_t px = static_cast<uint32_t>(idx % w), py = static_cast<uint32_t>(idx / w);
+        const float u = mul(mul(sub(dvd(mul(2.0f, add(static_cast<float>(px), 0.5f)), static_cast<float>(w)), 1.0f),
+                                aspect),
+                            cam.w);
+        const float v =
+            mul(sub(1.0f, dvd(mul(2.0f, add(static_cast<float>(py), 0.5f)), static_cast<float>(h))), cam.w);
+        L.d = vnorm(V3{u, v, 1.0f});
+        L.o = V3{cam.x, cam.y, cam.z};
+        L.r = L.g = L.b = 0.0f;
+        L.weight = 1.0f;
+        L.depth = 0;
+        L.bounces = 0;
+        valid = true;
+      }
+      const uint64_t want = __popc(need);
+      next += want < avail ? want : avail;
+      if (next >= end) claim();
+      need = __ballot_sync(kFull, !valid);
+    }
+    if (!__any_sync(kFull, valid)) break;
+
+    bool finished = !valid;
+    if (valid) {
+      // ---- one bounce (oracle: trace_pixel loop body) ----
+      float tmin = 1e30f;
+      int hit = -1;
+      for (uint32_t s = 0; s < ns; ++s) {
+        const float t = ray_sphere(L.o, L.d, sph[s]);
+        if (t > 0.0f && t < tmin) {
+          tmin = t;
+          hit = static_cast<int>(s);
+        }
+      }
+      if (L.d.y < 0.0f) {
+        const float tp = dvd(-L.o.y, L.d.y);
+        if (tp > 1e-3f && tp < tmin) {
+          tmin = tp;
+          hit = static_cast<int>(ns);
+        }
+      }
+      if (hit < 0) {
+        L.r = add(L.r, mul(L.weight, sky.x));
+        L.g = add(L.g, mul(L.weight, sky.y));
+        L.b = add(L.b, mul(L.weight, sky.z));
+        finished = true;
+      } else {
+        const V3 p{add(L.o.x, mul(tmin, L.d.x)), add(L.o.y, mul(tmin, L.d.y)), add(L.o.z, mul(tmin, L.d.z))};
+        V3 n;
+        float cr, cg, cb, refl;
+        if (hit < static_cast<int>(ns)) {
+          const float4 c = sph[hit], m = mat[hit];
+          n = vnorm(vsub(p, V3{c.x, c.y, c.z}));
+          cr = m.x;
+          cg = m.y;
+          cb = m.z;
+          refl = m.w;
+        } else {
+          n = V3{0.0f, 1.0f, 0.0f};
+          const int check = (static_cast<int>(floorf(p.x)) + static_cast<int>(floorf(p.z))) & 1;
+          const float k = check ? 1.0f : 0.35f;
+          cr = mul(pmat.x, k);
+          cg = mul(pmat.y, k);
+          cb = mul(pmat.z, k);
+          refl = pmat.w;
+        }
+        float lr = mul(shading.x, cr), lg = mul(shading.x, cg), lb = mul(shading.x, cb);
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+          const V3 Lv = vsub(V3{lights[l].x, lights[l].y, lights[l].z}, p);
+          const float dist = __fsqrt_rn(vdot(Lv, Lv));
+          const V3 ln{dvd(Lv.x, dist), dvd(Lv.y, dist), dvd(Lv.z, dist)};
+          const float ndl = vdot(n, ln);
+          if (ndl <= 0.0f) continue;
+          bool shadow = false;
+          for (uint32_t s = 0; s < ns && !shadow; ++s) {
+            const float t = ray_sphere(p, ln, sph[s]);
+            shadow = t > 0.0f && t < dist;
+          }
+          if (shadow) continue;
+          const float two_ndl = mul(2.0f, ndl);
+          const V3 rl{sub(mul(two_ndl, n.x), ln.x), sub(mul(two_ndl, n.y), ln.y), sub(mul(two_ndl, n.z), ln.z)};
+          float sp = -add(add(mul(rl.x, L.d.x), mul(rl.y, L.d.y)), mul(rl.z, L.d.z));
+          sp = sp > 0.0f ? sp : 0.0f;
+          sp = mul(sp, sp);
+          sp = mul(sp, sp);
+          sp = mul(sp, sp);
+          sp = mul(sp, sp);
+          const float I = lights[l].w;
+          lr = add(lr, mul(I, add(mul(cr, ndl), mul(shading.y, sp))));
+          lg = add(lg, mul(I, add(mul(cg, ndl), mul(shading.y, sp))));
+          lb = add(lb, mul(I, add(mul(cb, ndl), mul(shading.y, sp))));
+        }
+        const float keep = mul(L.weight, sub(1.0f, refl));
+        L.r = add(L.r, mul(keep, lr));
+        L.g = add(L.g, mul(keep, lg));
+        L.b = add(L.b, mul(keep, lb));
+        L.bounces = L.depth + 1;
+        L.weight = mul(L.weight, refl);
+        if (!(refl > 0.0f) || L.weight < 1e-3f || L.depth + 1 > max_depth) {
+          finished = true;
+        } else {
+          const float two_dn = mul(2.0f, vdot(L.d, n));
+          L.d = V3{sub(L.d.x, mul(two_dn, n.x)), sub(L.d.y, mul(two_dn, n.y)), sub(L.d.z, mul(two_dn, n.z))};
+          L.o = p;
+          L.depth += 1;
+        }
+      }
+    }
+    if (valid && finished) {
+      out[idx] = make_float4(L.r, L.g, L.b, static_cast<float>(L.bounces));
+      valid = false;
+    }
+  }
+
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned done = atomicAdd(ctrl + 1, 1u);
+    if (done == gridDim.x - 1) {
+      atomicExch(ctrl, 0u);
+      atomicExch(ctrl + 1, 0u);
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_ray(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
+  if (count == 0) return cudaSuccess;
+  static int blocks_per_sm = 0;
+  if (blocks_per_sm == 0) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ray_persistent, kThreads, 0);
+    if (e != cudaSuccess) return e;
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  const uint64_t chunks = (count + kChunk - 1) / kChunk;
+  const uint64_t blocks_needed = (chunks + kThreads / 32 - 1) / (kThreads / 32);
+  uint64_t grid = static_cast<uint64_t>(env.sms) * static_cast<uint64_t>(blocks_per_sm);
+  if (blocks_needed < grid) grid = blocks_needed;
+  ray_persistent<<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
+      static_cast<const float4*>(env.in[0]), spec.ray.spheres, spec.ray.width, spec.ray.height, spec.ray.max_depth,
+      static_cast<float4*>(env.out[0]), first, count, env.ctrl);
+  return cudaGetLastError();
+}
+
+}  // namespace ecl

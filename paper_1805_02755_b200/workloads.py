@@ -115,7 +115,47 @@ def binomial_inputs(options: int, seed: int = 42):
     return [unit_doubles(seed, 0, options).astype(np.float32)]
 
 
+def ray_spec(width: int, height: int, spheres: int = 64, max_depth: int = 4, lws: int = 128) -> ProgramSpec:
+    return ProgramSpec(width * height, lws, [BufferDesc("scene", 16, 2 * spheres + 8)],
+                       [BufferDesc("rgba", 16, width * height)], OutPattern(1, 1), "ray",
+                       [int(width), int(height), int(spheres), int(max_depth)])
+
+
+def ray_scene(spheres: int = 64, seed: int = 42) -> np.ndarray:
+    """Seeded fixed scene (float4 records, layout in oracle.c:orc_ray):
+    spheres resting above a checkered mirror-ish floor, every third sphere a
+    mirror, three point lights."""
+    u = unit_doubles(seed, 0, 8 * spheres).reshape(spheres, 8)
+    s = np.zeros((2 * spheres + 8, 4), np.float64)
+    r = 0.3 + 1.2 * u[:, 2]
+    s[:spheres, 0] = -8.0 + 16.0 * u[:, 0]
+    s[:spheres, 1] = r + 2.0 * u[:, 3]
+    s[:spheres, 2] = 2.0 + 16.0 * u[:, 1]
+    s[:spheres, 3] = r
+    s[spheres:2 * spheres, 0:3] = 0.2 + 0.8 * u[:, 4:7]
+    mirror = (np.arange(spheres) % 3) == 0
+    s[spheres:2 * spheres, 3] = np.where(mirror, 0.6 + 0.3 * u[:, 7], 0.15 * u[:, 7])
+    c = 2 * spheres
+    s[c + 0] = (0.0, 2.5, -12.0, 0.6)        # camera (x, y, z, tan(fov/2))
+    s[c + 1] = (-10.0, 12.0, -6.0, 0.7)      # lights (x, y, z, intensity)
+    s[c + 2] = (8.0, 15.0, 0.0, 0.5)
+    s[c + 3] = (0.0, 20.0, 10.0, 0.4)
+    s[c + 4] = (0.9, 0.9, 0.9, 0.3)          # floor material (r, g, b, reflectivity)
+    s[c + 5] = (0.08, 0.5, 0.0, 0.0)         # ambient, specular k
+    s[c + 6] = (0.25, 0.35, 0.55, 0.0)       # sky
+    return s.astype(np.float32)
+
+
 # ---- algorithmic work (SURVEY.md §8d) ---------------------------------------
+
+RAY_FLOPS_PER_SPHERE_TEST = 17  # oc (3), b (5), |oc|^2 - r^2 (7), disc (2); sqrt/roots excluded
+RAY_FLOPS_PER_PLANE_TEST = 2
+RAY_FLOPS_PER_SHADE = 30
+
+
+def ray_flops(sphere_tests: int, plane_tests: int, shades: int) -> float:
+    return float(RAY_FLOPS_PER_SPHERE_TEST * sphere_tests + RAY_FLOPS_PER_PLANE_TEST * plane_tests +
+                 RAY_FLOPS_PER_SHADE * shades)
 
 def mandelbrot_flops(counts: np.ndarray, max_iter: int) -> float:
     """8 FP ops per iteration + 3 for the final (failed) escape test."""

@@ -46,6 +46,16 @@ class Oracle:
         lib.orc_binomial.argtypes = [VP, VP, U32, U64, U64]
         lib.orc_binomial_init.argtypes = [U64, U64, VP]
         lib.orc_num_threads.restype = ctypes.c_int
+        lib.orc_ray.argtypes = [VP, U32, U32, U32, U32, VP, U64, U64, VP]
+
+    def ray(self, scene, spheres, w, h, max_depth=4, first=0, count=None):
+        """Returns (rgba float32[w*h,4], (sphere_tests, plane_tests, shades))."""
+        count = w * h - first if count is None else count
+        out = np.zeros((w * h, 4), np.float32)
+        cnt = np.zeros(3, np.uint64)
+        self.lib.orc_ray(np.ascontiguousarray(scene).ctypes.data, spheres, w, h, max_depth, out.ctypes.data, first,
+                         count, cnt.ctypes.data)
+        return out, tuple(int(c) for c in cnt)
 
     def fnv1a64(self, a: np.ndarray) -> int:
         a = np.ascontiguousarray(a)
