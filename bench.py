@@ -1,42 +1,39 @@
 #!/usr/bin/env python3
-"""bench.py — BASELINE.json's headline: Mandelbrot 16384^2 x 2048 (FP64, the
-reference kernel workloads.hpp:78-100) co-executed with HGuided over N B200s.
+"""bench.py — BASELINE.json's benchmarks on B200 through the co-execution engine.
 
-One step = one Engine run over the whole index space (268,435,456 work-items).
-  value  device-resident: outputs stay in each GPU's partition (no inputs).
-  e2e    the same run through the C-ABI with HOST buffers: every package's
-         out_range_for slice is copied D2H into a page-locked host buffer
-         inside the timed region (4 GiB per step).
-  roofline   dominant kernel (mandel_persistent<double>): algorithmic FP64
-         flops (8/iteration + 3/escaped pixel = 7.69796e11 per
-         step) / summed CUDA-event kernel time, against the DFMA peak measured
-         on this device by ecl_probe_vector_peaks.
-  cpu_baseline   the reference engine itself (oracle/_ref, wall mode, H
-         NativePool devices x 1 worker, Dynamic{max(64,16H)}) on a 4096^2
-         sub-grid of the same viewport and iteration cap.
---impl reference times that same CPU reference as the reference arm.
+Default (the driver's line): Mandelbrot 16384^2 x 2048 (FP64, the reference
+kernel workloads.hpp:78-100) co-executed with HGuided over N B200s.
+`--workload` selects the other BASELINE configs (gaussian, nbody, binomial,
+ray, mandelbrot_f32); same JSON contract.
+
+One step = one Engine run over the whole index space (NBody: 10 timesteps).
+  value   inputs already resident in HBM, outputs left in each GPU's
+          partition; CUDA events on the bench stream around K steps.
+  e2e     the same run through the C-ABI with HOST buffers: page-locked
+          inputs are uploaded (H2D + NVLink replication) and every package's
+          out_range_for slice is copied D2H inside the timed region.
+  roofline   algorithmic flops per step / step time, against
+          the vector peak measured on this device (ecl_probe_vector_peaks;
+          MEASURED_PEAKS.json has HBM and bf16 only).
+  cpu_baseline   the reference engine itself (oracle/_ref: wall mode, H
+          NativePool devices x 1 worker, Dynamic{max(64,16H)}) on a bounded
+          sample; for the kernels the reference lacks it drives this repo's
+          C restatement as an injected KernelFn.
+--impl reference times that CPU reference as the reference arm.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
 import sys
 import threading
-import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-W_PX, H_PX, ITERS = 16384, 16384, 2048
-VIEWPORT = (-2.5, -1.25, 1.0, 1.25)
-LWS = 256
-PIXELS = W_PX * H_PX
-# Golden facts of the config (pinned by tests/test_engine_gpu.py)
-SUM_COUNT, INSIDE = 96_141_151_663, 46_275_993
-ALG_FLOPS = 8.0 * SUM_COUNT + 3.0 * (PIXELS - INSIDE)
-SAMPLE_W = 4096  # CPU sample: 4096^2 sub-grid, same viewport and max_iter
 METRIC = "work-items/s at 1/2/4/8 B200 + HGuided co-exec efficiency & overhead vs native"
 
 
@@ -46,6 +43,247 @@ def env_int(name, default):
     except ValueError:
         return default
 
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def load_json(rel):
+    with open(os.path.join(ROOT, rel)) as f:
+        return json.load(f)
+
+
+# ---------------------------------------------------------------------------
+# workloads (BASELINE.json configs)
+
+class Workload:
+    name = ""
+    workload = ""
+    dtype = "f32"
+    bound = "fp32"
+    steps_per_run = 1
+    swaps = ()
+
+    def __init__(self, P, W, np):
+        self.P, self.W, self.np = P, W, np
+
+    def scheduler(self, n):
+        return self.P.HGuidedConfig()
+
+    def min_package(self, n):
+        return 1
+
+    def host_inputs(self):
+        return []
+
+    def cpu_sample(self, ref, inputs, threads):
+        raise NotImplementedError
+
+    def check(self, outputs):
+        return True
+
+
+class Mandelbrot(Workload):
+    name = "mandelbrot"
+    W_PX, ITERS, LWS = 16384, 2048, 256
+    VIEWPORT = (-2.5, -1.25, 1.0, 1.25)
+    SUM_COUNT, INSIDE = 96_141_151_663, 46_275_993  # SURVEY §8c golden facts
+    dtype = "f64"
+    bound = "fp64"
+    kernel = "mandelbrot"
+    workload = "mandelbrot 16384x16384 max_iter 2048 viewport (-2.5,-1.25)-(1,1.25), 4:1 uint32 out"
+
+    def spec(self):
+        return self.W.mandelbrot_spec(self.W_PX, self.W_PX, self.ITERS, lws=self.LWS, kernel=self.kernel)
+
+    def units(self):
+        return self.W_PX * self.W_PX
+
+    def flops(self):
+        return 8.0 * self.SUM_COUNT + 3.0 * (self.units() - self.INSIDE)
+
+    def min_package(self, n):
+        return 148 * 8
+
+    def scheduler(self, n):
+        return self.P.HGuidedConfig(k=2.0)
+
+    def check(self, outputs):
+        counts = outputs[0].view(self.np.uint32).reshape(-1, 4)[:, 0]
+        return (int(counts.sum(dtype=self.np.uint64)) == self.SUM_COUNT and
+                int((counts >= self.ITERS).sum()) == self.INSIDE)
+
+    def cpu_sample(self, ref, inputs, threads):
+        sw = 4096
+        prog = {"kernel": "mandelbrot", "global_work_size": sw * sw, "local_work_size": self.LWS,
+                "out_pattern": {"out_indices": 4, "work_items": 1},
+                "out_buffers": [{"name": "counts", "element_size_bytes": 4, "element_count": sw * sw * 4}],
+                "args": [sw, sw, self.ITERS] + list(self.VIEWPORT)}
+        s, _ = ref.wall_run(prog, threads, 1, max(64, 16 * threads))
+        return s, sw * sw, (f"{sw}x{sw} sub-grid of the same viewport, max_iter {self.ITERS} (1/16 of the pixels); "
+                            f"reference kernel workloads.hpp:78-100")
+
+
+class MandelbrotF32(Mandelbrot):
+    name = "mandelbrot_f32"
+    kernel = "mandelbrot_f32"
+    dtype = "f32"
+    bound = "fp32"
+    SUM_COUNT = 96_141_248_575  # FP32 restatement
+    workload = "mandelbrot_f32 16384x16384 max_iter 2048 (FP32 restatement, parity unpinned)"
+
+    def flops(self):
+        return 8.0 * self.SUM_COUNT + 3.0 * (self.units() - self.INSIDE)
+
+    def check(self, outputs):
+        counts = outputs[0].view(self.np.uint32).reshape(-1, 4)[:, 0]
+        return int(counts.sum(dtype=self.np.uint64)) == self.SUM_COUNT
+
+
+class Gaussian(Workload):
+    name = "gaussian"
+    WIDTH = HEIGHT = 4096
+    F = 31
+    workload = "gaussian 4096x4096 float image, 31x31 filter (sigma 5), clamp-to-edge, static, single device"
+
+    def spec(self):
+        return self.W.gaussian_spec(self.WIDTH, self.HEIGHT, self.F)
+
+    def scheduler(self, n):
+        return self.P.StaticConfig()
+
+    def units(self):
+        return self.WIDTH * self.HEIGHT
+
+    def flops(self):
+        return self.W.gaussian_flops(self.WIDTH, self.HEIGHT, self.F)
+
+    def host_inputs(self):
+        return self.W.gaussian_inputs(self.WIDTH, self.HEIGHT, self.F, seed=42)
+
+    def check(self, outputs):
+        out = outputs[0].view(self.np.float32)
+        # a normalized positive filter over U[0,1) keeps pixels in [0,1) with mean ~0.5
+        return bool(self.np.isfinite(out).all() and out.min() >= 0 and out.max() < 1 and abs(out.mean() - 0.5) < 0.01)
+
+    def cpu_sample(self, ref, inputs, threads):
+        n = self.units()
+        out = self.np.zeros(n, self.np.float32)
+        s = ref.wall_run_restated("gaussian", inputs, out, n, 1, [self.WIDTH, self.HEIGHT, self.F], threads)
+        return s, n, "full 4096x4096 image; restated kernel oracle.c:orc_gaussian injected as KernelFn"
+
+
+class NBody(Workload):
+    name = "nbody"
+    N = 1 << 20
+    steps_per_run = 10
+    swaps = ((0, 0), (1, 1))
+    workload = "nbody 1048576 bodies x 10 timesteps, dt 0.005, eps2 500, dynamic, NVLink owner-slice exchange"
+
+    def spec(self):
+        return self.W.nbody_spec(self.N)
+
+    def scheduler(self, n):
+        return self.P.DynamicConfig(max(8, 4 * n))
+
+    def units(self):
+        return self.N * self.steps_per_run
+
+    def flops(self):
+        return self.W.nbody_flops(self.N, self.steps_per_run)
+
+    def host_inputs(self):
+        return self.W.nbody_inputs(self.N, seed=42)
+
+    def check(self, outputs):
+        pos = outputs[0].view(self.np.float32).reshape(-1, 4)
+        return bool(self.np.isfinite(pos).all() and (pos[:, 3] >= 1).all())
+
+    def cpu_sample(self, ref, inputs, threads):
+        targets = 8192
+        out = self.np.zeros((self.N, 4), self.np.float32)
+        s = ref.wall_run_restated("nbody", inputs, out, targets, self.N // targets, [self.N, 0.005, 500.0], threads)
+        return s, targets, (f"{targets} target bodies (stride {self.N // targets}) x all {self.N} sources x 1 step; "
+                            "restated kernel oracle.c:orc_nbody_step")
+
+
+class Binomial(Workload):
+    name = "binomial"
+    OPTIONS = 8 * 1024 * 1024
+    STEPS = 254
+    workload = "binomial 8388608 options x 254 steps (2097152 float4 work-groups of 255), hguided"
+
+    def spec(self):
+        return self.W.binomial_spec(self.OPTIONS, self.STEPS)
+
+    def units(self):
+        return self.OPTIONS
+
+    def flops(self):
+        return self.W.binomial_flops(self.OPTIONS, self.STEPS)
+
+    def min_package(self, n):
+        return 148 * 8
+
+    def host_inputs(self):
+        return self.W.binomial_inputs(self.OPTIONS, seed=42)
+
+    def check(self, outputs):
+        call = outputs[0].view(self.np.float32)
+        return bool(self.np.isfinite(call).all() and (call >= 0).all() and (call <= 30.0001).all())
+
+    def cpu_sample(self, ref, inputs, threads):
+        stride = 64
+        n = self.OPTIONS // stride
+        out = self.np.zeros(self.OPTIONS, self.np.float32)
+        s = ref.wall_run_restated("binomial", inputs, out, n, stride, [self.STEPS], threads)
+        return s, n, f"{n} options (every {stride}th) x {self.STEPS} steps; restated kernel oracle.c:orc_binomial"
+
+
+class Ray(Workload):
+    name = "ray"
+    WIDTH = HEIGHT = 8192
+    SPHERES, DEPTH = 64, 4
+    workload = "ray 8192x8192, 64 spheres + plane, 3 lights, shadows, reflections depth 4, hguided"
+
+    def spec(self):
+        return self.W.ray_spec(self.WIDTH, self.HEIGHT, self.SPHERES, self.DEPTH)
+
+    def units(self):
+        return self.WIDTH * self.HEIGHT
+
+    def flops(self):
+        return load_json("tests/golden/ray_counts.json")["8192x8192"]["flops"]
+
+    def min_package(self, n):
+        return 148 * 4
+
+    def host_inputs(self):
+        return [self.W.ray_scene(self.SPHERES, seed=42)]
+
+    def check(self, outputs):
+        g = load_json("tests/golden/ray_counts.json")["8192x8192"]
+        img = outputs[0].view(self.np.float32).reshape(-1, 4)
+        hist = self.np.bincount(img[:, 3].astype(int), minlength=len(g["bounce_histogram"]))
+        return [int(x) for x in hist] == g["bounce_histogram"]
+
+    def cpu_sample(self, ref, inputs, threads):
+        stride = 16
+        n = self.units() // stride
+        out = self.np.zeros((self.units(), 4), self.np.float32)
+        s = ref.wall_run_restated("ray", inputs, out, n, stride,
+                                  [self.WIDTH, self.HEIGHT, self.SPHERES, self.DEPTH], threads)
+        return s, n, f"{n} pixels (every {stride}th of 8192^2); restated kernel oracle.c:orc_ray"
+
+
+WORKLOADS = {c.name: c for c in (Mandelbrot, MandelbrotF32, Gaussian, NBody, Binomial, Ray)}
+
+
+# ---------------------------------------------------------------------------
+# clocks
 
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
@@ -57,7 +295,6 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.samples = []
-        self._stop = threading.Event()
         self._proc = None
         self._thread = None
 
@@ -90,90 +327,84 @@ class ClockSampler:
             self._thread.join(timeout=5)
         return self.summary()
 
+    @staticmethod
+    def _num(v):
+        try:
+            return float(v)
+        except ValueError:
+            return None
+
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = sorted(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
-        mx = max((float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()), default=None)
+        sm = sorted(x for x in (self._num(s[1]) for s in self.samples) if x is not None)
+        mx = max((x for x in (self._num(s[2]) for s in self.samples) if x is not None), default=None)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         for s in self.samples:
-            for n, v in zip(names, s[5:9]):
+            for nm, v in zip(names, s[5:9]):
                 if v.lower().startswith("active"):
-                    reasons.add(n)
-        power = [float(s[3]) for s in self.samples if s[3].replace(".", "").isdigit()]
+                    reasons.add(nm)
+        power = [x for x in (self._num(s[3]) for s in self.samples) if x is not None]
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(self.samples), "power_w_max": max(power) if power else None}
 
 
-def mandel_program_json(w, h):
-    return {"kernel": "mandelbrot", "global_work_size": w * h, "local_work_size": LWS,
-            "out_pattern": {"out_indices": 4, "work_items": 1},
-            "out_buffers": [{"name": "counts", "element_size_bytes": 4, "element_count": w * h * 4}],
-            "args": [w, h, ITERS] + list(VIEWPORT)}
+def merge_clocks(*cs):
+    cs = [c for c in cs if c]
+    sm = [c["sm_mhz"] for c in cs if c.get("sm_mhz")]
+    return {"sm_mhz": min(sm) if sm else None, "sm_max_mhz": max((c["sm_max_mhz"] or 0) for c in cs) or None,
+            "reasons": sorted(set().union(*[set(c["reasons"]) for c in cs])),
+            "samples": sum(c["samples"] for c in cs),
+            "power_w_max": max((c.get("power_w_max") or 0) for c in cs) or None}
 
 
-def cpu_threads():
-    try:
-        return len(os.sched_getaffinity(0))
-    except AttributeError:
-        return os.cpu_count() or 1
-
-
-def cpu_reference_sample(steps: int = 1):
-    """Times the reference engine (oracle/_ref) on the 4096^2 sample; falls
-    back to the repo's C restatement (oracle/_build) when _ref is absent."""
-    from tests import _oracle
-    h = cpu_threads()
-    prog = mandel_program_json(SAMPLE_W, SAMPLE_W)
-    ref = _oracle.Reference.load()
-    times = []
-    if ref is not None:
-        kind = "reference"
-        for _ in range(steps):
-            s, _fnv = ref.wall_run(prog, h, 1, max(64, 16 * h))
-            times.append(s)
-    else:
-        kind = "port"
-        o = _oracle.Oracle()
-        for _ in range(steps):
-            t0 = time.perf_counter()
-            o.mandelbrot(SAMPLE_W, SAMPLE_W, ITERS)
-            times.append(time.perf_counter() - t0)
-    px = SAMPLE_W * SAMPLE_W
-    return {"kind": kind, "cores": h if kind == "reference" else _oracle.Oracle().threads(), "times_s": times,
-            "value": px / (sum(times) / len(times)),
-            "sample": f"{SAMPLE_W}x{SAMPLE_W} sub-grid of the same viewport, max_iter {ITERS} "
-                      f"({px} px = 1/16 of the config); reference engine wall mode, {h} NativePool devices x 1 "
-                      f"worker, Dynamic{{{max(64, 16 * h)}}}" if kind == "reference" else
-                      f"{SAMPLE_W}x{SAMPLE_W} sub-grid, oracle/oracle.c OpenMP restatement"}
-
+# ---------------------------------------------------------------------------
+# arms
 
 def init_dist():
-    world = env_int("WORLD_SIZE", 1)
-    rank = env_int("RANK", 0)
-    local = env_int("LOCAL_RANK", 0)
-    return world, rank, local
+    return env_int("WORLD_SIZE", 1), env_int("RANK", 0), env_int("LOCAL_RANK", 0)
+
+
+def reference_measure(wl, steps, threads):
+    """Times the reference engine on the workload's bounded sample."""
+    from tests import _oracle
+    ref = _oracle.Reference.load()
+    if ref is None:
+        raise RuntimeError("oracle/_ref is not built (make -C oracle where /root/reference exists)")
+    inputs = wl.host_inputs()
+    times, units, sample = [], 0, ""
+    for _ in range(steps):
+        s, units, sample = wl.cpu_sample(ref, inputs, threads)
+        times.append(s)
+    return times, units, sample
 
 
 def run_reference(args, world, rank):
     if rank != 0:
         return 0
-    steps = args.warmup + args.steps
-    res = cpu_reference_sample(steps)
-    timed = res["times_s"][args.warmup:]
-    value = SAMPLE_W * SAMPLE_W / (sum(timed) / len(timed))
+    import numpy as np
+    import paper_1805_02755_b200 as P
+    from paper_1805_02755_b200 import workloads as W
+    wl = WORKLOADS[args.workload](P, W, np)
+    h = cpu_threads()
+    times, units, sample = reference_measure(wl, args.warmup + args.steps, h)
+    timed = times[args.warmup:] or times
+    sec = sum(timed) / len(timed)
+    value = units / sec
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "work-items/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(timed) / len(timed),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "mandelbrot 16384x16384 max_iter 2048 (sampled: 4096x4096 sub-grid)",
-                       "scheduler": f"dynamic(packages={max(64, 16 * cpu_threads())})", "lws": LWS,
-                       "viewport": list(VIEWPORT)},
-            "cpu_baseline": {"value": value, "unit": "work-items/s", "cores": res["cores"], "kind": res["kind"],
-                             "sample": res["sample"]},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic",
+            "config": {"workload": wl.workload + " (sampled)", "sample": sample,
+                       "scheduler": f"dynamic(packages={max(64, 16 * h)})"},
+            "cpu_baseline": {"value": value, "unit": "work-items/s", "cores": h, "kind": "reference",
+                             "sample": sample},
             "e2e": {"value": value, "unit": "work-items/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+BARRIERS = 6  # barrier() calls bench_engine makes (ranks > 0 mirror them)
 
 
 def run_ours(args, world, rank, local):
@@ -182,9 +413,9 @@ def run_ours(args, world, rank, local):
 
     import paper_1805_02755_b200 as P
     from paper_1805_02755_b200 import _native as N
+    from paper_1805_02755_b200 import workloads as W
 
-    ngpu_visible = P.gpu_count()
-    if ngpu_visible < 1:
+    if P.gpu_count() < 1:
         print(json.dumps({"error": "no CUDA device visible"}))
         return 1
     dist = world > 1
@@ -194,9 +425,9 @@ def run_ours(args, world, rank, local):
         td.init_process_group("nccl", device_id=torch.device("cuda", local))
     # EngineCL's co-execution model: one host coordinator drives every device
     # of the box through its per-device threads (engine.hpp:354-405).  Under
-    # torchrun, rank 0 owns the engine over GPUs 0..N-1; the other ranks only
-    # join the barriers.
-    n = args.gpus if not dist else world
+    # torchrun rank 0 owns the engine over GPUs 0..N-1; the other ranks join
+    # the barriers.
+    n = world if dist else args.gpus
     torch.cuda.set_device(local if dist else 0)
 
     def barrier():
@@ -206,10 +437,10 @@ def run_ours(args, world, rank, local):
 
     line = None
     if rank == 0:
-        line = bench_engine(args, n, P, N, np, torch, barrier)
+        wl = WORKLOADS[args.workload](P, W, np)
+        line = bench_engine(args, n, wl, P, N, np, torch, barrier)
     else:
-        # follow rank 0's barrier sequence (warm-up/time/e2e/native phases)
-        for _ in range(6):
+        for _ in range(BARRIERS):
             barrier()
     if dist:
         torch.distributed.destroy_process_group()
@@ -218,124 +449,137 @@ def run_ours(args, world, rank, local):
     return 0
 
 
-def bench_engine(args, n, P, N, np, torch, barrier):
-    from paper_1805_02755_b200 import workloads as W
-    import ctypes
-
-    sms = 148
-    min_wg = args.min_package if args.min_package else sms * 8
+def bench_engine(args, n, wl, P, N, np, torch, barrier):
+    min_wg = args.min_package if args.min_package else wl.min_package(n)
     devs = [P.cuda_device(f"gpu{i}", ordinal=i % P.gpu_count(), power=1.0, queue_depth=args.queue_depth,
                           min_package_work_groups=min_wg) for i in range(n)]
-    sched = P.HGuidedConfig(k=args.k, adaptive=args.adaptive)
-    prog = P.validate_program(W.mandelbrot_spec(W_PX, H_PX, ITERS, lws=LWS))
+    sched = wl.scheduler(n)
+    if isinstance(sched, P.HGuidedConfig):
+        sched.k = args.k
+        sched.adaptive = args.adaptive
+    prog = P.validate_program(wl.spec())
     eng = P.Engine(P.EngineConfig(devs, sched), prog)
     stream = torch.cuda.current_stream()
+
+    # page-locked host buffers (inputs for the e2e H2D, outputs for the D2H)
+    host_in = wl.host_inputs()
+    pinned_in = []
+    for a in host_in:
+        pb = P.PinnedBuffer(a.nbytes, np.uint8)
+        pb.array[:] = np.ascontiguousarray(a).reshape(-1).view(np.uint8)
+        pinned_in.append(pb)
+    in_arrays = [pb.array for pb in pinned_in]
+    pinned_out = [P.PinnedBuffer(b.size_bytes(), np.uint8) for b in prog.spec().out_buffers]
+    out_arrays = [pb.array for pb in pinned_out]
+
+    def run(inputs, outputs):
+        if wl.steps_per_run > 1:
+            eng.run_steps(inputs, outputs, wl.steps_per_run, wl.swaps, want_trace=False)
+        else:
+            eng.run_into(inputs, outputs, want_trace=False)
 
     def timed(fn, steps):
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        traces = [fn() for _ in range(steps)]
+        for _ in range(steps):
+            fn()
         e1.record(stream)
         barrier()
-        return e0.elapsed_time(e1) / steps, traces
+        return e0.elapsed_time(e1) / steps
 
-    # --- device-resident (value) ---
-    for _ in range(args.warmup):
-        eng.run_into([], None)
+    # --- device-resident (value): inputs uploaded once before timing ---
+    run(in_arrays, None)
+    for _ in range(max(0, args.warmup - 1)):
+        run(None, None)
     eng.kernel_timing(reset=True)
     sampler = ClockSampler(0).start()
-    ms_dev, _ = timed(lambda: eng.run_into([], None, want_trace=False), args.steps)
+    ms_dev = timed(lambda: run(None, None), args.steps)
     clocks = sampler.stop()
     kernel_ms, launches = eng.kernel_timing(reset=True)
     last = eng.last_trace()
     bal = P.balance(last) if n > 1 else 1.0
 
-    # parity sanity on a device-resident result (golden facts, no oracle)
-    pinned = P.PinnedBuffer(PIXELS * 16, np.uint32)
-    out = pinned.array
-    eng.gather([out])
-    counts = out.reshape(-1, 4)[:, 0]
-    exact = int(counts.sum(dtype=np.uint64)) == SUM_COUNT and int((counts >= ITERS).sum()) == INSIDE
-
-    # --- end to end through the C-ABI with a page-locked host output ---
+    # --- end to end through the C-ABI with page-locked host buffers ---
     for _ in range(args.warmup):
-        eng.run_into([], [out])
+        run(in_arrays, out_arrays)
+    for a in out_arrays:
+        a[:] = 0
     sampler2 = ClockSampler(0).start()
-    out[:] = 0
-    ms_e2e, _ = timed(lambda: eng.run_into([], [out], want_trace=False), args.steps)
+    ms_e2e = timed(lambda: run(in_arrays, out_arrays), args.steps)
     clocks2 = sampler2.stop()
     eng.kernel_timing(reset=True)
-    exact_e2e = int(counts.sum(dtype=np.uint64)) == SUM_COUNT and int((counts >= ITERS).sum()) == INSIDE
+    sane = wl.check(out_arrays)
 
     # --- native single-kernel baseline (overhead denominator) ---
     barrier()
     native_k, native_e2e = [], []
-    for _ in range(args.warmup + args.steps):
-        native_k.append(eng.native_run([], None)[0])
-    for _ in range(max(1, args.steps)):
-        native_e2e.append(eng.native_run([], [out])[1])
-    native_k = native_k[args.warmup:]
-    k_native = sorted(native_k)[len(native_k) // 2]
-    t_native_e2e = sorted(native_e2e)[len(native_e2e) // 2]
+    if wl.steps_per_run == 1:
+        for _ in range(args.warmup + args.steps):
+            native_k.append(eng.native_run(None, None)[0])
+        for _ in range(max(1, args.steps)):
+            native_e2e.append(eng.native_run(in_arrays, out_arrays)[1])
+        native_k = native_k[args.warmup:]
     barrier()
+    k_native = sorted(native_k)[len(native_k) // 2] if native_k else None
+    t_native_e2e = sorted(native_e2e)[len(native_e2e) // 2] if native_e2e else None
 
-    # --- roofline: measured FP64 peak on this device ---
+    # --- roofline: vector peaks measured on this device ---
     f64, add, f32 = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
     N.lib.ecl_probe_vector_peaks(0, ctypes.byref(f64), ctypes.byref(add), ctypes.byref(f32))
-    kernel_ms_per_step = kernel_ms / args.steps
-    # Packages overlap on the device's two compute lanes, so summed launch
-    # times double-count the overlap: the achieved rate is taken over the whole
-    # device-resident step (every FP64 op of the step / step time).
-    achieved = ALG_FLOPS / (ms_dev * 1e-3) / 1e12
-    peak = f64.value
+    peak = f64.value if wl.bound == "fp64" else f32.value
+    achieved = wl.flops() / (ms_dev * 1e-3) / 1e12
     eng.close()
-    del out, counts
-    pinned.free()
+    h2d = sum(a.nbytes for a in in_arrays)
+    d2h = sum(a.nbytes for a in out_arrays)
+    del in_arrays, out_arrays
+    for pb in pinned_in + pinned_out:
+        pb.free()
 
     cpu = None
     if n == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference_sample(1)
+        try:
+            h = cpu_threads()
+            times, units_s, sample = reference_measure(wl, 1, h)
+            cpu = {"value": units_s / times[0], "unit": "work-items/s", "cores": h, "kind": "reference",
+                   "sample": sample + f"; reference engine wall mode, {h} NativePool devices x 1 worker, "
+                                      f"Dynamic{{{max(64, 16 * h)}}}"}
+        except Exception as exc:  # noqa: BLE001 — report it, keep the GPU line
+            cpu = {"value": None, "unit": "work-items/s", "cores": cpu_threads(), "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
 
-    value = PIXELS / (ms_dev * 1e-3)
+    units = wl.units()
     line = {
-        "metric": METRIC, "value": value, "unit": "work-items/s", "n_gpus": n, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_dev, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "mandelbrot 16384x16384 max_iter 2048 viewport (-2.5,-1.25)-(1,1.25), 4:1 uint32 out",
-                   "scheduler": P.describe(sched), "lws": LWS, "min_package_work_groups": min_wg,
-                   "queue_depth": args.queue_depth, "parallelism": f"coexec{n}",
-                   "l2": "outputs 4 GiB per step (> 126 MB L2); no inputs"},
-        "e2e": {"value": PIXELS / (ms_e2e * 1e-3), "unit": "work-items/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": PIXELS * 16, "ms_per_step": ms_e2e,
-                "note": "mandelbrot reads no input buffers (workloads.hpp:188-189); its 7 scalar args travel in "
-                        "the launch parameters; D2H = every package's 4:1 uint32 slice into pinned host memory"},
-        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "metric": METRIC, "value": units / (ms_dev * 1e-3), "unit": "work-items/s", "n_gpus": n,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic",
+        "config": {"workload": wl.workload, "scheduler": P.describe(sched), "lws": prog.local_work_size(),
+                   "work_items_per_step": units, "min_package_work_groups": min_wg, "queue_depth": args.queue_depth,
+                   "parallelism": f"coexec{n}",
+                   "l2": "no L2 flush: per-step outputs (and inputs) are streamed once; Mandelbrot writes 4 GiB/step"},
+        "e2e": {"value": units / (ms_e2e * 1e-3), "unit": "work-items/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
+        "roofline": {"bound": wl.bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": None,
-                     "kernel": "mandel_persistent<double,16>",
+                     "algorithmic_flops_per_step": wl.flops(),
                      "achieved_basis": "algorithmic flops per step / device-resident step time (packages overlap "
-                                       "on two compute lanes; summed launch time double-counts)",
-                     "algorithmic": "8 FP64 flops/iteration + 3/escaped pixel = 7.69796e11 per step (SURVEY §8d)",
-                     "peak_source": "DFMA chains measured on this GPU by ecl_probe_vector_peaks (MEASURED_PEAKS.json "
-                                    "has no FP64 figure)",
-                     "nonfma_ceiling_frac": 8.0 / 14.0,
-                     "fp64_dadd_tinstr_s": add.value, "fp32_ffma_tflops": f32.value},
-        "coexec": {"balance": bal, "packages_per_step": len(last.packages),
-                   "native_kernel_ms": k_native, "engine_ms": ms_dev,
-                   "overhead_pct_device": (ms_dev - k_native) / k_native * 100.0,
-                   "native_e2e_ms": t_native_e2e, "engine_e2e_ms": ms_e2e,
-                   "overhead_pct_e2e": (ms_e2e - t_native_e2e) / t_native_e2e * 100.0,
-                   "kernel_ms_per_step": kernel_ms_per_step,
-                   "bit_exact_sums": bool(exact and exact_e2e)},
+                                       "on two compute lanes, so summed launch time double-counts)",
+                     "peak_source": f"{'DFMA' if wl.bound == 'fp64' else 'FFMA'} chains measured on this GPU by "
+                                    "ecl_probe_vector_peaks (MEASURED_PEAKS.json has no FP64/FP32 vector figure)",
+                     "fp64_dfma_tflops": f64.value, "fp64_dadd_tinstr_s": add.value, "fp32_ffma_tflops": f32.value},
+        "coexec": {"balance": bal, "packages_per_step": len(last.packages), "native_kernel_ms": k_native,
+                   "engine_ms": ms_dev, "native_e2e_ms": t_native_e2e, "engine_e2e_ms": ms_e2e,
+                   "overhead_pct_device": (ms_dev - k_native) / k_native * 100.0 if k_native else None,
+                   "overhead_pct_e2e": (ms_e2e - t_native_e2e) / t_native_e2e * 100.0 if t_native_e2e else None,
+                   "kernel_ms_per_step": kernel_ms / args.steps, "outputs_sane": bool(sane)},
         "gpu_launches": launches,
-        "clocks": {"sm_mhz": clocks["sm_mhz"], "sm_max_mhz": clocks["sm_max_mhz"],
-                   "reasons": sorted(set(clocks["reasons"]) | set(clocks2["reasons"])),
-                   "samples": clocks["samples"] + clocks2["samples"], "power_w_max": clocks.get("power_w_max")},
+        "clocks": merge_clocks(clocks, clocks2),
     }
+    if wl.bound == "fp64":
+        line["roofline"]["nonfma_ceiling_frac"] = 8.0 / 14.0
     if cpu is not None:
-        line["cpu_baseline"] = {"value": cpu["value"], "unit": "work-items/s", "cores": cpu["cores"],
-                                "kind": cpu["kind"], "sample": cpu["sample"]}
+        line["cpu_baseline"] = cpu
     return line
 
 
@@ -345,13 +589,15 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="mandelbrot")
     ap.add_argument("--k", type=float, default=2.0, help="HGuided k")
     ap.add_argument("--adaptive", action="store_true", help="HGuided powers from measured throughput")
     ap.add_argument("--queue-depth", type=int, default=2)
     ap.add_argument("--min-package", type=int, default=0, help="HGuided minimum package (work-groups)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
-    args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
+    if args.impl == "ours":
+        args.warmup = max(3, args.warmup)
     world, rank, local = init_dist()
     if args.impl == "reference":
         return run_reference(args, world, rank)

@@ -191,7 +191,7 @@ static inline int64_t clampi(int64_t v, int64_t lo, int64_t hi) { return v < lo 
 void orc_gaussian(const float* img, const float* filt, float* out, uint32_t w, uint32_t h, uint32_t f,
                   uint64_t first, uint64_t count) {
   const int64_t r = (int64_t)f / 2;
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if (count > 256)
   for (int64_t k = 0; k < (int64_t)count; ++k) {
     const uint64_t idx = first + (uint64_t)k;
     const int64_t x = (int64_t)(idx % w), y = (int64_t)(idx / w);
@@ -216,7 +216,7 @@ void orc_gaussian(const float* img, const float* filt, float* out, uint32_t w, u
 
 void orc_nbody_step(const float* pos, const float* vel, uint64_t n, float dt, float eps2, float* npos,
                     float* nvel, uint64_t first, uint64_t count) {
-#pragma omp parallel for schedule(dynamic, 16)
+#pragma omp parallel for schedule(dynamic, 16) if (count > 16)
   for (int64_t k = 0; k < (int64_t)count; ++k) {
     const uint64_t i = first + (uint64_t)k;
     const double px = pos[4 * i], py = pos[4 * i + 1], pz = pos[4 * i + 2];
@@ -267,7 +267,7 @@ void orc_nbody_init(uint64_t seed, uint64_t n, float* pos, float* vel) {
 
 void orc_binomial(const float* rand4, float* out4, uint32_t steps, uint64_t first_opt, uint64_t n_opt) {
   const double R = 0.02, V = 0.30;
-#pragma omp parallel
+#pragma omp parallel if (n_opt > 16)
   {
     double call[1024];
 #pragma omp for schedule(static)
@@ -449,7 +449,7 @@ static void trace_pixel(const float* scene, uint32_t ns, uint32_t w, uint32_t h,
 void orc_ray(const float* scene, uint32_t ns, uint32_t w, uint32_t h, uint32_t max_depth, float* out4,
              uint64_t first, uint64_t count, uint64_t* counts3) {
   uint64_t st = 0, pt = 0, sh = 0;
-#pragma omp parallel for schedule(dynamic, 256) reduction(+ : st, pt, sh)
+#pragma omp parallel for schedule(dynamic, 256) reduction(+ : st, pt, sh) if (count > 256)
   for (int64_t k = 0; k < (int64_t)count; ++k) {
     RayCounts c = {0, 0, 0};
     const uint64_t idx = first + (uint64_t)k;

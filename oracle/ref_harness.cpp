@@ -25,6 +25,17 @@
 
 using namespace coexec;
 
+// This repo's C restatements (oracle/oracle.c), linked into the same library.
+extern "C" {
+void orc_gaussian(const float* img, const float* filt, float* out, uint32_t w, uint32_t h, uint32_t f, uint64_t first,
+                  uint64_t count);
+void orc_nbody_step(const float* pos, const float* vel, uint64_t n, float dt, float eps2, float* npos, float* nvel,
+                    uint64_t first, uint64_t count);
+void orc_binomial(const float* rand4, float* out4, uint32_t steps, uint64_t first_opt, uint64_t n_opt);
+void orc_ray(const float* scene, uint32_t ns, uint32_t w, uint32_t h, uint32_t max_depth, float* out4, uint64_t first,
+             uint64_t count, uint64_t* counts3);
+}
+
 namespace {
 
 thread_local std::string g_error;
@@ -160,6 +171,70 @@ int64_t ref_report_json(const char* trace_json, const double* solo, uint32_t nso
   } catch (const std::exception& e) {
     g_error = e.what();
     return -1;
+  }
+}
+
+// CPU baseline for the kernels the reference does not have (SURVEY §8d,
+// BASELINE.md §3): the reference engine itself in wall mode (devices x 1
+// worker, Dynamic{max(64,16*devices)}) drives this repo's C restatement,
+// injected as a KernelFn through Engine::run(inputs, kernel, cost)
+// (engine.hpp:223).  Work-item i of the sampled program is item i*stride of
+// the real workload.  Returns wall seconds of Engine::run, -1 on error.
+double ref_wall_run_restated(const char* kind, const void* in0, const void* in1, void* out, uint64_t sample,
+                             uint64_t stride, const double* p, uint32_t devices) {
+  try {
+    const std::string k = kind;
+    KernelFn fn;
+    std::vector<float> scratch;
+    if (k == "gaussian") {
+      fn = [=](std::uint64_t i, std::span<const ArgValue>, const KernelBuffers&) {
+        orc_gaussian(static_cast<const float*>(in0), static_cast<const float*>(in1), static_cast<float*>(out),
+                     static_cast<uint32_t>(p[0]), static_cast<uint32_t>(p[1]), static_cast<uint32_t>(p[2]), i * stride, 1);
+      };
+    } else if (k == "nbody") {
+      scratch.resize(4 * static_cast<size_t>(p[0]));
+      float* nvel = scratch.data();
+      fn = [=](std::uint64_t i, std::span<const ArgValue>, const KernelBuffers&) {
+        orc_nbody_step(static_cast<const float*>(in0), static_cast<const float*>(in1), static_cast<uint64_t>(p[0]),
+                       static_cast<float>(p[1]), static_cast<float>(p[2]), static_cast<float*>(out), nvel, i * stride, 1);
+      };
+    } else if (k == "binomial") {
+      fn = [=](std::uint64_t i, std::span<const ArgValue>, const KernelBuffers&) {
+        orc_binomial(static_cast<const float*>(in0), static_cast<float*>(out), static_cast<uint32_t>(p[0]), i * stride, 1);
+      };
+    } else if (k == "ray") {
+      fn = [=](std::uint64_t i, std::span<const ArgValue>, const KernelBuffers&) {
+        orc_ray(static_cast<const float*>(in0), static_cast<uint32_t>(p[2]), static_cast<uint32_t>(p[0]),
+                static_cast<uint32_t>(p[1]), static_cast<uint32_t>(p[3]), static_cast<float*>(out), i * stride, 1,
+                nullptr);
+      };
+    } else {
+      throw Error(ErrorCode::UnknownKernel, "restated kernel '" + k + "'");
+    }
+    ProgramSpec spec;
+    spec.kernel = "synthetic:constant";
+    spec.global_work_size = sample;
+    spec.local_work_size = 1;
+    spec.out_buffers.push_back({"unused", 8, sample, BufferRole::Output});
+    const auto prog = validate_program(spec);
+    EngineConfig cfg;
+    for (uint32_t d = 0; d < devices; ++d) {
+      DeviceProfile dev;
+      dev.id = "cpu" + std::to_string(d);
+      dev.name = dev.id;
+      dev.backend = {BackendKind::NativePool, 1};
+      cfg.devices.push_back(dev);
+    }
+    cfg.scheduler = DynamicConfig{std::max<uint64_t>(64, 16ull * devices)};
+    cfg.clock_mode = ClockMode::Wall;
+    Engine engine(cfg, prog);
+    const CostFn cost = [](std::uint64_t) { return 1.0; };
+    const auto t0 = std::chrono::steady_clock::now();
+    engine.run({}, fn, cost);
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return -1.0;
   }
 }
 

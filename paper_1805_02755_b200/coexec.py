@@ -489,6 +489,9 @@ class Engine:
         raise EngineFailure(errors)
 
     def _check_inputs(self, inputs):
+        """inputs=None reuses the replicas already resident on the devices."""
+        if inputs is None:
+            return []
         bufs = self._prog.spec().in_buffers
         if len(inputs) != len(bufs):
             raise Error(ErrorCode.InputSizeMismatch, f"expected {len(bufs)} input buffers, got {len(inputs)}")

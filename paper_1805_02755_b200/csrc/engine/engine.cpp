@@ -98,6 +98,7 @@ struct Engine::Impl {
   ExecutionTrace last;
   std::vector<Package> last_packages;  // packages of the last wall run (for gather)
   bool last_resident = false;
+  bool inputs_resident = false;  // the devices hold replicas of every input
 
   // device-thread run protocol
   std::mutex run_m;
@@ -290,11 +291,7 @@ struct Engine::Impl {
 
   ExecutionTrace run_wall(std::span<const void* const> inputs, std::span<void* const> outputs) {
     const ProgramSpec& s = prog.spec();
-    if (inputs.size() != s.in_buffers.size())
-      throw Error(ErrorCode::InputSizeMismatch, "expected " + std::to_string(s.in_buffers.size()) +
-                                                    " input buffers, got " + std::to_string(inputs.size()));
-    for (std::size_t i = 0; i < inputs.size(); ++i)
-      if (!inputs[i]) throw Error(ErrorCode::InputSizeMismatch, "input '" + s.in_buffers[i].name + "' is null");
+    check_inputs(inputs);
     bool resident = true;
     for (void* p : outputs) resident = resident && p == nullptr;
     if (!outputs.empty() && outputs.size() != s.out_buffers.size())
@@ -307,6 +304,22 @@ struct Engine::Impl {
     ExecutionTrace t = assemble(std::move(done));
     last = t;
     return t;
+  }
+
+  // An empty input list on a program with inputs reuses the replicas already
+  // resident on the devices from an earlier run (inputs in HBM).
+  void check_inputs(std::span<const void* const> inputs) const {
+    const ProgramSpec& s = prog.spec();
+    if (inputs.empty() && !s.in_buffers.empty()) {
+      if (!inputs_resident)
+        throw Error(ErrorCode::InputSizeMismatch, "no inputs given and none resident on the devices yet");
+      return;
+    }
+    if (inputs.size() != s.in_buffers.size())
+      throw Error(ErrorCode::InputSizeMismatch, "expected " + std::to_string(s.in_buffers.size()) +
+                                                    " input buffers, got " + std::to_string(inputs.size()));
+    for (std::size_t i = 0; i < inputs.size(); ++i)
+      if (!inputs[i]) throw Error(ErrorCode::InputSizeMismatch, "input '" + s.in_buffers[i].name + "' is null");
   }
 
   std::vector<ecl_gpu*> gpus() const {
@@ -328,6 +341,7 @@ struct Engine::Impl {
     if (!inputs.empty()) {
       check(ecl_gpu_upload_inputs(g[0], const_cast<const void* const*>(inputs.data())), "upload");
       if (g.size() > 1) check(ecl_replicate_inputs(g.data(), static_cast<std::uint32_t>(g.size()), 0), "replicate");
+      inputs_resident = true;
     }
     return tally;
   }
@@ -374,8 +388,7 @@ struct Engine::Impl {
                            std::span<const std::pair<std::uint32_t, std::uint32_t>> swaps) {
     const ProgramSpec& s = prog.spec();
     if (steps == 0) throw Error(ErrorCode::ConfigError, "run_steps needs at least one step");
-    if (inputs.size() != s.in_buffers.size())
-      throw Error(ErrorCode::InputSizeMismatch, "expected " + std::to_string(s.in_buffers.size()) + " input buffers");
+    check_inputs(inputs);
     for (const auto& [i, o] : swaps)
       if (i >= s.in_buffers.size() || o >= s.out_buffers.size() ||
           s.in_buffers[i].size_bytes() != s.out_buffers[o].size_bytes())
@@ -562,11 +575,14 @@ struct Engine::Impl {
   NativeResult native_run(std::span<const void* const> inputs, std::span<void* const> outputs) {
     if (!wall()) throw Error(ErrorCode::ConfigError, "native_run needs cuda devices");
     const ProgramSpec& s = prog.spec();
-    if (inputs.size() != s.in_buffers.size()) throw Error(ErrorCode::InputSizeMismatch, "native_run: input count");
+    check_inputs(inputs);
     ecl_gpu* g = devices[0]->gpu;
     check(ecl_gpu_sync(g), "sync");
     const auto t0 = Clock::now();
-    if (!inputs.empty()) check(ecl_gpu_upload_inputs(g, const_cast<const void* const*>(inputs.data())), "upload");
+    if (!inputs.empty()) {
+      check(ecl_gpu_upload_inputs(g, const_cast<const void* const*>(inputs.data())), "upload");
+      if (devices.size() == 1) inputs_resident = true;
+    }
     float kms = 0.f;
     check(ecl_gpu_native_run(g, &kms), "native run");
     for (std::uint32_t b = 0; b < outputs.size(); ++b)

@@ -142,6 +142,19 @@ class Reference:
         lib.ref_wall_run.restype = D
         lib.ref_wall_run.argtypes = [ctypes.c_char_p, U32, U32, U64, U64, ctypes.POINTER(U64)]
 
+    def wall_run_restated(self, kind, inputs, out, sample, stride, params, devices):
+        """Reference engine (wall mode) driving oracle.c's restated kernel."""
+        f = self.lib.ref_wall_run_restated
+        f.restype = D
+        f.argtypes = [ctypes.c_char_p, VP, VP, VP, U64, U64, ctypes.POINTER(D), U32]
+        ins = [np.ascontiguousarray(a) for a in inputs] + [None, None]
+        p = (D * len(params))(*params)
+        s = f(kind.encode(), ins[0].ctypes.data if ins[0] is not None else None,
+              ins[1].ctypes.data if ins[1] is not None else None, out.ctypes.data, sample, stride, p, devices)
+        if s < 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return s
+
     def mandelbrot(self, w, h, it, viewport=(-2.5, -1.25, 1.0, 1.25)):
         out = np.zeros(w * h, np.uint32)
         self.lib.ref_mandelbrot_counts(w, h, it, *viewport, 0, w * h, out.ctypes.data)
