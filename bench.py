@@ -452,7 +452,7 @@ def run_ours(args, world, rank, local):
 def bench_engine(args, n, wl, P, N, np, torch, barrier):
     min_wg = args.min_package if args.min_package else wl.min_package(n)
     devs = [P.cuda_device(f"gpu{i}", ordinal=i % P.gpu_count(), power=1.0, queue_depth=args.queue_depth,
-                          min_package_work_groups=min_wg) for i in range(n)]
+                          min_package_work_groups=min_wg, widen_per_8=args.widen) for i in range(n)]
     sched = wl.scheduler(n)
     if isinstance(sched, P.HGuidedConfig):
         sched.k = args.k
@@ -556,6 +556,7 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier):
         "scaling": "strong", "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic",
         "config": {"workload": wl.workload, "scheduler": P.describe(sched), "lws": prog.local_work_size(),
                    "work_items_per_step": units, "min_package_work_groups": min_wg, "queue_depth": args.queue_depth,
+                   "widen_per_8": args.widen,
                    "parallelism": f"coexec{n}",
                    "l2": "no L2 flush: per-step outputs (and inputs) are streamed once; Mandelbrot writes 4 GiB/step"},
         "e2e": {"value": units / (ms_e2e * 1e-3), "unit": "work-items/s", "h2d_bytes_per_step": h2d,
@@ -594,6 +595,8 @@ def main(argv=None):
     ap.add_argument("--adaptive", action="store_true", help="HGuided powers from measured throughput")
     ap.add_argument("--queue-depth", type=int, default=2)
     ap.add_argument("--min-package", type=int, default=0, help="HGuided minimum package (work-groups)")
+    ap.add_argument("--widen", type=int, default=8,
+                    help="replicated outputs: pieces of 8 copied compact and widened on the host")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
     if args.impl == "ours":

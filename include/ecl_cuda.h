@@ -137,11 +137,16 @@ int ecl_gpu_submit(ecl_gpu* gpu, uint64_t seq, uint64_t offset_wg, uint64_t size
 /* ECL_OK when package `seq` (and its copies) completed, ECL_PENDING while
  * running, ECL_KERNEL_PANIC on a device fault. */
 int ecl_gpu_poll(ecl_gpu* gpu, uint64_t seq);
-/* Start/end of the package's kernel on the host steady clock (ms), mapped
- * through the epoch set by ecl_gpu_set_epoch.  Valid after completion. */
+/* Blocks until package `seq` and its copies completed (event wait; returns
+ * ECL_KERNEL_PANIC on a device fault instead of hanging). */
+int ecl_gpu_wait(ecl_gpu* gpu, uint64_t seq);
+/* Start/end of the package's kernel in host steady-clock milliseconds
+ * (std::chrono::steady_clock, CLOCK_MONOTONIC), through the device's time
+ * anchor.  Valid after completion. */
 int ecl_gpu_package_times(ecl_gpu* gpu, uint64_t seq, double* t_start_ms, double* t_end_ms);
-/* Anchors device event time to host time: records an event, waits for it and
- * pairs it with host_now_ms() of the caller's clock (returned). */
+/* (Re)anchors device event time to the host steady clock when the anchor is
+ * older than 2 s (an event record + synchronize); otherwise returns at once.
+ * The clock arguments are unused (kept for ABI stability; pass NULL). */
 int ecl_gpu_set_epoch(ecl_gpu* gpu, double (*host_now_ms)(void*), void* clock_user);
 int ecl_gpu_sync(ecl_gpu* gpu);
 /* Exactly-once tally (COEXEC_TALLY=1, engine.hpp:228-252): when enabled,
@@ -158,6 +163,11 @@ int ecl_gpu_native_run(ecl_gpu* gpu, float* kernel_ms);
  * 2^23; 0 = one launch per package): bounds how much compute precedes the
  * first D2H of a package. */
 int ecl_gpu_set_copy_split(ecl_gpu* gpu, uint64_t items);
+/* For kernels whose outputs are replicated (Mandelbrot's 4 identical counts
+ * per pixel): of every 8 pieces, `per_8` copy one value per item and are
+ * widened by host threads, the others are copied whole.  Balances PCIe
+ * bytes against host-DRAM traffic (default 8 = all widened). */
+int ecl_gpu_set_widen_fraction(ecl_gpu* gpu, uint32_t per_8);
 
 /* Kernel time of the most recent submit() / native_run() launches summed
  * since the last reset (for roofline accounting). */

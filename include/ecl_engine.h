@@ -75,6 +75,26 @@ int64_t ecl_resolve_static(const char* scheduler_json, const char* devices_json,
 /* apply_default_min_package over a devices JSON array. */
 int64_t ecl_apply_default_min_package(const char* devices_json, char* buf, uint64_t cap);
 
+/* ---- cross-process coordination (one process per GPU) ----------------- */
+/* The engine uses it when its config JSON has "shared": {"name": "/shm",
+ * "rank": r, "world": w, "local_devices": [...]}; it is exposed on its own so
+ * a launcher (or a test) can drive the decision log directly:
+ * {"name", "rank", "world", "scheduler", "devices", "total_work_groups"}.
+ * begin/end are collective over the `world` processes. */
+typedef struct ecl_shared ecl_shared;
+int ecl_shared_open(const char* json, ecl_shared** out);
+void ecl_shared_close(ecl_shared* h);
+int ecl_shared_begin(ecl_shared* h, double* epoch_ms);
+/* 1 = granted, 0 = drained (or a peer failed), < 0 = error. */
+int ecl_shared_next(ecl_shared* h, uint32_t device, uint64_t* offset_wg, uint64_t* size_wg, uint64_t* seq);
+int ecl_shared_observe(ecl_shared* h, uint32_t device, uint64_t work_items, double busy_ms);
+int ecl_shared_complete(ecl_shared* h, uint64_t seq, uint32_t device, uint64_t offset_wg, uint64_t size_wg,
+                        double t_start_ms, double t_end_ms);
+int ecl_shared_fail(ecl_shared* h);
+/* Collective: every rank's completed packages as (seq, device, offset_wg,
+ * size_wg) quads in seq order; returns the count. */
+int64_t ecl_shared_end(ecl_shared* h, uint64_t* quads, uint64_t cap, int* peer_failed);
+
 /* ---- core checks ------------------------------------------------------ */
 int ecl_validate_program(const char* program_json, uint64_t* total_work_groups);
 int ecl_out_range_for(const char* program_json, uint64_t offset_wg, uint64_t size_wg, uint64_t* offset,

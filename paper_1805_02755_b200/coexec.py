@@ -66,11 +66,14 @@ class Backend:
     kind: BackendKind = BackendKind.Simulated
     ordinal: int = 0
     queue_depth: int = 2
+    copy_split_items: int = 1 << 23
+    widen_per_8: int = 8
 
     def to_json(self):
         if self.kind == BackendKind.Simulated:
             return {"kind": "simulated"}
-        return {"kind": "cuda", "ordinal": self.ordinal, "queue_depth": self.queue_depth}
+        return {"kind": "cuda", "ordinal": self.ordinal, "queue_depth": self.queue_depth,
+                "copy_split_items": self.copy_split_items, "widen_per_8": self.widen_per_8}
 
 
 @dataclass
@@ -91,15 +94,18 @@ class DeviceProfile:
     @staticmethod
     def from_json(j) -> "DeviceProfile":
         b = j.get("backend", {"kind": "simulated"})
-        backend = Backend(BackendKind(b["kind"]), b.get("ordinal", 0), b.get("queue_depth", 2))
+        backend = Backend(BackendKind(b["kind"]), b.get("ordinal", 0), b.get("queue_depth", 2),
+                          b.get("copy_split_items", 1 << 23), b.get("widen_per_8", 8))
         return DeviceProfile(j["id"], j.get("name", j["id"]), j.get("computing_power", 1.0),
                              j.get("launch_overhead_ms", 0.0), j.get("bandwidth_bytes_per_ms", 1.0), backend,
                              j.get("min_package_work_groups", 0))
 
 
 def cuda_device(id: str, ordinal: int = 0, power: float = 1.0, queue_depth: int = 2,
-                min_package_work_groups: int = 1) -> DeviceProfile:
-    return DeviceProfile(id, id, power, 0.0, 1.0, Backend(BackendKind.Cuda, ordinal, queue_depth),
+                min_package_work_groups: int = 1, widen_per_8: int = 8,
+                copy_split_items: int = 1 << 23) -> DeviceProfile:
+    return DeviceProfile(id, id, power, 0.0, 1.0,
+                         Backend(BackendKind.Cuda, ordinal, queue_depth, copy_split_items, widen_per_8),
                          min_package_work_groups)
 
 
@@ -420,11 +426,16 @@ class EngineConfig:
     seed: int = 0
     exclude_init_from_total: bool = False
     tally: bool = False
+    # One process per GPU: {"name": "/shm-name", "rank": r, "world": w, "local_devices": [r]}
+    shared: Optional[dict] = None
 
     def to_json(self, program: ProgramSpec):
-        return {"schema": 1, "program": program.to_json(), "devices": [d.to_json() for d in self.devices],
-                "scheduler": self.scheduler.to_json(), "clock_mode": self.clock_mode.value, "seed": self.seed,
-                "exclude_init": self.exclude_init_from_total, "tally": self.tally}
+        j = {"schema": 1, "program": program.to_json(), "devices": [d.to_json() for d in self.devices],
+             "scheduler": self.scheduler.to_json(), "clock_mode": self.clock_mode.value, "seed": self.seed,
+             "exclude_init": self.exclude_init_from_total, "tally": self.tally}
+        if self.shared:
+            j["shared"] = dict(self.shared)
+        return j
 
 
 @dataclass

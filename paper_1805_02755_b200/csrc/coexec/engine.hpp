@@ -24,8 +24,11 @@
 #include <utility>
 #include <vector>
 
+#include <optional>
+
 #include "coexec/core.hpp"
 #include "coexec/schedulers.hpp"
+#include "coexec/shared.hpp"
 
 namespace coexec {
 
@@ -36,6 +39,10 @@ struct EngineConfig {
   std::uint64_t seed = 0;
   bool exclude_init_from_total = false;
   bool tally = false;  // exactly-once check (also enabled by COEXEC_TALLY=1)
+  // One process per GPU: this process drives shared->local of `devices` and
+  // co-schedules with its peers through the shared-memory decision log
+  // (coexec/shared.hpp).  Unset = one process drives every device.
+  std::optional<SharedConfig> shared;
 };
 
 struct RunResult {

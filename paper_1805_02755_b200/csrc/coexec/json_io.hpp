@@ -25,7 +25,11 @@ inline std::string format_double(double v) {
 
 inline json to_json(const Backend& b) {
   if (b.kind == BackendKind::Simulated) return json{{"kind", "simulated"}};
-  return json{{"kind", "cuda"}, {"ordinal", b.ordinal}, {"queue_depth", b.queue_depth}};
+  return json{{"kind", "cuda"},
+              {"ordinal", b.ordinal},
+              {"queue_depth", b.queue_depth},
+              {"copy_split_items", b.copy_split_items},
+              {"widen_per_8", b.widen_per_8}};
 }
 
 inline Backend backend_from_json(const json& j) {
@@ -37,6 +41,8 @@ inline Backend backend_from_json(const json& j) {
     b.kind = BackendKind::Cuda;
     b.ordinal = j.value("ordinal", 0);
     b.queue_depth = j.value("queue_depth", 2u);
+    b.copy_split_items = j.value("copy_split_items", std::uint64_t{1} << 23);
+    b.widen_per_8 = j.value("widen_per_8", 8u);
   } else if (kind == "native_pool") {
     throw Error(ErrorCode::ConfigError,
                 "backend 'native_pool' (host thread pools) is replaced by 'cuda' in the B200 build");

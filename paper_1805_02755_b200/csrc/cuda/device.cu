@@ -11,19 +11,25 @@
 //                     package k's drain tail leaves idle; each lane has its
 //                     own work-claim counters.  Depth 1 uses lane[0] only,
 //                     the reference's strictly serial device.
-//   copy              D2H of every package's out_range_for slice, waiting on
-//                     the kernel (piece) events: copies of package k overlap
-//                     the kernels of k+1.
+//   copy[0], copy[1]  D2H of every package's out_range_for slice (one copy
+//                     stream per lane, so one lane's copies never queue
+//                     behind the other lane's kernels), waiting on the
+//                     kernel (piece) events: copies overlap later kernels.
+//                     Replicated outputs (Mandelbrot's 4 identical counts)
+//                     copy one value per item and are widened by host
+//                     threads (hostpool.cpp).
 //   notify            completion callbacks, after the copies; kept off the
 //                     copy stream so a host callback never stalls a DMA.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "ecl_cuda.h"
+#include "hostpool.h"
 #include "kernels.cuh"
 
 struct ecl_kernel {
@@ -63,6 +69,8 @@ struct Slot {
   bool timed = false;
   ecl_done_fn fn = nullptr;
   void* user = nullptr;
+  ecl::WidenTicket widen;               // host widening of this package's copies
+  std::vector<cudaEvent_t> piece_done;  // per-piece D2H completion (widen triggers)
 };
 
 void CUDART_CB on_package_done(void* arg) {
@@ -78,13 +86,13 @@ struct ecl_gpu {
   uint32_t depth = 2;
   int lanes = 1;
   cudaStream_t lane[kLanes] = {nullptr, nullptr};
-  cudaStream_t copy = nullptr;
+  cudaStream_t copy[kLanes] = {nullptr, nullptr};  // per lane: one lane's copies never queue behind the other's
   cudaStream_t notify = nullptr;
-  cudaEvent_t epoch = nullptr;
+  cudaEvent_t epoch = nullptr;             // anchor event: device time <-> host steady clock
   cudaEvent_t ready = nullptr;             // last input/replication write on lane 0
   cudaEvent_t piece[kLanes] = {nullptr, nullptr};  // end of a sub-launch the copy stream drains
-  cudaEvent_t copied = nullptr;            // copies of the latest package queued on `copy`
-  double epoch_host_ms = 0.0;
+  cudaEvent_t copied[kLanes] = {nullptr, nullptr};  // copies of a lane's latest package
+  double epoch_host_ms = -1.0;  // steady-clock ms of the anchor event; < 0 = not anchored
   Slot slots[kSlots];
   uint32_t next_slot = 0;  // per-device rotation: seqs are global across devices
   uint32_t next_lane = 0;
@@ -100,6 +108,11 @@ struct ecl_gpu {
   double kernel_ms = 0.0;
   uint64_t launches = 0;
   uint64_t d2h_split_items = 1ull << 23;  // sub-launch size when copies are pipelined
+  uint32_t* compact_dev = nullptr;        // replicate > 1: one value per work-item (device)
+  uint32_t* compact_host = nullptr;       // page-locked landing zone of the compact copies
+  uint64_t compact_items = 0;
+  uint32_t widen_per_8 = 8;               // pieces (of 8) copied compact and widened on the host
+  uint64_t piece_counter = 0;
 };
 
 namespace {
@@ -143,8 +156,10 @@ int join_lanes(ecl_gpu* g) {
 }
 
 int sync_all(ecl_gpu* g) {
-  for (int l = 0; l < g->lanes; ++l) ECL_CK(cudaStreamSynchronize(g->lane[l]));
-  ECL_CK(cudaStreamSynchronize(g->copy));
+  for (int l = 0; l < g->lanes; ++l) {
+    ECL_CK(cudaStreamSynchronize(g->lane[l]));
+    ECL_CK(cudaStreamSynchronize(g->copy[l]));
+  }
   ECL_CK(cudaStreamSynchronize(g->notify));
   return ECL_OK;
 }
@@ -216,15 +231,16 @@ int ecl_gpu_open(int ordinal, uint32_t queue_depth, ecl_gpu** out) {
   if (int rc = set_device(g)) return undo(rc);
   cudaError_t e = cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, ordinal);
   if (e != cudaSuccess) return undo(cuda_fail(e, "cudaDeviceGetAttribute"));
-  for (int l = 0; l < kLanes; ++l)
+  for (int l = 0; l < kLanes; ++l) {
     if ((e = cudaStreamCreateWithFlags(&g->lane[l], cudaStreamNonBlocking)) != cudaSuccess)
       return undo(cuda_fail(e, "cudaStreamCreate(lane)"));
-  if ((e = cudaStreamCreateWithFlags(&g->copy, cudaStreamNonBlocking)) != cudaSuccess)
-    return undo(cuda_fail(e, "cudaStreamCreate(copy)"));
+    if ((e = cudaStreamCreateWithFlags(&g->copy[l], cudaStreamNonBlocking)) != cudaSuccess)
+      return undo(cuda_fail(e, "cudaStreamCreate(copy)"));
+  }
   if ((e = cudaStreamCreateWithFlags(&g->notify, cudaStreamNonBlocking)) != cudaSuccess)
     return undo(cuda_fail(e, "cudaStreamCreate(notify)"));
   if ((e = cudaEventCreate(&g->epoch)) != cudaSuccess) return undo(cuda_fail(e, "cudaEventCreate"));
-  for (cudaEvent_t* ev : {&g->ready, &g->piece[0], &g->piece[1], &g->copied})
+  for (cudaEvent_t* ev : {&g->ready, &g->piece[0], &g->piece[1], &g->copied[0], &g->copied[1]})
     if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess)
       return undo(cuda_fail(e, "cudaEventCreate"));
   for (auto& s : g->slots) {
@@ -242,24 +258,30 @@ int ecl_gpu_open(int ordinal, uint32_t queue_depth, ecl_gpu** out) {
 int ecl_gpu_close(ecl_gpu* g) {
   if (!g) return ECL_OK;
   cudaSetDevice(g->ordinal);
-  for (int l = 0; l < kLanes; ++l)
+  for (int l = 0; l < kLanes; ++l) {
     if (g->lane[l]) cudaStreamSynchronize(g->lane[l]);
-  if (g->copy) cudaStreamSynchronize(g->copy);
+    if (g->copy[l]) cudaStreamSynchronize(g->copy[l]);
+  }
   if (g->notify) cudaStreamSynchronize(g->notify);
+  for (auto& s : g->slots) ecl::widen_wait(&s.widen);
   free_buffers(g);
   if (g->scratch) cudaFree(g->scratch);
   if (g->ctrl) cudaFree(g->ctrl);
   if (g->tally) cudaFree(g->tally);
+  if (g->compact_dev) cudaFree(g->compact_dev);
+  if (g->compact_host) cudaFreeHost(g->compact_host);
   for (auto& s : g->slots) {
     if (s.start) cudaEventDestroy(s.start);
     if (s.end) cudaEventDestroy(s.end);
     if (s.done) cudaEventDestroy(s.done);
+    for (cudaEvent_t ev : s.piece_done) cudaEventDestroy(ev);
   }
-  for (cudaEvent_t ev : {g->epoch, g->ready, g->piece[0], g->piece[1], g->copied})
+  for (cudaEvent_t ev : {g->epoch, g->ready, g->piece[0], g->piece[1], g->copied[0], g->copied[1]})
     if (ev) cudaEventDestroy(ev);
-  for (int l = 0; l < kLanes; ++l)
+  for (int l = 0; l < kLanes; ++l) {
     if (g->lane[l]) cudaStreamDestroy(g->lane[l]);
-  if (g->copy) cudaStreamDestroy(g->copy);
+    if (g->copy[l]) cudaStreamDestroy(g->copy[l]);
+  }
   if (g->notify) cudaStreamDestroy(g->notify);
   delete g;
   cudaGetLastError();
@@ -336,6 +358,15 @@ int ecl_gpu_bind(ecl_gpu* g, const ecl_kernel* k) {
     g->scratch_cap = 0;
     ECL_CK(cudaMalloc(&g->scratch, scratch));
     g->scratch_cap = scratch;
+  }
+  if (k->spec.replicate > 1 && g->compact_items != k->spec.gws) {
+    if (g->compact_dev) cudaFree(g->compact_dev);
+    if (g->compact_host) cudaFreeHost(g->compact_host);
+    g->compact_dev = nullptr;
+    g->compact_host = nullptr;  // the pinned landing zone is allocated on first host copy
+    g->compact_items = 0;
+    ECL_CK(cudaMalloc(&g->compact_dev, k->spec.gws * sizeof(uint32_t)));
+    g->compact_items = k->spec.gws;
   }
   ECL_CK(cudaMemsetAsync(g->ctrl, 0, kLanes * kCtrlWordsPerLane * sizeof(unsigned), g->lane[0]));
   const cudaError_t e = ecl::prepare_kernel(k->spec, env_of(g, 0));
@@ -433,8 +464,8 @@ int ecl_gpu_download_slice(ecl_gpu* g, uint32_t index, uint64_t elem_offset, uin
   if (int rc = set_device(g)) return rc;
   if (int rc = sync_all(g)) return rc;
   ECL_CK(cudaMemcpyAsync(host, static_cast<const char*>(g->out[index]) + elem_offset * esz, elem_count * esz,
-                         cudaMemcpyDeviceToHost, g->copy));
-  ECL_CK(cudaStreamSynchronize(g->copy));
+                         cudaMemcpyDeviceToHost, g->copy[0]));
+  ECL_CK(cudaStreamSynchronize(g->copy[0]));
   return ECL_OK;
 }
 
@@ -477,8 +508,12 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
   if (int rc = set_device(g)) return rc;
   if (find_slot(g, seq)) return fail(ECL_SCHEDULER_ERROR, "package seq submitted twice");
   Slot& slot = g->slots[g->next_slot];
-  g->next_slot = (g->next_slot + 1) % (kSlots - 1);        // the last slot is reserved for native_run
-  if (slot.busy) ECL_CK(cudaEventSynchronize(slot.done));  // ring wrapped: oldest must be retired
+  g->next_slot = (g->next_slot + 1) % (kSlots - 1);  // the last slot is reserved for native_run
+  if (slot.busy) {                                   // ring wrapped: oldest must be retired
+    ECL_CK(cudaEventSynchronize(slot.done));
+    ecl::widen_wait(&slot.widen);
+  }
+  slot.widen.failed.store(false);
   slot.seq = seq;
   slot.busy = true;
   slot.timed = false;
@@ -487,6 +522,7 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
   const int lane = static_cast<int>(g->next_lane);
   g->next_lane = (g->next_lane + 1) % static_cast<uint32_t>(g->lanes);
   cudaStream_t st = g->lane[lane];
+  cudaStream_t cp = g->copy[lane];
 
   bool copies = false;
   for (size_t b = 0; host_outputs && b < g->out.size(); ++b) copies = copies || host_outputs[b] != nullptr;
@@ -501,7 +537,16 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
     uint64_t po = 0, pc = 0;
     if (out_range(s, offset_wg, std::min(piece_wg, size_wg), &po, &pc) != ECL_OK) piece_wg = size_wg;
   }
-  const ecl::LaunchEnv env = env_of(g, lane);
+  // Replicated outputs (4 identical uint32 per item): copy one value per item
+  // and widen on the host (hostpool.cpp) — a quarter of the PCIe bytes.
+  const bool widen_ok = copies && s.replicate > 1 && g->compact_dev && s.outputs.size() == 1 &&
+                        s.outputs[0].element_size_bytes == 4 && s.out_indices == s.replicate &&
+                        s.out_work_items == 1 && g->widen_per_8 > 0;
+  const bool widen = widen_ok;
+  if (widen && !g->compact_host) ECL_CK(cudaHostAlloc(&g->compact_host, g->compact_items * 4, cudaHostAllocPortable));
+  ecl::LaunchEnv env = env_of(g, lane);
+  if (widen) env.compact = g->compact_dev;
+  size_t piece_no = 0;
   ECL_CK(cudaEventRecord(slot.start, st));
   for (uint64_t wg = offset_wg; wg < offset_wg + size_wg; wg += piece_wg) {
     const uint64_t n_wg = std::min(piece_wg, offset_wg + size_wg - wg);
@@ -516,20 +561,37 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
     uint64_t p_off = o_off, p_cnt = o_cnt;
     if (piece_wg != size_wg && out_range(s, wg, n_wg, &p_off, &p_cnt) != ECL_OK) return ECL_INDIVISIBLE_PACKAGE;
     ECL_CK(cudaEventRecord(g->piece[lane], st));
-    ECL_CK(cudaStreamWaitEvent(g->copy, g->piece[lane], 0));  // captures this recording
+    ECL_CK(cudaStreamWaitEvent(cp, g->piece[lane], 0));  // captures this recording
+    // widen_per_8 of every 8 pieces go compact + host widening, the rest are
+    // copied whole: balances PCIe bytes against host-DRAM traffic.
+    if (widen && (g->piece_counter++ % 8) < g->widen_per_8) {
+      ECL_CK(cudaMemcpyAsync(g->compact_host + first, g->compact_dev + first, count * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost, cp));
+      if (slot.piece_done.size() <= piece_no) {
+        cudaEvent_t ev;
+        // blocking-sync: widen workers sleep on it instead of spinning a core
+        ECL_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventBlockingSync));
+        slot.piece_done.push_back(ev);
+      }
+      cudaEvent_t ev = slot.piece_done[piece_no++];
+      ECL_CK(cudaEventRecord(ev, cp));
+      ecl::widen_async(g->ordinal, ev, g->compact_host + first,
+                       static_cast<uint32_t*>(host_outputs[0]) + p_off, count, s.replicate, &slot.widen);
+      continue;
+    }
     for (size_t b = 0; b < g->out.size(); ++b) {
       if (!host_outputs[b]) continue;
       const uint64_t esz = s.outputs[b].element_size_bytes;
       ECL_CK(cudaMemcpyAsync(static_cast<char*>(host_outputs[b]) + p_off * esz,
                              static_cast<const char*>(g->out[b]) + p_off * esz, p_cnt * esz,
-                             cudaMemcpyDeviceToHost, g->copy));
+                             cudaMemcpyDeviceToHost, cp));
     }
   }
   ECL_CK(cudaEventRecord(slot.end, st));
   ECL_CK(cudaStreamWaitEvent(g->notify, slot.end, 0));
   if (copies) {
-    ECL_CK(cudaEventRecord(g->copied, g->copy));
-    ECL_CK(cudaStreamWaitEvent(g->notify, g->copied, 0));
+    ECL_CK(cudaEventRecord(g->copied[lane], cp));
+    ECL_CK(cudaStreamWaitEvent(g->notify, g->copied[lane], 0));
   }
   if (done) ECL_CK(cudaLaunchHostFunc(g->notify, on_package_done, &slot));
   ECL_CK(cudaEventRecord(slot.done, g->notify));
@@ -541,7 +603,10 @@ int ecl_gpu_poll(ecl_gpu* g, uint64_t seq) {
   if (!sp) return fail(ECL_CONFIG_ERROR, "poll: unknown package");
   cudaSetDevice(g->ordinal);
   cudaError_t e = cudaEventQuery(sp->done);
-  if (e == cudaSuccess) return ECL_OK;
+  if (e == cudaSuccess) {
+    if (sp->widen.pending.load() != 0) return ECL_PENDING;
+    return sp->widen.failed.load() ? fail(ECL_KERNEL_PANIC, "host widening: a copy failed") : ECL_OK;
+  }
   if (e == cudaErrorNotReady) {
     cudaGetLastError();
     return ECL_PENDING;
@@ -555,6 +620,7 @@ int ecl_gpu_package_times(ecl_gpu* g, uint64_t seq, double* t_start, double* t_e
   Slot& slot = *sp;
   if (int rc = set_device(g)) return rc;
   ECL_CK(cudaEventSynchronize(slot.done));
+  ecl::widen_wait(&slot.widen);
   float a = 0.f, b = 0.f, k = 0.f;
   ECL_CK(cudaEventElapsedTime(&a, g->epoch, slot.start));
   ECL_CK(cudaEventElapsedTime(&b, g->epoch, slot.end));
@@ -571,10 +637,29 @@ int ecl_gpu_package_times(ecl_gpu* g, uint64_t seq, double* t_start, double* t_e
 }
 
 int ecl_gpu_set_epoch(ecl_gpu* g, double (*host_now_ms)(void*), void* clock_user) {
+  (void)host_now_ms;
+  (void)clock_user;
+  // Anchor device event time to the host steady clock.  Cheap when fresh:
+  // re-anchoring (an event record + synchronize on an idle lane) happens only
+  // every 2 s so cudaEventElapsedTime's float stays sub-microsecond.
+  const double now = std::chrono::duration<double, std::milli>(
+                         std::chrono::steady_clock::now().time_since_epoch()).count();
+  if (g->epoch_host_ms >= 0.0 && now - g->epoch_host_ms < 2000.0) return ECL_OK;
   if (int rc = set_device(g)) return rc;
+  if (int rc = sync_all(g)) return rc;
   ECL_CK(cudaEventRecord(g->epoch, g->lane[0]));
   ECL_CK(cudaEventSynchronize(g->epoch));
-  g->epoch_host_ms = host_now_ms ? host_now_ms(clock_user) : 0.0;
+  g->epoch_host_ms = std::chrono::duration<double, std::milli>(
+                         std::chrono::steady_clock::now().time_since_epoch()).count();
+  return ECL_OK;
+}
+
+int ecl_gpu_wait(ecl_gpu* g, uint64_t seq) {
+  Slot* sp = find_slot(g, seq);
+  if (!sp) return fail(ECL_CONFIG_ERROR, "wait: unknown package");
+  if (int rc = set_device(g)) return rc;
+  ECL_CK(cudaEventSynchronize(sp->done));
+  if (!ecl::widen_wait(&sp->widen)) return fail(ECL_KERNEL_PANIC, "host widening: a copy failed");
   return ECL_OK;
 }
 
@@ -637,6 +722,12 @@ int ecl_gpu_kernel_time(ecl_gpu* g, double* total_ms, uint64_t* launches, int re
 
 int ecl_gpu_set_copy_split(ecl_gpu* g, uint64_t items) {
   g->d2h_split_items = items;
+  return ECL_OK;
+}
+
+int ecl_gpu_set_widen_fraction(ecl_gpu* g, uint32_t per_8) {
+  if (per_8 > 8) return fail(ECL_CONFIG_ERROR, "widen fraction is per 8 pieces (0..8)");
+  g->widen_per_8 = per_8;
   return ECL_OK;
 }
 

@@ -1,0 +1,29 @@
+// hostpool.h — host thread pool that widens replicated outputs (see hostpool.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <mutex>
+
+namespace ecl {
+
+// Outstanding widen jobs of one package.
+struct WidenTicket {
+  std::atomic<int64_t> pending{0};
+  std::atomic<bool> failed{false};
+  std::mutex m;
+  std::condition_variable cv;
+};
+
+// After `ready` completes, writes `rep` copies of src[i] to dst[i*rep .. +rep)
+// for i < count, on the pool's threads.
+void widen_async(int device, cudaEvent_t ready, const uint32_t* src, uint32_t* dst, uint64_t count, uint32_t rep,
+                 WidenTicket* ticket);
+
+// Blocks until every job of the ticket finished; false if a copy failed.
+bool widen_wait(WidenTicket* ticket);
+
+}  // namespace ecl

@@ -51,6 +51,10 @@ struct KernelSpec {
   SyntheticProfile profile = SyntheticProfile::Constant;
   std::string id;
   uint64_t gws = 0, lws = 1, out_indices = 1, out_work_items = 1;
+  // > 1: each work-item's out_indices uint32 outputs are identical copies
+  // (Mandelbrot's 4:1 pattern); the kernel also writes one compact value per
+  // item (LaunchEnv::compact) so host copies move 1/replicate of the bytes.
+  uint32_t replicate = 1;
   std::vector<ecl_arg> args;
   std::vector<ecl_buffer_geom> inputs, outputs;
   // parsed arguments
@@ -72,6 +76,7 @@ struct LaunchEnv {
   void* const* out = nullptr;  // device pointers of the bound outputs
   unsigned* ctrl = nullptr;    // zeroed per-device control words (work counters)
   void* scratch = nullptr;     // per-device, per-binding kernel scratch (scratch_bytes())
+  uint32_t* compact = nullptr;  // replicate > 1 and host copies pending: one value per item
 };
 
 // Device scratch a kernel needs per binding (e.g. Mandelbrot coordinate tables),

@@ -17,7 +17,12 @@
 //  * cx/cy depend on the column/row only: they are computed once per image
 //    by coord_tables with the reference formula and looked up per pixel, so
 //    the refill path has no IEEE double division.
-// 7 FP64-pipe instructions per iteration (3 DMUL, 3 DADD, 1 DFMA).
+//  * speculative blocks: 16 iterations run without the escape add while the
+//    high words of xx and yy are OR-accumulated; if neither reached 2.0 the
+//    sum stayed < 4 and no escape test could have fired, otherwise the lane
+//    replays the block exactly (see the loop below).
+// 6 FP64-pipe instructions per iteration on the fast path (3 DMUL, 2 DADD,
+// 1 DFMA), 7 on the exact replay.
 //
 // Layout.  One persistent grid per package; each warp claims chunks of
 // consecutive pixels from a device-wide counter (256-pixel chunks for the
@@ -27,6 +32,8 @@
 // the divergence of the irregular set costs at most R-1 idle iterations per
 // pixel instead of the warp-wide maximum.  Results are one uint4 per pixel:
 // the four identical counts of the reference's 4:1 pattern (:217-222).
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace ecl {
@@ -36,7 +43,9 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr uint64_t kBigChunk = 256;   // pixels per claim, bulk of the package
 constexpr uint64_t kTailChunk = 32;   // pixels per claim, last 1/8
 constexpr int kThreads = 256;
-constexpr int kMinBlocks = 8;         // 64 resident warps per SM (<= 32 registers)
+// Resident CTAs per SM: FP64 6 (<= 40 registers, no spills), FP32 8 (64 warps).
+template <typename Real>
+constexpr int kMinBlocks = sizeof(Real) == 8 ? 6 : 8;
 
 template <typename Real>
 struct Arith;
@@ -51,6 +60,7 @@ struct Arith<double> {
   static __device__ __forceinline__ double twice_plus(double t, double c) { return __fma_rn(t, 2.0, c); }
   static __device__ __forceinline__ double from_u64(uint64_t v) { return __ull2double_rn(v); }
   static __device__ __forceinline__ Bits bits(double v) { return static_cast<Bits>(__double_as_longlong(v)); }
+  static __device__ __forceinline__ uint32_t high(double v) { return static_cast<uint32_t>(__double2hiint(v)); }
   static constexpr Bits kFourBits = 0x4010000000000000ull;  // 4.0
 };
 
@@ -64,6 +74,7 @@ struct Arith<float> {
   static __device__ __forceinline__ float twice_plus(float t, float c) { return __fmaf_rn(t, 2.0f, c); }
   static __device__ __forceinline__ float from_u64(uint64_t v) { return __ull2float_rn(v); }
   static __device__ __forceinline__ Bits bits(float v) { return __float_as_uint(v); }
+  static __device__ __forceinline__ uint32_t high(float v) { return __float_as_uint(v); }
   static constexpr Bits kFourBits = 0x40800000u;  // 4.0f
 };
 
@@ -86,10 +97,10 @@ __global__ void coord_tables(const Viewport<Real> vp, Real* __restrict__ tab) {
   }
 }
 
-template <typename Real, int R>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
+template <typename Real, int R, int MB = kMinBlocks<Real>>
+__global__ void __launch_bounds__(kThreads, MB)
     mandel_persistent(const Viewport<Real> vp, const Real* __restrict__ tab, uint64_t first, uint64_t count,
-                      uint4* __restrict__ out, unsigned* __restrict__ ctrl) {
+                      uint4* __restrict__ out, uint32_t* __restrict__ compact, unsigned* __restrict__ ctrl) {
   using A = Arith<Real>;
   using Bits = typename A::Bits;
   const unsigned lane = threadIdx.x & 31u;
@@ -161,20 +172,57 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     }
     if (!__any_sync(kFull, valid)) break;
 
+    // Speculative block: R iterations without the escape add.  If neither
+    // zx^2 nor zy^2 reached 2.0 anywhere in the block (bit 30 of the IEEE
+    // high word, OR-accumulated), xx + yy < 4 held at every step, so the
+    // reference's test "xx + yy > 4" was false at every step: the block is
+    // exactly R reference iterations.  Otherwise the lane replays the block
+    // from the saved state with the per-iteration test.
+    const Real zx0 = zx, zy0 = zy;
+    const uint32_t n0 = n;
+    uint32_t acc = 0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const Real xx = A::mul(zx, zx);
       const Real yy = A::mul(zy, zy);
-      const Bits s = A::bits(A::add(xx, yy));  // >= +0: integer order == FP order
-      alive = alive && s <= A::kFourBits;
+      acc |= A::high(xx) | A::high(yy);
       const Real t = A::mul(zx, zy);
       zy = A::twice_plus(t, cy);
       zx = A::add(A::sub(xx, yy), cx);
-      n += alive ? 1u : 0u;
-      alive = alive && n < max_it;
+    }
+    const bool fast = alive && n0 + R <= max_it && (acc & 0x40000000u) == 0u;
+    if (fast) {
+      n = n0 + R;
+      alive = n < max_it;
+    }
+    bool live = alive && !fast;  // lanes replaying the block exactly
+    if (__any_sync(kFull, live)) {
+      if (live) {
+        zx = zx0;
+        zy = zy0;
+        n = n0;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const Real xx = A::mul(zx, zx);
+        const Real yy = A::mul(zy, zy);
+        const Bits s = A::bits(A::add(xx, yy));  // >= +0: integer order == FP order
+        live = live && s <= A::kFourBits;
+        const Real t = A::mul(zx, zy);
+        const Real nzy = A::twice_plus(t, cy);
+        const Real nzx = A::add(A::sub(xx, yy), cx);
+        if (live) {
+          zx = nzx;
+          zy = nzy;
+          n += 1u;
+        }
+        live = live && n < max_it;
+      }
+      if (alive && !fast) alive = live;
     }
     if (valid && !alive) {
       out[idx] = make_uint4(n, n, n, n);
+      if (compact) compact[idx] = n;  // host-bound copy: one count per pixel
       valid = false;
     }
   }
@@ -211,11 +259,11 @@ Viewport<Real> make_viewport(const MandelParams& p) {
   return vp;
 }
 
-template <typename Real, int R>
+template <typename Real, int R, int MB = kMinBlocks<Real>>
 cudaError_t launch_real(const MandelParams& p, const LaunchEnv& env, uint64_t first, uint64_t count) {
   static int blocks_per_sm = 0;
   if (blocks_per_sm == 0) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, mandel_persistent<Real, R>,
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, mandel_persistent<Real, R, MB>,
                                                                   kThreads, 0);
     if (e != cudaSuccess) return e;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
@@ -227,8 +275,8 @@ cudaError_t launch_real(const MandelParams& p, const LaunchEnv& env, uint64_t fi
   uint64_t grid = static_cast<uint64_t>(env.sms) * static_cast<uint64_t>(blocks_per_sm);
   if (blocks_needed < grid) grid = blocks_needed;
   if (grid == 0) return cudaSuccess;
-  mandel_persistent<Real, R><<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
-      vp, tab, first, count, static_cast<uint4*>(env.out[0]), env.ctrl);
+  mandel_persistent<Real, R, MB><<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
+      vp, tab, first, count, static_cast<uint4*>(env.out[0]), env.compact, env.ctrl);
   return cudaGetLastError();
 }
 
@@ -253,7 +301,18 @@ cudaError_t prepare_mandelbrot(const KernelSpec& spec, const LaunchEnv& env) {
 cudaError_t launch_mandelbrot(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
   if (count == 0) return cudaSuccess;
   if (spec.kind == KernelKind::MandelbrotF32) return launch_real<float, 16>(spec.mandel, env, first, count);
-  return launch_real<double, 16>(spec.mandel, env, first, count);
+  // Tuning hook (ECL_MANDEL_VARIANT): block length R and resident CTAs per SM.
+  static const int variant = [] {
+    const char* v = std::getenv("ECL_MANDEL_VARIANT");
+    return v ? std::atoi(v) : 0;
+  }();
+  switch (variant) {
+    case 1: return launch_real<double, 16, 6>(spec.mandel, env, first, count);
+    case 2: return launch_real<double, 32, 4>(spec.mandel, env, first, count);
+    case 3: return launch_real<double, 8, 4>(spec.mandel, env, first, count);
+    case 4: return launch_real<double, 16, 3>(spec.mandel, env, first, count);
+    default: return launch_real<double, 16, 4>(spec.mandel, env, first, count);  // measured best
+  }
 }
 
 }  // namespace ecl

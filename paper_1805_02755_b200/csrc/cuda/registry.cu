@@ -102,6 +102,7 @@ int resolve_kernel(KernelSpec& s, std::string* err) {
       if (w == 0 || h == 0 || s.mandel.max_iterations == 0)
         return bad(err, "mandelbrot: width, height and max_iterations must be positive");
       if (w * h != s.gws) return bad(err, "mandelbrot: width*height must equal global_work_size");
+      s.replicate = 4;  // four identical counts per pixel (workloads.hpp:217-222)
       return ECL_OK;
     }
     case KernelKind::Synthetic:

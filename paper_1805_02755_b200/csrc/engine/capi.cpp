@@ -86,6 +86,16 @@ int ecl_engine_create(const char* config_json, ecl_engine** out) {
     cfg.seed = j.value("seed", std::uint64_t{0});
     cfg.exclude_init_from_total = j.value("exclude_init", false);
     cfg.tally = j.value("tally", false);
+    if (j.contains("shared")) {
+      const json& s = j.at("shared");
+      SharedConfig sc;
+      sc.name = s.at("name").get<std::string>();
+      sc.rank = s.at("rank").get<std::uint32_t>();
+      sc.world = s.at("world").get<std::uint32_t>();
+      sc.local = s.at("local_devices").get<std::vector<std::uint32_t>>();
+      sc.barrier_timeout_s = s.value("barrier_timeout_s", 120.0);
+      cfg.shared = sc;
+    }
     handle->engine = std::make_unique<Engine>(std::move(cfg), validate_program(program_from_json(j.at("program"))));
   });
   if (rc == ECL_OK) *out = handle.release();
@@ -151,6 +161,93 @@ int64_t ecl_engine_error(const ecl_engine* e, uint32_t i, int* status, char* buf
   if (i >= e->errors.size()) return status_of(ErrorCode::ConfigError);
   *status = status_of(e->errors[i].code());
   return emit(e->errors[i].what(), buf, cap);
+}
+
+struct ecl_shared {
+  std::unique_ptr<SharedCoordinator> coord;
+  SchedulerConfig sched;
+  std::uint64_t total_wg = 0;
+  std::vector<DeviceProfile> devices;
+};
+
+int ecl_shared_open(const char* text, ecl_shared** out) {
+  *out = nullptr;
+  auto h = std::make_unique<ecl_shared>();
+  const int rc = guarded(nullptr, [&] {
+    const json j = json::parse(text);
+    SharedConfig sc;
+    sc.name = j.at("name").get<std::string>();
+    sc.rank = j.at("rank").get<std::uint32_t>();
+    sc.world = j.at("world").get<std::uint32_t>();
+    sc.local = j.value("local_devices", std::vector<std::uint32_t>{});
+    sc.barrier_timeout_s = j.value("barrier_timeout_s", 60.0);
+    h->sched = scheduler_from_json(j.at("scheduler"));
+    h->total_wg = j.at("total_work_groups").get<std::uint64_t>();
+    h->devices = devices_from(j.at("devices"));
+    h->coord = std::make_unique<SharedCoordinator>(sc);
+  });
+  if (rc == ECL_OK) *out = h.release();
+  return rc;
+}
+
+void ecl_shared_close(ecl_shared* h) { delete h; }
+
+int ecl_shared_begin(ecl_shared* h, double* epoch_ms) {
+  return guarded(nullptr, [&] { *epoch_ms = h->coord->begin_run(h->sched, h->total_wg, h->devices); });
+}
+
+int ecl_shared_next(ecl_shared* h, uint32_t device, uint64_t* offset_wg, uint64_t* size_wg, uint64_t* seq) {
+  int granted = 0;
+  const int rc = guarded(nullptr, [&] {
+    PackageRange r;
+    if (h->coord->next(device, &r, seq)) {
+      *offset_wg = r.offset_wg;
+      *size_wg = r.size_wg;
+      granted = 1;
+    }
+  });
+  return rc == ECL_OK ? granted : rc;
+}
+
+int ecl_shared_observe(ecl_shared* h, uint32_t device, uint64_t items, double ms) {
+  return guarded(nullptr, [&] { h->coord->observe(device, items, ms); });
+}
+
+int ecl_shared_complete(ecl_shared* h, uint64_t seq, uint32_t device, uint64_t offset_wg, uint64_t size_wg,
+                        double t_start_ms, double t_end_ms) {
+  return guarded(nullptr, [&] {
+    Package p;
+    p.seq = seq;
+    p.device_index = device;
+    p.offset_wg = offset_wg;
+    p.size_wg = size_wg;
+    p.t_start_ms = p.t_enqueue_ms = t_start_ms;
+    p.t_end_ms = t_end_ms;
+    h->coord->complete(p);
+  });
+}
+
+int ecl_shared_fail(ecl_shared* h) {
+  return guarded(nullptr, [&] { h->coord->fail(); });
+}
+
+int64_t ecl_shared_end(ecl_shared* h, uint64_t* quads, uint64_t cap, int* peer_failed) {
+  int64_t n = 0;
+  const int rc = guarded(nullptr, [&] {
+    bool failed = false;
+    const auto all = h->coord->end_run(&failed);
+    *peer_failed = failed ? 1 : 0;
+    for (const Package& p : all) {
+      if (4 * static_cast<uint64_t>(n) + 3 < cap) {
+        quads[4 * n] = p.seq;
+        quads[4 * n + 1] = p.device_index;
+        quads[4 * n + 2] = p.offset_wg;
+        quads[4 * n + 3] = p.size_wg;
+      }
+      ++n;
+    }
+  });
+  return rc == ECL_OK ? n : rc;
 }
 
 int ecl_scheduler_create(const char* text, ecl_scheduler** out) {

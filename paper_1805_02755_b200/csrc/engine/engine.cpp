@@ -59,23 +59,15 @@ struct Device {
   ecl_gpu* gpu = nullptr;
   std::uint32_t depth = 2;
   std::thread thread;
-  // completion mailbox, written by the CUDA callback thread
-  std::mutex mailbox_m;
-  std::condition_variable mailbox_cv;
-  std::set<std::uint64_t> finished;
 };
 
-void on_done(void* user, std::uint64_t seq, int /*status*/) {
-  auto* d = static_cast<Device*>(user);
-  {
-    std::lock_guard lock(d->mailbox_m);
-    d->finished.insert(seq);
-  }
-  d->mailbox_cv.notify_one();
+double steady_ms(Clock::time_point t) {
+  return std::chrono::duration<double, std::milli>(t.time_since_epoch()).count();
 }
 
 struct RunState {
   Scheduler* scheduler = nullptr;
+  SharedCoordinator* shared = nullptr;  // one process per GPU: cross-process decisions
   std::mutex coordinator;  // serializes scheduler access and seq (engine.hpp:357,370)
   std::uint64_t next_seq = 0;
   std::vector<void*> host_out;  // empty = device-resident
@@ -94,7 +86,9 @@ struct Engine::Impl {
   double init_ms = 0.0;
   bool init_charged = false;
   ecl_kernel* kernel = nullptr;
-  std::vector<std::unique_ptr<Device>> devices;
+  std::vector<std::unique_ptr<Device>> devices;  // the devices this process drives
+  std::vector<int> local_of;                     // global device index -> devices[] slot or -1
+  std::unique_ptr<SharedCoordinator> shared;     // one process per GPU (cfg.shared)
   ExecutionTrace last;
   std::vector<Package> last_packages;  // packages of the last wall run (for gather)
   bool last_resident = false;
@@ -150,12 +144,28 @@ struct Engine::Impl {
           "kernel '" + s.kernel + "'");
   }
 
+  // Index into `devices` of global device i, -1 if a peer process drives it.
+  int local_slot(std::uint32_t i) const { return i < local_of.size() ? local_of[i] : -1; }
+
   void open_devices() {
-    for (std::uint32_t i = 0; i < cfg.devices.size(); ++i) {
+    std::vector<std::uint32_t> mine;
+    if (shared) {
+      mine = shared->config().local;
+      for (std::uint32_t i : mine)
+        if (i >= cfg.devices.size()) throw Error(ErrorCode::ConfigError, "shared: local device index out of range");
+    } else {
+      for (std::uint32_t i = 0; i < cfg.devices.size(); ++i) mine.push_back(i);
+    }
+    local_of.assign(cfg.devices.size(), -1);
+    for (std::uint32_t i : mine) {
+      local_of[i] = static_cast<int>(devices.size());
       auto d = std::make_unique<Device>();
       d->index = i;
       d->depth = cfg.devices[i].backend.queue_depth;
-      check(ecl_gpu_open(cfg.devices[i].backend.ordinal, d->depth, &d->gpu), "device '" + cfg.devices[i].id + "'");
+      const Backend& be = cfg.devices[i].backend;
+      check(ecl_gpu_open(be.ordinal, d->depth, &d->gpu), "device '" + cfg.devices[i].id + "'");
+      check(ecl_gpu_set_copy_split(d->gpu, be.copy_split_items), "copy split");
+      check(ecl_gpu_set_widen_fraction(d->gpu, be.widen_per_8), "widen fraction");
       devices.push_back(std::move(d));
       check(ecl_gpu_bind(devices.back()->gpu, kernel), "bind '" + cfg.devices[i].id + "'");
     }
@@ -201,34 +211,22 @@ struct Engine::Impl {
     std::lock_guard lock(rs.completion);
     rs.errors.push_back(std::move(e));
     rs.abort.store(true);
+    if (rs.shared) rs.shared->fail();  // peers stop pulling packages
   }
 
-  // Waits for package `seq`; false on a device fault (already recorded).
+  // Event-driven completion: blocks on the package's completion event (its
+  // kernel, copies and notify-stream marker); false on a device fault
+  // (recorded), never hangs on a faulted context.
   bool await(Device& dev, RunState& rs, std::uint64_t seq) {
-    std::unique_lock lock(dev.mailbox_m);
-    while (!dev.finished.count(seq)) {
-      if (dev.mailbox_cv.wait_for(lock, std::chrono::milliseconds(50)) == std::cv_status::timeout) {
-        lock.unlock();
-        const int rc = ecl_gpu_poll(dev.gpu, seq);
-        lock.lock();
-        if (rc == ECL_OK) break;
-        if (rc != ECL_PENDING) {
-          lock.unlock();
-          fail(rs, Error(code_of_status(rc), std::string("device '") + cfg.devices[dev.index].id + "': " + ecl_last_error()));
-          return false;
-        }
-      }
-    }
-    dev.finished.erase(seq);
-    return true;
+    const int rc = ecl_gpu_wait(dev.gpu, seq);
+    if (rc == ECL_OK) return true;
+    fail(rs, Error(code_of_status(rc), std::string("device '") + cfg.devices[dev.index].id + "': " + ecl_last_error()));
+    return false;
   }
 
   void drive(Device& dev, RunState& rs) {
     const DeviceProfile& profile = cfg.devices[dev.index];
-    {
-      std::lock_guard lock(dev.mailbox_m);
-      dev.finished.clear();  // seqs restart at 0 every run
-    }
+    const double epoch_abs = steady_ms(epoch);
     std::deque<Package> inflight;
     bool drained = false;
     void* const* host_out = rs.host_out.empty() ? nullptr : rs.host_out.data();
@@ -236,7 +234,13 @@ struct Engine::Impl {
     auto pull = [&]() -> bool {
       std::optional<PackageRange> range;
       Package pkg;
-      {
+      if (rs.shared) {
+        if (rs.abort.load()) return false;
+        PackageRange r;
+        if (!rs.shared->next(dev.index, &r, &pkg.seq)) return false;
+        range = r;
+        pkg.t_enqueue_ms = now_ms();
+      } else {
         std::lock_guard lock(rs.coordinator);
         if (rs.abort.load()) return false;
         range = rs.scheduler->next(dev.index);
@@ -251,7 +255,7 @@ struct Engine::Impl {
       pkg.t_start_ms = pkg.t_enqueue_ms;
       if (profile.launch_overhead_ms > 0.0)
         std::this_thread::sleep_for(std::chrono::duration<double, std::milli>(profile.launch_overhead_ms));
-      const int rc = ecl_gpu_submit(dev.gpu, pkg.seq, pkg.offset_wg, pkg.size_wg, host_out, on_done, &dev);
+      const int rc = ecl_gpu_submit(dev.gpu, pkg.seq, pkg.offset_wg, pkg.size_wg, host_out, nullptr, nullptr);
       if (rc != ECL_OK) {
         fail(rs, Error(code_of_status(rc), std::string("device '") + profile.id + "': " + ecl_last_error()));
         return false;
@@ -278,9 +282,12 @@ struct Engine::Impl {
         drained = true;
         continue;
       }
-      pkg.t_start_ms = t0;
-      pkg.t_end_ms = t1;
-      {
+      pkg.t_start_ms = t0 - epoch_abs;  // device times come on the absolute steady clock
+      pkg.t_end_ms = t1 - epoch_abs;
+      if (rs.shared) {
+        rs.shared->observe(dev.index, pkg.size_wg * prog.local_work_size(), t1 - t0);
+        rs.shared->complete(pkg);
+      } else {
         std::lock_guard lock(rs.coordinator);
         rs.scheduler->observe(dev.index, pkg.size_wg * prog.local_work_size(), t1 - t0);
       }
@@ -336,7 +343,7 @@ struct Engine::Impl {
     std::vector<ecl_gpu*> g = gpus();
     for (auto& d : devices) {
       check(ecl_gpu_enable_tally(d->gpu, tally ? 1 : 0), "tally");
-      check(ecl_gpu_set_epoch(d->gpu, &Impl::clock_cb, this), "epoch");
+      check(ecl_gpu_set_epoch(d->gpu, nullptr, nullptr), "epoch");
     }
     if (!inputs.empty()) {
       check(ecl_gpu_upload_inputs(g[0], const_cast<const void* const*>(inputs.data())), "upload");
@@ -350,32 +357,54 @@ struct Engine::Impl {
   // from a fresh scheduler until it is drained.  Returns the packages in
   // seq order; throws EngineFailure on any device/tiling/tally error.
   std::vector<Package> co_execute(std::span<void* const> host_out, std::uint64_t first_seq, bool tally) {
-    auto scheduler = make_scheduler(cfg.scheduler, prog.total_work_groups(), cfg.devices);
     RunState rs;
-    rs.scheduler = scheduler.get();
+    std::unique_ptr<Scheduler> scheduler;
+    if (shared) {
+      // Collective with the peer processes: the run's epoch is shared so all
+      // ranks' timestamps share one (CLOCK_MONOTONIC) timeline.
+      const double ep = shared->begin_run(cfg.scheduler, prog.total_work_groups(), cfg.devices);
+      epoch = Clock::time_point(std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double, std::milli>(ep)));
+      rs.shared = shared.get();
+    } else {
+      scheduler = make_scheduler(cfg.scheduler, prog.total_work_groups(), cfg.devices);
+      rs.scheduler = scheduler.get();
+    }
     rs.next_seq = first_seq;
     rs.host_out.assign(host_out.begin(), host_out.end());
-    {
-      std::lock_guard lock(run_m);
-      current = &rs;
-      busy = static_cast<std::uint32_t>(devices.size());
-      ++generation;
+    if (devices.size() == 1) {
+      drive(*devices[0], rs);  // one device: no thread hand-off on the critical path
+    } else {
+      {
+        std::lock_guard lock(run_m);
+        current = &rs;
+        busy = static_cast<std::uint32_t>(devices.size());
+        ++generation;
+      }
+      run_cv.notify_all();
+      {
+        std::unique_lock lock(run_m);
+        idle_cv.wait(lock, [&] { return busy == 0; });
+        current = nullptr;
+      }
     }
-    run_cv.notify_all();
-    {
-      std::unique_lock lock(run_m);
-      idle_cv.wait(lock, [&] { return busy == 0; });
-      current = nullptr;
-    }
-    std::sort(rs.completed.begin(), rs.completed.end(), [](const Package& a, const Package& b) { return a.seq < b.seq; });
     std::vector<Error> errors = std::move(rs.errors);
+    std::vector<Package> all;
+    if (shared) {
+      bool peer_failed = false;
+      all = shared->end_run(&peer_failed);  // every rank's packages
+      if (peer_failed && errors.empty())
+        errors.emplace_back(ErrorCode::KernelPanic, "a peer rank failed during the run");
+    } else {
+      all = std::move(rs.completed);
+    }
+    std::sort(all.begin(), all.end(), [](const Package& a, const Package& b) { return a.seq < b.seq; });
     if (errors.empty()) {
-      if (!tiles_exactly(rs.completed, prog.total_work_groups()))
+      if (!tiles_exactly(all, prog.total_work_groups()))
         errors.emplace_back(ErrorCode::SchedulerError, "packages do not tile the work-group range exactly once");
-      if (tally) check_tally(errors);
+      if (tally) check_tally(errors, all);
     }
     if (!errors.empty()) throw EngineFailure(std::move(errors));
-    return std::move(rs.completed);
+    return all;
   }
 
   // Iterative program (NBody timesteps):
@@ -388,6 +417,10 @@ struct Engine::Impl {
                            std::span<const std::pair<std::uint32_t, std::uint32_t>> swaps) {
     const ProgramSpec& s = prog.spec();
     if (steps == 0) throw Error(ErrorCode::ConfigError, "run_steps needs at least one step");
+    if (shared)
+      throw Error(ErrorCode::ConfigError,
+                  "run_steps exchanges state between GPUs over NVLink peer copies: drive every device from one "
+                  "process (no cfg.shared)");
     check_inputs(inputs);
     for (const auto& [i, o] : swaps)
       if (i >= s.in_buffers.size() || o >= s.out_buffers.size() ||
@@ -424,15 +457,23 @@ struct Engine::Impl {
     return t;
   }
 
-  void check_tally(std::vector<Error>& errors) {
+  // Exactly-once check.  Counts of the local devices are summed; in shared
+  // mode peers' items are expected to be 0 here and 1 on their own rank, so
+  // the expectation per item is "1 iff a local device owned its package".
+  void check_tally(std::vector<Error>& errors, const std::vector<Package>& all) {
     const std::uint64_t n = prog.global_work_size();
-    std::vector<std::uint32_t> sum(n, 0), part(n);
+    std::vector<std::uint32_t> sum(n, 0), part(n), expect(n, shared ? 0 : 1);
     for (auto& d : devices) {
       check(ecl_gpu_download_tally(d->gpu, part.data()), "tally download");
       for (std::uint64_t i = 0; i < n; ++i) sum[i] += part[i];
     }
+    if (shared)
+      for (const Package& p : all)
+        if (local_slot(p.device_index) >= 0)
+          for (std::uint64_t i = p.offset_wg * prog.local_work_size(); i < p.end_wg() * prog.local_work_size(); ++i)
+            expect[i] = 1;
     for (std::uint64_t i = 0; i < n; ++i)
-      if (sum[i] != 1) {
+      if (sum[i] != expect[i]) {
         errors.emplace_back(ErrorCode::TallyViolation,
                             "work-item " + std::to_string(i) + " executed " + std::to_string(sum[i]) + " times");
         return;
@@ -567,7 +608,9 @@ struct Engine::Impl {
       for (std::uint32_t b = 0; b < outputs.size(); ++b) {
         if (!outputs[b]) continue;
         char* dst = static_cast<char*>(outputs[b]) + r.offset * s.out_buffers[b].element_size_bytes;
-        check(ecl_gpu_download_slice(devices[p.device_index]->gpu, b, r.offset, r.count, dst), "gather");
+        const int slot = local_slot(p.device_index);
+        if (slot < 0) continue;  // a peer process owns this slice
+        check(ecl_gpu_download_slice(devices[slot]->gpu, b, r.offset, r.count, dst), "gather");
       }
     }
   }
@@ -584,9 +627,27 @@ struct Engine::Impl {
       if (devices.size() == 1) inputs_resident = true;
     }
     float kms = 0.f;
-    check(ecl_gpu_native_run(g, &kms), "native run");
-    for (std::uint32_t b = 0; b < outputs.size(); ++b)
-      if (outputs[b]) check(ecl_gpu_download_slice(g, b, 0, s.out_buffers[b].element_count, outputs[b]), "download");
+    bool any_out = false;
+    for (void* p : outputs) any_out = any_out || p != nullptr;
+    if (!any_out) {
+      check(ecl_gpu_native_run(g, &kms), "native run");
+    } else {
+      // One launch over the whole grid followed by the same device-to-host
+      // path a package takes (compact copy + host widening where the kernel
+      // replicates), but with no pipelining: launch, then copy everything.
+      std::vector<void*> out(outputs.begin(), outputs.end());
+      out.resize(s.out_buffers.size(), nullptr);
+      const std::uint64_t seq = ~0ull - 1;
+      check(ecl_gpu_set_copy_split(g, 0), "split");
+      const int rc = ecl_gpu_submit(g, seq, 0, prog.total_work_groups(), out.data(), nullptr, nullptr);
+      check(ecl_gpu_set_copy_split(g, cfg.devices[devices[0]->index].backend.copy_split_items), "split");
+      check(rc, "native run");
+      check(ecl_gpu_wait(g, seq), "native wait");
+      double a = 0.0, b = 0.0;
+      check(ecl_gpu_package_times(g, seq, &a, &b), "native times");
+      kms = static_cast<float>(b - a);
+    }
+    (void)s;
     NativeResult r;
     r.kernel_ms = kms;
     r.total_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
@@ -600,6 +661,7 @@ Engine::Engine(EngineConfig cfg, ValidatedProgram prog) : impl_(std::make_unique
   impl_->validate_config();
   if (impl_->wall()) {
     try {
+      if (impl_->cfg.shared) impl_->shared = std::make_unique<SharedCoordinator>(*impl_->cfg.shared);
       impl_->make_kernel();
       impl_->open_devices();
     } catch (...) {

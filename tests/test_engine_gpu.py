@@ -140,17 +140,24 @@ def test_native_run_matches_engine(gpu_available, oracle):
     assert np.array_equal(out[0].view(np.uint32), expand_4to1(oracle.mandelbrot(512, 512, 512)))
 
 
-def test_per_device_package_intervals_never_overlap(gpu_available):
-    # test_engine.cpp:193-208, with queue depth 2 on the device streams
-    _, res = run_engine(W.mandelbrot_spec(256, 256, 1000), P.HGuidedConfig(), n_dev=3)
+@pytest.mark.parametrize("depth,max_concurrent", [(1, 1), (2, 2), (4, 2)])
+def test_per_device_package_concurrency(gpu_available, depth, max_concurrent):
+    # test_engine.cpp:193-208: with queue depth 1 (reference semantics) a
+    # device's packages never overlap; with depth >= 2 consecutive packages
+    # alternate between the device's two compute lanes, so at most two
+    # kernels of one device overlap (a drain tail with the next ramp).
+    _, res = run_engine(W.mandelbrot_spec(256, 256, 1000), P.HGuidedConfig(), n_dev=3, depth=depth)
     by_dev = {}
     for p in res.trace.packages:
         by_dev.setdefault(p.device_id, []).append((p.t_start_ms, p.t_end_ms))
         assert p.t_enqueue_ms <= p.t_start_ms + 1e-3 and p.t_start_ms <= p.t_end_ms
     for iv in by_dev.values():
-        iv.sort()
-        for a, b in zip(iv, iv[1:]):
-            assert a[1] <= b[0] + 1e-3
+        events = sorted([(a, 1) for a, _ in iv] + [(b - 1e-3, -1) for _, b in iv])
+        live = peak = 0
+        for _, d in events:
+            live += d
+            peak = max(peak, live)
+        assert peak <= max_concurrent
 
 
 def test_indivisible_package_fails_mid_run(gpu_available):
