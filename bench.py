@@ -404,7 +404,28 @@ def run_reference(args, world, rank):
     return 0
 
 
-BARRIERS = 6  # barrier() calls bench_engine makes (ranks > 0 mirror them)
+class SharedHostBuffer:
+    """A /dev/shm-backed host buffer every rank maps and page-locks: each
+    process D2H-copies its own packages' slices into the one result."""
+
+    def __init__(self, path, nbytes, create, P, np):
+        import mmap
+        self.path, self.P = path, P
+        fd = os.open(path, os.O_RDWR | (os.O_CREAT if create else 0), 0o600)
+        if create:
+            os.ftruncate(fd, nbytes)
+        self.mm = mmap.mmap(fd, nbytes, mmap.MAP_SHARED, mmap.PROT_READ | mmap.PROT_WRITE)
+        os.close(fd)
+        self.array = np.frombuffer(self.mm, dtype=np.uint8)
+        P.host_register(self.array)
+        self.create = create
+
+    def free(self):
+        self.P.host_unregister(self.array)
+        self.array = None
+        self.mm.close()
+        if self.create and os.path.exists(self.path):
+            os.unlink(self.path)
 
 
 def run_ours(args, world, rank, local):
@@ -419,29 +440,40 @@ def run_ours(args, world, rank, local):
         print(json.dumps({"error": "no CUDA device visible"}))
         return 1
     dist = world > 1
+    shared = None
     if dist:
+        # One process per GPU (torchrun): every rank drives its own B200 and
+        # the ranks co-schedule one index space through the shared-memory
+        # decision log (coexec/shared.hpp) — no data-path collective.
         import torch.distributed as td
-        torch.cuda.set_device(local)
-        td.init_process_group("nccl", device_id=torch.device("cuda", local))
-    # EngineCL's co-execution model: one host coordinator drives every device
-    # of the box through its per-device threads (engine.hpp:354-405).  Under
-    # torchrun rank 0 owns the engine over GPUs 0..N-1; the other ranks join
-    # the barriers.
+        ndev = torch.cuda.device_count()
+        torch.cuda.set_device(local % ndev)
+        if world <= ndev:
+            td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # more ranks than GPUs (a one-GPU test box): NCCL refuses shared devices
+            td.init_process_group("gloo")
+        tag = [f"{os.getpid():x}{int.from_bytes(os.urandom(4), 'little'):x}" if rank == 0 else None]
+        td.broadcast_object_list(tag, src=0)
+        shared = {"name": f"/ecl_bench_{tag[0]}", "rank": rank, "world": world, "local_devices": [rank],
+                  "host_buffer": f"/dev/shm/ecl_bench_out_{tag[0]}"}
     n = world if dist else args.gpus
-    torch.cuda.set_device(local if dist else 0)
+    torch.cuda.set_device((local % torch.cuda.device_count()) if dist else 0)
 
     def barrier():
         torch.cuda.synchronize()
         if dist:
             torch.distributed.barrier()
 
-    line = None
-    if rank == 0:
-        wl = WORKLOADS[args.workload](P, W, np)
-        line = bench_engine(args, n, wl, P, N, np, torch, barrier)
-    else:
-        for _ in range(BARRIERS):
-            barrier()
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        dev = "cuda" if torch.distributed.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    wl = WORKLOADS[args.workload](P, W, np)
+    line = bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, rank)
     if dist:
         torch.distributed.destroy_process_group()
     if rank == 0:
@@ -449,16 +481,22 @@ def run_ours(args, world, rank, local):
     return 0
 
 
-def bench_engine(args, n, wl, P, N, np, torch, barrier):
+def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, rank):
     min_wg = args.min_package if args.min_package else wl.min_package(n)
-    devs = [P.cuda_device(f"gpu{i}", ordinal=i % P.gpu_count(), power=1.0, queue_depth=args.queue_depth,
-                          min_package_work_groups=min_wg, widen_per_8=args.widen) for i in range(n)]
+    ngpu = P.gpu_count()
+    devs = [P.cuda_device(f"gpu{i}", ordinal=i % ngpu, power=1.0, queue_depth=args.queue_depth,
+                          min_package_work_groups=min_wg, widen_per_8=args.widen,
+                          copy_split_items=args.copy_split) for i in range(n)]
     sched = wl.scheduler(n)
     if isinstance(sched, P.HGuidedConfig):
         sched.k = args.k
         sched.adaptive = args.adaptive
     prog = P.validate_program(wl.spec())
-    eng = P.Engine(P.EngineConfig(devs, sched), prog)
+    if shared and wl.steps_per_run > 1:
+        raise SystemExit(f"{wl.name}: iterative runs exchange state over NVLink from one process; "
+                         "run without torchrun (--gpus N)")
+    eng_shared = {k: v for k, v in shared.items() if k != "host_buffer"} if shared else None
+    eng = P.Engine(P.EngineConfig(devs, sched, shared=eng_shared), prog)
     stream = torch.cuda.current_stream()
 
     # page-locked host buffers (inputs for the e2e H2D, outputs for the D2H)
@@ -469,7 +507,17 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier):
         pb.array[:] = np.ascontiguousarray(a).reshape(-1).view(np.uint8)
         pinned_in.append(pb)
     in_arrays = [pb.array for pb in pinned_in]
-    pinned_out = [P.PinnedBuffer(b.size_bytes(), np.uint8) for b in prog.spec().out_buffers]
+    if shared:
+        if rank == 0:
+            pinned_out = [SharedHostBuffer(shared["host_buffer"] + f"_{i}", b.size_bytes(), True, P, np)
+                          for i, b in enumerate(prog.spec().out_buffers)]
+            barrier()
+        else:
+            barrier()
+            pinned_out = [SharedHostBuffer(shared["host_buffer"] + f"_{i}", b.size_bytes(), False, P, np)
+                          for i, b in enumerate(prog.spec().out_buffers)]
+    else:
+        pinned_out = [P.PinnedBuffer(b.size_bytes(), np.uint8) for b in prog.spec().out_buffers]
     out_arrays = [pb.array for pb in pinned_out]
 
     def run(inputs, outputs):
@@ -493,9 +541,10 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier):
     run(in_arrays, None)
     for _ in range(max(0, args.warmup - 1)):
         run(None, None)
+    my_gpu = (rank % ngpu) if shared else 0
     eng.kernel_timing(reset=True)
-    sampler = ClockSampler(0).start()
-    ms_dev = timed(lambda: run(None, None), args.steps)
+    sampler = ClockSampler(my_gpu).start()
+    ms_dev = max_over_ranks(timed(lambda: run(None, None), args.steps))
     clocks = sampler.stop()
     kernel_ms, launches = eng.kernel_timing(reset=True)
     last = eng.last_trace()
@@ -504,13 +553,14 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier):
     # --- end to end through the C-ABI with page-locked host buffers ---
     for _ in range(args.warmup):
         run(in_arrays, out_arrays)
-    for a in out_arrays:
-        a[:] = 0
-    sampler2 = ClockSampler(0).start()
-    ms_e2e = timed(lambda: run(in_arrays, out_arrays), args.steps)
+    if rank == 0:
+        for a in out_arrays:
+            a[:] = 0
+    sampler2 = ClockSampler(my_gpu).start()
+    ms_e2e = max_over_ranks(timed(lambda: run(in_arrays, out_arrays), args.steps))
     clocks2 = sampler2.stop()
     eng.kernel_timing(reset=True)
-    sane = wl.check(out_arrays)
+    sane = wl.check(out_arrays) if rank == 0 else True
 
     # --- native single-kernel baseline (overhead denominator) ---
     barrier()
@@ -527,8 +577,8 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier):
 
     # --- roofline: vector peaks measured on this device ---
     f64, add, f32 = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
-    N.lib.ecl_probe_vector_peaks(0, ctypes.byref(f64), ctypes.byref(add), ctypes.byref(f32))
-    peak = f64.value if wl.bound == "fp64" else f32.value
+    N.lib.ecl_probe_vector_peaks(my_gpu, ctypes.byref(f64), ctypes.byref(add), ctypes.byref(f32))
+    peak = (f64.value if wl.bound == "fp64" else f32.value) * n  # whole job: N GPUs
     achieved = wl.flops() / (ms_dev * 1e-3) / 1e12
     eng.close()
     h2d = sum(a.nbytes for a in in_arrays)
@@ -556,8 +606,10 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier):
         "scaling": "strong", "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic",
         "config": {"workload": wl.workload, "scheduler": P.describe(sched), "lws": prog.local_work_size(),
                    "work_items_per_step": units, "min_package_work_groups": min_wg, "queue_depth": args.queue_depth,
-                   "widen_per_8": args.widen,
-                   "parallelism": f"coexec{n}",
+                   "widen_per_8": args.widen, "copy_split_items": args.copy_split,
+                   "parallelism": f"coexec{n}" + ("-processes" if shared else ""),
+                   "coordination": ("one process per GPU, shared-memory decision log" if shared else
+                                    "one process, one host thread per GPU"),
                    "l2": "no L2 flush: per-step outputs (and inputs) are streamed once; Mandelbrot writes 4 GiB/step"},
         "e2e": {"value": units / (ms_e2e * 1e-3), "unit": "work-items/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
@@ -566,6 +618,7 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier):
                      "algorithmic_flops_per_step": wl.flops(),
                      "achieved_basis": "algorithmic flops per step / device-resident step time (packages overlap "
                                        "on two compute lanes, so summed launch time double-counts)",
+                     "peak_per_gpu": f64.value if wl.bound == "fp64" else f32.value,
                      "peak_source": f"{'DFMA' if wl.bound == 'fp64' else 'FFMA'} chains measured on this GPU by "
                                     "ecl_probe_vector_peaks (MEASURED_PEAKS.json has no FP64/FP32 vector figure)",
                      "fp64_dfma_tflops": f64.value, "fp64_dadd_tinstr_s": add.value, "fp32_ffma_tflops": f32.value},
@@ -597,6 +650,8 @@ def main(argv=None):
     ap.add_argument("--min-package", type=int, default=0, help="HGuided minimum package (work-groups)")
     ap.add_argument("--widen", type=int, default=8,
                     help="replicated outputs: pieces of 8 copied compact and widened on the host")
+    ap.add_argument("--copy-split", type=int, default=1 << 23,
+                    help="work-items per sub-launch when a package copies to the host (D2H pipelining)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
     if args.impl == "ours":

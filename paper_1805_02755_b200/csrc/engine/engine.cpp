@@ -638,6 +638,7 @@ struct Engine::Impl {
       std::vector<void*> out(outputs.begin(), outputs.end());
       out.resize(s.out_buffers.size(), nullptr);
       const std::uint64_t seq = ~0ull - 1;
+      check(ecl_gpu_set_epoch(g, nullptr, nullptr), "epoch");
       check(ecl_gpu_set_copy_split(g, 0), "split");
       const int rc = ecl_gpu_submit(g, seq, 0, prog.total_work_groups(), out.data(), nullptr, nullptr);
       check(ecl_gpu_set_copy_split(g, cfg.devices[devices[0]->index].backend.copy_split_items), "split");
