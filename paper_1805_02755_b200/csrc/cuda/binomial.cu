@@ -24,7 +24,34 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kNodesPerLane = 8;  // 32 x 8 = 256 >= steps + 1 for steps <= 255
 
-__global__ void __launch_bounds__(kThreads)
+// Backward steps j, j-1, ... while j > stop, with NL nodes per lane (lane l
+// holds nodes NL*l .. NL*l+NL-1): c[t] <- c[t] + pu*(c[t+1] - c[t]).  The
+// neighbour of a lane's last node is the next lane's first (one shuffle).
+// Returns the next j.  After it, only nodes t < stop are live.
+template <int NL>
+__device__ __forceinline__ int backward(float (&c)[NL], int j, int stop, float pu) {
+  for (; j > stop; --j) {
+    const float right = __shfl_down_sync(0xffffffffu, c[0], 1);
+#pragma unroll
+    for (int k = 0; k < NL - 1; ++k) c[k] = fmaf(pu, c[k + 1] - c[k], c[k]);
+    c[NL - 1] = fmaf(pu, right - c[NL - 1], c[NL - 1]);
+  }
+  return j;
+}
+
+// NL -> NL/2 nodes per lane: lane l's new nodes (NL/2)*l + k live in lane
+// l/2 at register (l%2)*NL/2 + k.
+template <int NL>
+__device__ __forceinline__ void repack(const float (&c)[NL], float (&h)[NL / 2], unsigned lane) {
+#pragma unroll
+  for (int k = 0; k < NL / 2; ++k) {
+    const float lo = __shfl_sync(0xffffffffu, c[k], lane >> 1);
+    const float hi = __shfl_sync(0xffffffffu, c[NL / 2 + k], lane >> 1);
+    h[k] = (lane & 1u) ? hi : lo;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 4)
     binomial_warp(const float* __restrict__ rand, float* __restrict__ out, int steps, uint64_t first_opt,
                   uint64_t n_opt) {
   const unsigned lane = threadIdx.x & 31u;
@@ -47,20 +74,33 @@ __global__ void __launch_bounds__(kThreads)
     // 1/a factored out: c <- c0 + pu*(c1 - c0) is the reference's
     // puByr*c1 + pdByr*c0 times a, and the a^-steps = exp(-R T) is applied
     // once at the end, so rounding 1/a to f32 does not compound 254 times.
+    // S*exp(vsdt*(2t - steps)) for the lane's 8 nodes: one exp per lane, then
+    // successive factors u^2 = exp(2 vsdt) (FP64, ~1e-16 relative drift).
     float c[kNodesPerLane];
+    double st = S * exp(vsdt * static_cast<double>(2 * static_cast<int>(lane) * kNodesPerLane - steps));
+    const double u2 = u * u;
 #pragma unroll
     for (int k = 0; k < kNodesPerLane; ++k) {
       const int t = static_cast<int>(lane) * kNodesPerLane + k;
-      const double leaf = S * exp(vsdt * static_cast<double>(2 * t - steps)) - K;
+      const double leaf = st - K;
       c[k] = (t <= steps && leaf > 0.0) ? static_cast<float>(leaf) : 0.0f;
+      st *= u2;
     }
-    for (int j = steps; j > 0; --j) {
-      const float right = __shfl_down_sync(0xffffffffu, c[0], 1);  // node 8(l+1)
-#pragma unroll
-      for (int k = 0; k < kNodesPerLane - 1; ++k) c[k] = fmaf(fpu, c[k + 1] - c[k], c[k]);
-      c[kNodesPerLane - 1] = fmaf(fpu, right - c[kNodesPerLane - 1], c[kNodesPerLane - 1]);
-    }
-    if (lane == 0) out[o] = static_cast<float>(static_cast<double>(c[0]) * exp(-0.02 * T));
+    // The live part of the lattice shrinks by one node per step: once it fits
+    // in 128 / 64 / 32 nodes the warp repacks to 4 / 2 / 1 nodes per lane
+    // (one shuffle per register), so later steps cost proportionally less.
+    int j = steps;
+    j = backward<8>(c, j, 128, fpu);
+    float c4[4];
+    repack<8>(c, c4, lane);
+    j = backward<4>(c4, j, 64, fpu);
+    float c2[2];
+    repack<4>(c4, c2, lane);
+    j = backward<2>(c2, j, 32, fpu);
+    float c1[1];
+    repack<2>(c2, c1, lane);
+    backward<1>(c1, j, 0, fpu);
+    if (lane == 0) out[o] = static_cast<float>(static_cast<double>(c1[0]) * exp(-0.02 * T));
   }
 }
 

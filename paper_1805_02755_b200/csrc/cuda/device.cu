@@ -61,8 +61,11 @@ constexpr int kLanes = 2;
 constexpr size_t kCtrlWordsPerLane = 16;
 
 struct Slot {
-  cudaEvent_t start = nullptr;  // kernel start (its lane)
-  cudaEvent_t end = nullptr;    // kernel end (its lane)
+  cudaEvent_t start = nullptr;  // kernel start (first lane of the package)
+  cudaEvent_t end = nullptr;    // kernel end (first lane)
+  cudaEvent_t start2 = nullptr;  // pieces also ran on the other lane: its start / end
+  cudaEvent_t end2 = nullptr;
+  bool two_lanes = false;
   cudaEvent_t done = nullptr;   // copies + callback finished (notify stream)
   uint64_t seq = ~0ull;
   bool busy = false;
@@ -245,6 +248,7 @@ int ecl_gpu_open(int ordinal, uint32_t queue_depth, ecl_gpu** out) {
       return undo(cuda_fail(e, "cudaEventCreate"));
   for (auto& s : g->slots) {
     if ((e = cudaEventCreate(&s.start)) != cudaSuccess || (e = cudaEventCreate(&s.end)) != cudaSuccess ||
+        (e = cudaEventCreate(&s.start2)) != cudaSuccess || (e = cudaEventCreate(&s.end2)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming)) != cudaSuccess)
       return undo(cuda_fail(e, "cudaEventCreate(slot)"));
   }
@@ -273,6 +277,8 @@ int ecl_gpu_close(ecl_gpu* g) {
   for (auto& s : g->slots) {
     if (s.start) cudaEventDestroy(s.start);
     if (s.end) cudaEventDestroy(s.end);
+    if (s.start2) cudaEventDestroy(s.start2);
+    if (s.end2) cudaEventDestroy(s.end2);
     if (s.done) cudaEventDestroy(s.done);
     for (cudaEvent_t ev : s.piece_done) cudaEventDestroy(ev);
   }
@@ -521,16 +527,16 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
   slot.user = user;
   const int lane = static_cast<int>(g->next_lane);
   g->next_lane = (g->next_lane + 1) % static_cast<uint32_t>(g->lanes);
-  cudaStream_t st = g->lane[lane];
-  cudaStream_t cp = g->copy[lane];
 
   bool copies = false;
   for (size_t b = 0; host_outputs && b < g->out.size(); ++b) copies = copies || host_outputs[b] != nullptr;
 
   // With host outputs the package runs as sub-launches of ~d2h_split_items
-  // work-items, each followed on the copy stream by the D2H of its own
-  // slice, so the PCIe copy of piece i overlaps the kernel of piece i+1
-  // (the package's timing events still bracket the whole package).
+  // work-items, each followed on its lane's copy stream by the D2H of its own
+  // slice, so the PCIe copy of piece i overlaps the kernels of later pieces.
+  // Pieces alternate between the two compute lanes so one piece's drain tail
+  // overlaps the next piece's ramp (the timing events bracket the package
+  // across both lanes).
   uint64_t piece_wg = size_wg;
   if (copies && g->d2h_split_items > 0) {
     piece_wg = std::max<uint64_t>(1, g->d2h_split_items / s.lws);
@@ -539,16 +545,21 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
   }
   // Replicated outputs (4 identical uint32 per item): copy one value per item
   // and widen on the host (hostpool.cpp) — a quarter of the PCIe bytes.
-  const bool widen_ok = copies && s.replicate > 1 && g->compact_dev && s.outputs.size() == 1 &&
-                        s.outputs[0].element_size_bytes == 4 && s.out_indices == s.replicate &&
-                        s.out_work_items == 1 && g->widen_per_8 > 0;
-  const bool widen = widen_ok;
+  const bool widen = copies && s.replicate > 1 && g->compact_dev && s.outputs.size() == 1 &&
+                     s.outputs[0].element_size_bytes == 4 && s.out_indices == s.replicate &&
+                     s.out_work_items == 1 && g->widen_per_8 > 0;
   if (widen && !g->compact_host) ECL_CK(cudaHostAlloc(&g->compact_host, g->compact_items * 4, cudaHostAllocPortable));
-  ecl::LaunchEnv env = env_of(g, lane);
-  if (widen) env.compact = g->compact_dev;
-  size_t piece_no = 0;
-  ECL_CK(cudaEventRecord(slot.start, st));
-  for (uint64_t wg = offset_wg; wg < offset_wg + size_wg; wg += piece_wg) {
+  const int other = (lane + 1) % g->lanes;
+  slot.two_lanes = g->lanes > 1 && piece_wg < size_wg;
+  ECL_CK(cudaEventRecord(slot.start, g->lane[lane]));
+  if (slot.two_lanes) ECL_CK(cudaEventRecord(slot.start2, g->lane[other]));
+  size_t piece_no = 0, piece_idx = 0;
+  for (uint64_t wg = offset_wg; wg < offset_wg + size_wg; wg += piece_wg, ++piece_idx) {
+    const int pl = slot.two_lanes && (piece_idx & 1) ? other : lane;
+    cudaStream_t st = g->lane[pl];
+    cudaStream_t cp = g->copy[pl];
+    ecl::LaunchEnv env = env_of(g, pl);
+    if (widen) env.compact = g->compact_dev;
     const uint64_t n_wg = std::min(piece_wg, offset_wg + size_wg - wg);
     const uint64_t first = wg * s.lws, count = n_wg * s.lws;
     cudaError_t e = ecl::launch_kernel(s, env, first, count);
@@ -560,8 +571,8 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
     if (!copies) continue;
     uint64_t p_off = o_off, p_cnt = o_cnt;
     if (piece_wg != size_wg && out_range(s, wg, n_wg, &p_off, &p_cnt) != ECL_OK) return ECL_INDIVISIBLE_PACKAGE;
-    ECL_CK(cudaEventRecord(g->piece[lane], st));
-    ECL_CK(cudaStreamWaitEvent(cp, g->piece[lane], 0));  // captures this recording
+    ECL_CK(cudaEventRecord(g->piece[pl], st));
+    ECL_CK(cudaStreamWaitEvent(cp, g->piece[pl], 0));  // captures this recording
     // widen_per_8 of every 8 pieces go compact + host widening, the rest are
     // copied whole: balances PCIe bytes against host-DRAM traffic.
     if (widen && (g->piece_counter++ % 8) < g->widen_per_8) {
@@ -587,11 +598,18 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
                              cudaMemcpyDeviceToHost, cp));
     }
   }
-  ECL_CK(cudaEventRecord(slot.end, st));
+  ECL_CK(cudaEventRecord(slot.end, g->lane[lane]));
   ECL_CK(cudaStreamWaitEvent(g->notify, slot.end, 0));
+  if (slot.two_lanes) {
+    ECL_CK(cudaEventRecord(slot.end2, g->lane[other]));
+    ECL_CK(cudaStreamWaitEvent(g->notify, slot.end2, 0));
+  }
   if (copies) {
-    ECL_CK(cudaEventRecord(g->copied[lane], cp));
-    ECL_CK(cudaStreamWaitEvent(g->notify, g->copied[lane], 0));
+    for (int l : {lane, other}) {
+      if (l == other && !slot.two_lanes) continue;
+      ECL_CK(cudaEventRecord(g->copied[l], g->copy[l]));
+      ECL_CK(cudaStreamWaitEvent(g->notify, g->copied[l], 0));
+    }
   }
   if (done) ECL_CK(cudaLaunchHostFunc(g->notify, on_package_done, &slot));
   ECL_CK(cudaEventRecord(slot.done, g->notify));
@@ -624,7 +642,14 @@ int ecl_gpu_package_times(ecl_gpu* g, uint64_t seq, double* t_start, double* t_e
   float a = 0.f, b = 0.f, k = 0.f;
   ECL_CK(cudaEventElapsedTime(&a, g->epoch, slot.start));
   ECL_CK(cudaEventElapsedTime(&b, g->epoch, slot.end));
-  ECL_CK(cudaEventElapsedTime(&k, slot.start, slot.end));
+  if (slot.two_lanes) {  // the package spans both lanes: earliest start, latest end
+    float a2 = 0.f, b2 = 0.f;
+    ECL_CK(cudaEventElapsedTime(&a2, g->epoch, slot.start2));
+    ECL_CK(cudaEventElapsedTime(&b2, g->epoch, slot.end2));
+    a = std::min(a, a2);
+    b = std::max(b, b2);
+  }
+  k = b - a;
   *t_start = g->epoch_host_ms + a;
   *t_end = g->epoch_host_ms + b;
   if (!slot.timed) {

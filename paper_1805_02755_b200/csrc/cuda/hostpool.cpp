@@ -49,7 +49,10 @@ void widen(const uint32_t* src, uint32_t* dst, uint64_t count, uint32_t rep) {
 class Pool {
  public:
   Pool() {
-    const unsigned n = std::max(1u, std::thread::hardware_concurrency());
+    // Leave two cores for the engine's device threads and CUDA's own threads:
+    // a descheduled widen worker stalls its piece for a whole time slice.
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned n = hw > 4 ? hw - 2 : hw;
     for (unsigned i = 0; i < n; ++i) threads_.emplace_back([this] { loop(); });
   }
   ~Pool() {
