@@ -140,6 +140,11 @@ int ecl_gpu_poll(ecl_gpu* gpu, uint64_t seq);
 /* Blocks until package `seq` and its copies completed (event wait; returns
  * ECL_KERNEL_PANIC on a device fault instead of hanging). */
 int ecl_gpu_wait(ecl_gpu* gpu, uint64_t seq);
+/* Blocks until package `seq`'s kernels completed; its copies to host memory
+ * (and host widening) may still be in flight — ecl_gpu_sync drains them.
+ * Lets a scheduler pull the next package as soon as the device is free
+ * instead of behind the host-side copy backlog. */
+int ecl_gpu_wait_compute(ecl_gpu* gpu, uint64_t seq);
 /* Start/end of the package's kernel in host steady-clock milliseconds
  * (std::chrono::steady_clock, CLOCK_MONOTONIC), through the device's time
  * anchor.  Valid after completion. */
@@ -148,6 +153,7 @@ int ecl_gpu_package_times(ecl_gpu* gpu, uint64_t seq, double* t_start_ms, double
  * older than 2 s (an event record + synchronize); otherwise returns at once.
  * The clock arguments are unused (kept for ABI stability; pass NULL). */
 int ecl_gpu_set_epoch(ecl_gpu* gpu, double (*host_now_ms)(void*), void* clock_user);
+/* Waits for every submitted package, copies and host widening included. */
 int ecl_gpu_sync(ecl_gpu* gpu);
 /* Exactly-once tally (COEXEC_TALLY=1, engine.hpp:228-252): when enabled,
  * every submitted package also bumps one uint32 per work-item on device. */

@@ -164,7 +164,9 @@ int sync_all(ecl_gpu* g) {
     ECL_CK(cudaStreamSynchronize(g->copy[l]));
   }
   ECL_CK(cudaStreamSynchronize(g->notify));
-  return ECL_OK;
+  bool ok = true;
+  for (auto& s : g->slots) ok = ecl::widen_wait(&s.widen) && ok;  // host widening of the copies
+  return ok ? ECL_OK : fail(ECL_KERNEL_PANIC, "host widening: a copy failed");
 }
 
 // out_range_for (core.hpp:172-185): the package's output-element range.
@@ -515,10 +517,10 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
   if (find_slot(g, seq)) return fail(ECL_SCHEDULER_ERROR, "package seq submitted twice");
   Slot& slot = g->slots[g->next_slot];
   g->next_slot = (g->next_slot + 1) % (kSlots - 1);  // the last slot is reserved for native_run
-  if (slot.busy) {                                   // ring wrapped: oldest must be retired
-    ECL_CK(cudaEventSynchronize(slot.done));
-    ecl::widen_wait(&slot.widen);
-  }
+  // Ring wrapped: the slot's previous package must be retired, copies and
+  // widening included (a package timed by package_times may still be copying).
+  ECL_CK(cudaEventSynchronize(slot.done));
+  if (!ecl::widen_wait(&slot.widen)) return fail(ECL_KERNEL_PANIC, "host widening: a copy failed");
   slot.widen.failed.store(false);
   slot.seq = seq;
   slot.busy = true;
@@ -637,8 +639,8 @@ int ecl_gpu_package_times(ecl_gpu* g, uint64_t seq, double* t_start, double* t_e
   if (!sp) return fail(ECL_CONFIG_ERROR, "package_times: unknown package");
   Slot& slot = *sp;
   if (int rc = set_device(g)) return rc;
-  ECL_CK(cudaEventSynchronize(slot.done));
-  ecl::widen_wait(&slot.widen);
+  ECL_CK(cudaEventSynchronize(slot.end));  // kernel times only: copies may still be in flight
+  if (slot.two_lanes) ECL_CK(cudaEventSynchronize(slot.end2));
   float a = 0.f, b = 0.f, k = 0.f;
   ECL_CK(cudaEventElapsedTime(&a, g->epoch, slot.start));
   ECL_CK(cudaEventElapsedTime(&b, g->epoch, slot.end));
@@ -685,6 +687,15 @@ int ecl_gpu_wait(ecl_gpu* g, uint64_t seq) {
   if (int rc = set_device(g)) return rc;
   ECL_CK(cudaEventSynchronize(sp->done));
   if (!ecl::widen_wait(&sp->widen)) return fail(ECL_KERNEL_PANIC, "host widening: a copy failed");
+  return ECL_OK;
+}
+
+int ecl_gpu_wait_compute(ecl_gpu* g, uint64_t seq) {
+  Slot* sp = find_slot(g, seq);
+  if (!sp) return fail(ECL_CONFIG_ERROR, "wait_compute: unknown package");
+  if (int rc = set_device(g)) return rc;
+  ECL_CK(cudaEventSynchronize(sp->end));
+  if (sp->two_lanes) ECL_CK(cudaEventSynchronize(sp->end2));
   return ECL_OK;
 }
 

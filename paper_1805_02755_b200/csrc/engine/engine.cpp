@@ -214,11 +214,13 @@ struct Engine::Impl {
     if (rs.shared) rs.shared->fail();  // peers stop pulling packages
   }
 
-  // Event-driven completion: blocks on the package's completion event (its
-  // kernel, copies and notify-stream marker); false on a device fault
-  // (recorded), never hangs on a faulted context.
+  // Event-driven completion: blocks on the package's kernel-end events only —
+  // its D2H copies and host widening drain in the background (drive() ends
+  // with ecl_gpu_sync), so the next package is pulled as soon as the device
+  // is free; false on a device fault (recorded), never hangs on a faulted
+  // context.
   bool await(Device& dev, RunState& rs, std::uint64_t seq) {
-    const int rc = ecl_gpu_wait(dev.gpu, seq);
+    const int rc = ecl_gpu_wait_compute(dev.gpu, seq);
     if (rc == ECL_OK) return true;
     fail(rs, Error(code_of_status(rc), std::string("device '") + cfg.devices[dev.index].id + "': " + ecl_last_error()));
     return false;
@@ -294,6 +296,9 @@ struct Engine::Impl {
       std::lock_guard lock(rs.completion);
       rs.completed.push_back(std::move(pkg));
     }
+    // Outputs complete in host memory: pending copies and widening drained.
+    if (const int rc = ecl_gpu_sync(dev.gpu); rc != ECL_OK)
+      fail(rs, Error(code_of_status(rc), std::string("device '") + profile.id + "': " + ecl_last_error()));
   }
 
   ExecutionTrace run_wall(std::span<const void* const> inputs, std::span<void* const> outputs) {
