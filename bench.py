@@ -286,68 +286,86 @@ WORKLOADS = {c.name: c for c in (Mandelbrot, MandelbrotF32, Gaussian, NBody, Bin
 # clocks
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled in-process through
+    NVML every ~2 ms during the timed region, so even a few-millisecond region
+    gets samples (nvidia-smi's process start alone takes longer)."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    PERIOD_S = 0.002
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.samples = []
-        self._proc = None
+        self.samples = []  # (sm_mhz, max_mhz, power_w, reasons bitmask)
+        self._stop = threading.Event()
         self._thread = None
+        self._nvml = None
+        self._handle = None
+        self._error = None
+
+    def _open(self):
+        import pynvml
+        pynvml.nvmlInit()
+        self._nvml = pynvml
+        try:  # NVML enumerates physical GPUs: map through the PCI bus id
+            import torch
+            props = torch.cuda.get_device_properties(self.gpu)
+            bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+            self._handle = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:
+            self._handle = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
 
     def start(self):
         try:
-            self._proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self._proc = None
+            self._open()
+        except Exception as e:  # no NVML: reported, not silently ignored
+            self._error = f"nvml unavailable: {e}"
             return self
-        self._thread = threading.Thread(target=self._read, daemon=True)
+        self._sample()  # one sample at the start of the region
+        self._thread = threading.Thread(target=self._loop, daemon=True)
         self._thread.start()
         return self
 
-    def _read(self):
-        for line in self._proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 9:
-                self.samples.append(parts)
+    def _sample(self):
+        n, h = self._nvml, self._handle
+        try:
+            sm = n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)
+            mx = n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)
+            try:
+                pw = n.nvmlDeviceGetPowerUsage(h) / 1000.0
+            except Exception:
+                pw = None
+            try:
+                rs = n.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                rs = n.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            self.samples.append((sm, mx, pw, rs))
+        except Exception as e:
+            self._error = f"nvml sample failed: {e}"
+
+    def _loop(self):
+        while not self._stop.wait(self.PERIOD_S):
+            self._sample()
 
     def stop(self):
-        if self._proc:
-            self._proc.terminate()
-            try:
-                self._proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self._proc.kill()
         if self._thread:
+            self._stop.set()
             self._thread.join(timeout=5)
+            self._sample()  # and one at the end
         return self.summary()
-
-    @staticmethod
-    def _num(v):
-        try:
-            return float(v)
-        except ValueError:
-            return None
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = sorted(x for x in (self._num(s[1]) for s in self.samples) if x is not None)
-        mx = max((x for x in (self._num(s[2]) for s in self.samples) if x is not None), default=None)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for s in self.samples:
-            for nm, v in zip(names, s[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        power = [x for x in (self._num(s[3]) for s in self.samples) if x is not None]
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(self.samples), "power_w_max": max(power) if power else None}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self._error or "no samples"], "samples": 0}
+        n = self._nvml
+        bits = {"hw_slowdown": getattr(n, "nvmlClocksEventReasonHwSlowdown", 0x8),
+                "hw_thermal_slowdown": getattr(n, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+                "hw_power_brake_slowdown": getattr(n, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+                "sw_thermal_slowdown": getattr(n, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+                "sw_power_cap": getattr(n, "nvmlClocksEventReasonSwPowerCap", 0x4)}
+        sm = sorted(s[0] for s in self.samples)
+        reasons = sorted({name for s in self.samples for name, b in bits.items() if s[3] & b})
+        power = [s[2] for s in self.samples if s[2] is not None]
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml", "power_w_max": max(power) if power else None}
 
 
 def merge_clocks(*cs):

@@ -105,6 +105,21 @@ int ecl_tiles_exactly(const uint64_t* offsets, const uint64_t* sizes, uint64_t n
 int64_t ecl_metrics_report(const char* trace_json, const double* solo_ms, uint32_t n_solo, double reference_ms,
                            char* buf, uint64_t cap);
 int64_t ecl_trace_csv(const char* trace_json, char* buf, uint64_t cap);
+/* The Introspector chart of a trace as SVG (reference chart.hpp:52-154;
+ * byte-identical output). */
+int64_t ecl_chart_svg(const char* trace_json, char* buf, uint64_t cap);
+
+/* ---- experiment harness (reference experiment.hpp:67-181, config.hpp:159-195,
+ * coexec_main.cpp:40-108) ---------------------------------------------------
+ * Runs an experiment file: solo baselines, the scheduler matrix, warm-up
+ * discard and medians; writes traces, charts and summary.json under the
+ * output directory and copies summary.json's path into path_buf.
+ * overrides_json (NULL = none): {"scheduler": {...}, "out_dir": "...",
+ * "exclude_init": bool, "write_traces": bool, "write_csv": bool,
+ * "write_charts": bool, "dump_pgm": bool}. */
+int ecl_experiment_run(const char* config_path, const char* overrides_json, char* path_buf, uint64_t cap);
+/* Parses and validates an experiment file; the `coexec validate` text. */
+int64_t ecl_experiment_validate(const char* config_path, char* buf, uint64_t cap);
 
 const char* ecl_engine_last_error(void);
 

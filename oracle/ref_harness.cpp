@@ -19,6 +19,7 @@
 
 #include "coexec/config.hpp"
 #include "coexec/engine.hpp"
+#include "coexec/experiment.hpp"
 #include "coexec/metrics.hpp"
 #include "coexec/trace_io.hpp"
 #include "coexec/workloads.hpp"
@@ -255,6 +256,21 @@ int ref_out_range(const char* program_json, uint64_t offset_wg, uint64_t size_wg
     return 1 + static_cast<int>(e.code());
   } catch (const std::exception& e) {
     g_error = e.what();
+    return -1;
+  }
+}
+
+// The reference's experiment harness (experiment.hpp:67-181) on one
+// experiment file, output_dir overridden; returns 0 or -1 (message in out).
+int ref_run_experiment(const char* config_path, const char* out_dir, char* out, uint64_t cap) {
+  try {
+    coexec::ExperimentConfig cfg = coexec::load_experiment(config_path);
+    cfg.output_dir = out_dir;
+    coexec::RunOptions opts;
+    coexec::run_experiment(cfg, opts);
+    return 0;
+  } catch (const std::exception& e) {
+    copy_out(e.what(), out, cap);
     return -1;
   }
 }

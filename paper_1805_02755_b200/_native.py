@@ -69,6 +69,9 @@ _sig("ecl_out_range_for", c_int, c_char_p, c_u64, c_u64, ctypes.POINTER(c_u64), 
 _sig("ecl_tiles_exactly", c_int, ctypes.POINTER(c_u64), ctypes.POINTER(c_u64), c_u64, c_u64)
 _sig("ecl_metrics_report", c_i64, c_char_p, ctypes.POINTER(c_dbl), c_u32, c_dbl, c_char_p, c_u64)
 _sig("ecl_trace_csv", c_i64, c_char_p, c_char_p, c_u64)
+_sig("ecl_chart_svg", c_i64, c_char_p, c_char_p, c_u64)
+_sig("ecl_experiment_run", c_int, c_char_p, c_char_p, c_char_p, c_u64)
+_sig("ecl_experiment_validate", c_i64, c_char_p, c_char_p, c_u64)
 _sig("ecl_engine_last_error", c_char_p)
 # device layer (subset used from Python)
 _sig("ecl_gpu_count", c_int, ctypes.POINTER(c_int))

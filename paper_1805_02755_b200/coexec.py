@@ -252,7 +252,51 @@ class ExecutionTrace:
         return json.dumps(self.raw, indent=2)
 
     def to_csv(self) -> str:
-        return N.read_string(N.lib.ecl_trace_csv, json.dumps(self.raw).encode())
+        return _checked_string(N.lib.ecl_trace_csv, json.dumps(self.raw).encode())
+
+    def to_svg(self) -> str:
+        """The Introspector package chart (reference chart.hpp:52-154)."""
+        return _checked_string(N.lib.ecl_chart_svg, json.dumps(self.raw).encode())
+
+
+def _checked_string(fn, *args) -> str:
+    s = N.read_string(fn, *args)
+    if isinstance(s, int):
+        _raise(s)
+    return s
+
+
+# ---------------------------------------------------------------------------
+# experiment harness (experiment.hpp:67-181, config.hpp:159-195)
+
+def run_experiment(config_path: str, scheduler: Optional[dict] = None, out_dir: Optional[str] = None,
+                   exclude_init: Optional[bool] = None, write_traces: bool = True, write_csv: bool = False,
+                   write_charts: bool = True, dump_pgm: bool = False) -> dict:
+    """Runs an experiment file (solo baselines + scheduler matrix, warm-up
+    discard, medians); writes traces / charts / summary.json under the
+    output directory and returns the parsed summary (plus "summary_file")."""
+    o: dict = {"write_traces": write_traces, "write_csv": write_csv, "write_charts": write_charts,
+               "dump_pgm": dump_pgm}
+    if scheduler is not None:
+        o["scheduler"] = scheduler
+    if out_dir is not None:
+        o["out_dir"] = str(out_dir)
+    if exclude_init is not None:
+        o["exclude_init"] = bool(exclude_init)
+    buf = ctypes.create_string_buffer(4096)
+    rc = N.lib.ecl_experiment_run(str(config_path).encode(), json.dumps(o).encode(), buf, len(buf))
+    if rc != 0:
+        _raise(rc)
+    path = buf.value.decode()
+    with open(path) as f:
+        summary = json.load(f)
+    summary["summary_file"] = path
+    return summary
+
+
+def validate_experiment(config_path: str) -> str:
+    """What `coexec validate` prints; raises Error on a bad file."""
+    return _checked_string(N.lib.ecl_experiment_validate, str(config_path).encode())
 
 
 # ---------------------------------------------------------------------------

@@ -7,7 +7,9 @@
 #include <string>
 #include <vector>
 
+#include "coexec/chart.hpp"
 #include "coexec/engine.hpp"
+#include "coexec/experiment.hpp"
 #include "coexec/json_io.hpp"
 #include "ecl_engine.h"
 
@@ -354,6 +356,39 @@ int64_t ecl_metrics_report(const char* trace_json, const double* solo, uint32_t 
 
 int64_t ecl_trace_csv(const char* trace_json, char* buf, uint64_t cap) {
   return guarded_string([&] { return trace_to_csv(trace_from_json(json::parse(trace_json))); }, buf, cap);
+}
+
+int64_t ecl_chart_svg(const char* trace_json, char* buf, uint64_t cap) {
+  return guarded_string([&] { return render_svg(trace_from_json(json::parse(trace_json))); }, buf, cap);
+}
+
+int ecl_experiment_run(const char* config_path, const char* overrides_json, char* path_buf, uint64_t cap) {
+  return guarded(nullptr, [&] {
+    ExperimentConfig cfg = load_experiment(config_path);
+    RunOptions opts;
+    if (overrides_json && *overrides_json) {
+      const json o = json::parse(overrides_json);
+      if (o.contains("scheduler")) {
+        SchedulerConfig s = scheduler_from_json(o.at("scheduler"));
+        if (auto* st = std::get_if<StaticConfig>(&s)) *st = resolve_static(*st, cfg.devices);
+        cfg.schedulers = {s};
+      }
+      if (o.contains("out_dir")) cfg.output_dir = o.at("out_dir").get<std::string>();
+      cfg.exclude_init = o.value("exclude_init", cfg.exclude_init);
+      opts.write_traces = o.value("write_traces", opts.write_traces);
+      opts.write_csv = o.value("write_csv", opts.write_csv);
+      opts.write_charts = o.value("write_charts", opts.write_charts);
+      opts.dump_pgm = o.value("dump_pgm", opts.dump_pgm);
+    }
+    const ExperimentResult r = run_experiment(cfg, opts);
+    const std::string path = r.summary_file.string();
+    if (!path_buf || cap <= path.size()) throw Error(ErrorCode::ConfigError, "summary path buffer too small");
+    std::memcpy(path_buf, path.c_str(), path.size() + 1);
+  });
+}
+
+int64_t ecl_experiment_validate(const char* config_path, char* buf, uint64_t cap) {
+  return guarded_string([&] { return describe_experiment(load_experiment(config_path)); }, buf, cap);
 }
 
 }  // extern "C"

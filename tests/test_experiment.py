@@ -1,0 +1,144 @@
+"""Experiment harness, CLI and Introspector chart
+against what the reference's own harness writes for the same experiment
+files (tests/golden/experiments/, made by tests/golden/make_experiments.py
+from oracle/_ref; the mandelbrot-batel fixtures also equal the reference
+repo's committed proj/out/mandelbrot-batel files, up to nlohmann's line
+breaking of the args array).
+
+CPU: every golden trace re-rendered as SVG byte-for-byte; vecscale-batel run
+end to end (analytic costs); validate / chart / exit codes through the CLI.
+GPU: the Mandelbrot experiments, whose virtual-clock cost table (the escape
+counts) is computed by the B200 kernel, and a wall-clock B200 experiment.
+"""
+import glob
+import json
+import os
+import shutil
+import subprocess
+
+import pytest
+
+import paper_1805_02755_b200 as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden", "experiments")
+CLI = os.path.join(ROOT, "paper_1805_02755_b200", "_lib", "coexec")
+
+
+def golden_traces():
+    return sorted(glob.glob(os.path.join(GOLD, "*", "*-rep0.trace.json")))
+
+
+@pytest.mark.parametrize("path", golden_traces(), ids=lambda p: "/".join(p.split(os.sep)[-2:]))
+def test_chart_svg_is_byte_identical_to_reference(path):
+    with open(path) as f:
+        trace = P.ExecutionTrace(json.load(f))
+    with open(path.replace("-rep0.trace.json", "-median.svg")) as f:
+        expected = f.read()
+    assert trace.to_svg() == expected
+
+
+def check_against_golden(name, out_dir, summary):
+    gold = os.path.join(GOLD, name)
+    with open(os.path.join(gold, "summary.json")) as f:
+        assert f.read() == open(summary["summary_file"]).read()
+    for g in glob.glob(os.path.join(gold, "*-rep0.trace.json")):
+        ref = json.load(open(g))
+        for rep in sorted(glob.glob(os.path.join(out_dir, os.path.basename(g).replace("-rep0", "-rep*")))):
+            assert json.load(open(rep)) == ref, rep
+            assert open(rep).read() == open(g).read(), rep
+    for g in glob.glob(os.path.join(gold, "*.svg")):
+        assert open(os.path.join(out_dir, os.path.basename(g))).read() == open(g).read(), g
+
+
+def test_vecscale_experiment_matches_reference_harness(tmp_path):
+    out = tmp_path / "out"
+    s = P.run_experiment(os.path.join(GOLD, "vecscale-batel", "experiment.json"), out_dir=str(out))
+    check_against_golden("vecscale-batel", str(out), s)
+    assert [o["name"] for o in s["outcomes"]] == ["s0-static", "s1-dynamic", "s2-hguided"]
+
+
+def test_experiment_overrides_and_csv(tmp_path):
+    out = tmp_path / "o"
+    s = P.run_experiment(os.path.join(GOLD, "vecscale-batel", "experiment.json"), out_dir=str(out),
+                         scheduler={"type": "dynamic", "num_packages": 7}, write_csv=True, write_charts=False)
+    assert [o["name"] for o in s["outcomes"]] == ["s0-dynamic"]
+    assert s["outcomes"][0]["description"].startswith("dynamic")
+    csvs = sorted(os.listdir(out))
+    assert "s0-dynamic-rep0.trace.csv" in csvs and not any(c.endswith(".svg") for c in csvs)
+    head = open(out / "s0-dynamic-rep0.trace.csv").readline().strip()
+    assert head == "seq,device_id,offset_wg,size_wg,t_enqueue_ms,t_start_ms,t_end_ms"
+
+
+def test_validate_text_and_errors(tmp_path):
+    text = P.validate_experiment(os.path.join(GOLD, "mandelbrot-batel", "experiment.json"))
+    assert text.startswith("ok: mandelbrot, gws 262144, lws 256, 1024 work-groups, 3 devices, 5 schedulers")
+    assert "hguided" in text
+    bad = json.load(open(os.path.join(GOLD, "vecscale-batel", "experiment.json")))
+    bad["devices_file"] = os.path.join(GOLD, "vecscale-batel", "profile.json")
+    bad["warmup_discard"] = bad["repetitions"]
+    p = tmp_path / "bad.json"
+    p.write_text(json.dumps(bad))
+    with pytest.raises(P.Error) as e:
+        P.validate_experiment(str(p))
+    assert e.value.code == P.ErrorCode.ConfigError
+    bad["warmup_discard"] = 0
+    bad["program"]["global_work_size"] = 1000  # lws 128 does not divide
+    p.write_text(json.dumps(bad))
+    with pytest.raises(P.Error) as e:
+        P.validate_experiment(str(p))
+    assert e.value.code == P.ErrorCode.NonDivisibleWorkSize
+
+
+def cli(*args, cwd=None):
+    return subprocess.run([CLI, *args], capture_output=True, text=True, timeout=600, cwd=cwd)
+
+
+def test_cli_validate_chart_and_exit_codes(tmp_path):
+    r = cli("validate", os.path.join(GOLD, "remo-missing.json"))
+    assert r.returncode == 1 and "cannot open" in r.stderr
+    r = cli("validate", os.path.join(GOLD, "mandelbrot-remo", "experiment.json"))
+    assert r.returncode == 0 and r.stdout.startswith("ok: mandelbrot")
+    trace = os.path.join(GOLD, "mandelbrot-remo", "s3-hguided-rep0.trace.json")
+    out = tmp_path / "c.svg"
+    r = cli("chart", trace, "-o", str(out))
+    assert r.returncode == 0, r.stderr
+    assert out.read_text() == open(trace.replace("-rep0.trace.json", "-median.svg")).read()
+    r = cli("run", os.path.join(GOLD, "vecscale-batel", "experiment.json"), "--scheduler", "bogus")
+    assert r.returncode == 1 and "--scheduler" in r.stderr
+    r = cli("run", os.path.join(GOLD, "vecscale-batel", "experiment.json"), "--out-dir", str(tmp_path / "v"),
+            "--format", "json", "--scheduler", "static", "--props", "0.5,0.25")
+    assert r.returncode == 0, r.stderr
+    s = json.loads(r.stdout)
+    assert s["outcomes"][0]["scheduler"]["proportions"] == [0.5, 0.25, 0.25]
+    r = cli("frobnicate")
+    assert r.returncode == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["mandelbrot-batel", "mandelbrot-remo"])
+def test_mandelbrot_virtual_experiment_matches_reference(name, tmp_path, gpu_available):
+    # the per-pixel cost table (escape counts) comes from the B200 kernel
+    out = tmp_path / "out"
+    s = P.run_experiment(os.path.join(GOLD, name, "experiment.json"), out_dir=str(out))
+    check_against_golden(name, str(out), s)
+
+
+@pytest.mark.gpu
+def test_wall_clock_b200_experiment(tmp_path, gpu_available):
+    cfg = json.load(open(os.path.join(ROOT, "experiments", "b200-mandelbrot-small.json")))
+    cfg["output_dir"] = str(tmp_path / "out")
+    p = tmp_path / "exp.json"
+    p.write_text(json.dumps(cfg))
+    r = cli("run", str(p), "--dump-pgm")
+    assert r.returncode == 0, r.stderr
+    s = json.load(open(tmp_path / "out" / "summary.json"))
+    assert s["clock_mode"] == "wall" and len(s["outcomes"]) == len(cfg["schedulers"])
+    for o in s["outcomes"]:
+        m = o["metrics"]
+        assert 0 < m["balance"] <= 1.0 and m["speedup"] > 0 and abs(sum(m["work_share"].values()) - 1) < 1e-9
+        assert len(o["t_totals_ms"]) == cfg["repetitions"] - cfg["warmup_discard"]
+        t = P.ExecutionTrace(json.load(open(tmp_path / "out" / o["median_trace"])))
+        assert P.tiles_exactly(t.packages, t.raw["program"]["total_work_groups"])
+    pgm = sorted(glob.glob(str(tmp_path / "out" / "*.pgm")))
+    assert pgm and open(pgm[0], "rb").read(2) == b"P5"
