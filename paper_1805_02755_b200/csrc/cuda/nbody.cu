@@ -5,15 +5,16 @@
 //   acc_i = sum_j m_j * r_ij / (|r_ij|^2 + eps2)^(3/2),  r_ij = p_j - p_i
 //   p_i' = p_i + v_i dt + acc_i dt^2 / 2,   v_i' = v_i + acc_i dt
 //
-// Mapping: a thread integrates B consecutive-in-block bodies of the package
-// (independent accumulator chains); the CTA walks the whole body array in
-// T-body tiles staged in shared memory as float4 (xyz + mass), so each
-// source body is read from L2 once per CTA and from shared memory
-// (broadcast) by every thread.  Per interaction: 3 FADD, 3 FFMA
-// (|r|^2 + eps2), one MUFU.RSQ, 3 FMUL (m/r^3), 3 FFMA (acc): FP32-pipe
-// bound (the "20 flops/interaction" convention).  The grid is
-// sized so a package of 1M/8 bodies gives every SM several CTAs (the first
-// profile showed < 2 CTAs/SM and 21 % warp occupancy with 512-body CTAs).
+// Mapping: a thread integrates B = 2 bodies of the package (one packed
+// float2 pair per coordinate, FFMA2/FADD2/FMUL2) against a contiguous share of every 1024-body source
+// tile staged in shared memory as float4 (xyz + mass): each source body is
+// read from L2 once per CTA and from shared memory (broadcast) by every
+// thread.  Per interaction: 3 FADD, 3 FFMA (|r|^2 + eps2), one MUFU.RSQ,
+// 3 FMUL (m/r^3), 3 FFMA (acc) — 12 FP32 operations for the "20
+// flops/interaction" convention, issued as 6 packed
+// instructions per target, so the attainable ceiling is 20/24 of the FFMA
+// peak without the issue slots binding first.  The source split S is chosen per launch so even a
+// small package fills every SM (the first profile: 21 % warp occupancy).
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -23,40 +24,99 @@
 namespace ecl {
 namespace {
 
-template <int T, int B>
-__global__ void __launch_bounds__(T)
+// CTA = kThreads threads = T target slots x S source splits; thread
+// (s, t) = threadIdx.x / T, % T integrates B targets (t, t+T, ...) against
+// the s-th contiguous quarter/eighth/... of every source tile, so all lanes
+// of a warp (same s) read the same shared-memory word (broadcast).  Partial
+// accelerations of the S splits are summed in split order at the end.  S > 1
+// multiplies the CTAs of a package — small packages (Dynamic at 8 GPUs is
+// 32768 bodies) otherwise leave most of the 148 SMs idle.
+constexpr int kThreads = 256;
+constexpr int kTile = 4 * kThreads;  // sources staged per __syncthreads pair
+
+// 1/sqrt on the MUFU without the denormal-input fixup rsqrtf carries
+// (FSETP + 2 predicated FMUL per call): d2 >= eps2 > 0 is never denormal.
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// One thread integrates 2*B2 targets held as B2 packed pairs (float2 per
+// coordinate): every interaction step is an FADD2/FFMA2/FMUL2 on the pair
+// (the source body is a broadcast .F32 operand), halving the FP32 issue
+// slots; only the two MUFU.RSQ stay scalar.
+template <int S, int B2>
+__global__ void __launch_bounds__(kThreads)
     nbody_step(const float4* __restrict__ pos, const float4* __restrict__ vel, uint64_t n, float dt, float eps2,
                float4* __restrict__ npos, float4* __restrict__ nvel, uint64_t first, uint64_t count) {
-  __shared__ float4 tile[T];
-  const uint64_t base = first + (static_cast<uint64_t>(blockIdx.x) * T * B) + threadIdx.x;
+  constexpr int T = kThreads / S, B = 2 * B2;
+  __shared__ float4 tile[kTile];
+  __shared__ float3 part[S > 1 ? (S - 1) * B * T : 1];
+  const int t = threadIdx.x % T, split = threadIdx.x / T;
+  const uint64_t base = first + static_cast<uint64_t>(blockIdx.x) * T * B + t;
   float4 p[B];
-  float ax[B], ay[B], az[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) {
     const uint64_t i = base + static_cast<uint64_t>(b) * T;
     p[b] = i < first + count ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-    ax[b] = ay[b] = az[b] = 0.0f;
   }
-  for (uint64_t t0 = 0; t0 < n; t0 += T) {
-    const uint64_t j = t0 + threadIdx.x;
-    tile[threadIdx.x] = j < n ? pos[j] : make_float4(0.f, 0.f, 0.f, 0.f);  // mass 0: no force
-    __syncthreads();
-    const int lim = n - t0 < static_cast<uint64_t>(T) ? static_cast<int>(n - t0) : T;
-#pragma unroll 8
-    for (int k = 0; k < lim; ++k) {
-      const float4 q = tile[k];
+  float2 px[B2], py[B2], pz[B2], ax[B2], ay[B2], az[B2];
 #pragma unroll
-      for (int b = 0; b < B; ++b) {
-        const float rx = q.x - p[b].x, ry = q.y - p[b].y, rz = q.z - p[b].z;
-        const float d2 = fmaf(rx, rx, fmaf(ry, ry, fmaf(rz, rz, eps2)));
-        const float inv = rsqrtf(d2);
-        const float s = q.w * (inv * inv * inv);
-        ax[b] = fmaf(s, rx, ax[b]);
-        ay[b] = fmaf(s, ry, ay[b]);
-        az[b] = fmaf(s, rz, az[b]);
+  for (int h = 0; h < B2; ++h) {
+    px[h] = make_float2(p[2 * h].x, p[2 * h + 1].x);
+    py[h] = make_float2(p[2 * h].y, p[2 * h + 1].y);
+    pz[h] = make_float2(p[2 * h].z, p[2 * h + 1].z);
+    ax[h] = ay[h] = az[h] = make_float2(0.f, 0.f);
+  }
+  const float2 e2 = make_float2(eps2, eps2);
+  for (uint64_t t0 = 0; t0 < n; t0 += kTile) {
+#pragma unroll
+    for (int r = 0; r < kTile / kThreads; ++r) {
+      const uint64_t j = t0 + r * kThreads + threadIdx.x;
+      tile[r * kThreads + threadIdx.x] = j < n ? pos[j] : make_float4(0.f, 0.f, 0.f, 0.f);  // mass 0: no force
+    }
+    __syncthreads();
+    const float4* src = tile + split * (kTile / S);
+#pragma unroll 4
+    for (int k = 0; k < kTile / S; ++k) {
+      const float4 q = src[k];
+#pragma unroll
+      for (int h = 0; h < B2; ++h) {
+        const float2 rx = __fadd2_rn(make_float2(q.x, q.x), make_float2(-px[h].x, -px[h].y));
+        const float2 ry = __fadd2_rn(make_float2(q.y, q.y), make_float2(-py[h].x, -py[h].y));
+        const float2 rz = __fadd2_rn(make_float2(q.z, q.z), make_float2(-pz[h].x, -pz[h].y));
+        const float2 d2 = __ffma2_rn(rx, rx, __ffma2_rn(ry, ry, __ffma2_rn(rz, rz, e2)));
+        const float2 inv = make_float2(rsqrt_ftz(d2.x), rsqrt_ftz(d2.y));
+        const float2 s = __fmul2_rn(__fmul2_rn(make_float2(q.w, q.w), inv), __fmul2_rn(inv, inv));
+        ax[h] = __ffma2_rn(s, rx, ax[h]);
+        ay[h] = __ffma2_rn(s, ry, ay[h]);
+        az[h] = __ffma2_rn(s, rz, az[h]);
       }
     }
     __syncthreads();
+  }
+  float3 acc[B];
+#pragma unroll
+  for (int h = 0; h < B2; ++h) {
+    acc[2 * h] = make_float3(ax[h].x, ay[h].x, az[h].x);
+    acc[2 * h + 1] = make_float3(ax[h].y, ay[h].y, az[h].y);
+  }
+  if constexpr (S > 1) {
+    if (split > 0) {
+#pragma unroll
+      for (int b = 0; b < B; ++b) part[((split - 1) * B + b) * T + t] = acc[b];
+    }
+    __syncthreads();
+    if (split > 0) return;
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      for (int s2 = 1; s2 < S; ++s2) {
+        const float3 q = part[((s2 - 1) * B + b) * T + t];
+        acc[b].x += q.x;
+        acc[b].y += q.y;
+        acc[b].z += q.z;
+      }
   }
   const float hdt2 = 0.5f * dt * dt;
 #pragma unroll
@@ -64,17 +124,17 @@ __global__ void __launch_bounds__(T)
     const uint64_t i = base + static_cast<uint64_t>(b) * T;
     if (i >= first + count) continue;
     const float4 v = vel[i];
-    npos[i] = make_float4(p[b].x + v.x * dt + ax[b] * hdt2, p[b].y + v.y * dt + ay[b] * hdt2,
-                          p[b].z + v.z * dt + az[b] * hdt2, p[b].w);
-    nvel[i] = make_float4(v.x + ax[b] * dt, v.y + ay[b] * dt, v.z + az[b] * dt, v.w);
+    npos[i] = make_float4(p[b].x + v.x * dt + acc[b].x * hdt2, p[b].y + v.y * dt + acc[b].y * hdt2,
+                          p[b].z + v.z * dt + acc[b].z * hdt2, p[b].w);
+    nvel[i] = make_float4(v.x + acc[b].x * dt, v.y + acc[b].y * dt, v.z + acc[b].z * dt, v.w);
   }
 }
 
-template <int T, int B>
+template <int S, int B2>
 cudaError_t launch(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
-  const uint64_t per_block = static_cast<uint64_t>(T) * B;
+  const uint64_t per_block = static_cast<uint64_t>(kThreads / S) * 2 * B2;
   const uint64_t blocks = (count + per_block - 1) / per_block;
-  nbody_step<T, B><<<static_cast<unsigned>(blocks), T, 0, env.stream>>>(
+  nbody_step<S, B2><<<static_cast<unsigned>(blocks), kThreads, 0, env.stream>>>(
       static_cast<const float4*>(env.in[0]), static_cast<const float4*>(env.in[1]), spec.nbody.bodies,
       spec.nbody.dt, spec.nbody.eps2, static_cast<float4*>(env.out[0]), static_cast<float4*>(env.out[1]), first,
       count);
@@ -85,17 +145,24 @@ cudaError_t launch(const KernelSpec& spec, const LaunchEnv& env, uint64_t first,
 
 cudaError_t launch_nbody(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
   if (count == 0) return cudaSuccess;
-  // Tuning hook (ECL_NBODY_VARIANT): CTA size x bodies per thread.
-  static const int variant = [] {
-    const char* v = std::getenv("ECL_NBODY_VARIANT");
+  // Source splits: the fewest that still give ~4 CTAs per SM for this
+  // package (ECL_NBODY_SPLIT forces 1/2/4/8).
+  static const int forced = [] {
+    const char* v = std::getenv("ECL_NBODY_SPLIT");
     return v ? std::atoi(v) : 0;
   }();
-  switch (variant) {
-    case 1: return launch<256, 2>(spec, env, first, count);  // the first version
-    case 2: return launch<256, 1>(spec, env, first, count);
-    case 3: return launch<64, 2>(spec, env, first, count);
-    case 4: return launch<128, 4>(spec, env, first, count);
-    default: return launch<128, 2>(spec, env, first, count);
+  constexpr int B2 = 1, B = 2 * B2;
+  const uint64_t want = 4ull * static_cast<uint64_t>(env.sms > 0 ? env.sms : 148);
+  int split = forced;
+  if (split <= 0) {
+    split = 1;
+    while (split < 8 && (count + (kThreads / split) * B - 1) / ((kThreads / split) * B) < want) split *= 2;
+  }
+  switch (split) {
+    case 1: return launch<1, B2>(spec, env, first, count);
+    case 2: return launch<2, B2>(spec, env, first, count);
+    case 4: return launch<4, B2>(spec, env, first, count);
+    default: return launch<8, B2>(spec, env, first, count);
   }
 }
 

@@ -99,6 +99,35 @@ def test_binomial_matches_oracle(gpu_available, oracle, options, steps, n_dev, s
     assert ok, f"max rel err {worst}"
 
 
+_VARIANT_SCRIPT = """
+import sys, numpy as np
+import paper_1805_02755_b200 as P
+from paper_1805_02755_b200 import workloads as W
+opts = 4 * 777
+rand = W.binomial_inputs(opts, seed=11)[0]
+prog = P.validate_program(W.binomial_spec(opts))
+with P.Engine(P.EngineConfig([P.cuda_device("gpu0", 0)], P.DynamicConfig(13)), prog) as e:
+    np.save(sys.argv[1], e.run([rand]).outputs[0].view(np.float32))
+"""
+
+
+def test_binomial_packed_lattice_is_bit_identical_to_scalar(gpu_available, tmp_path):
+    # FFMA2/FADD2 round each component like FFMA/FADD: the packed two-options-
+    # per-warp kernel must reproduce the scalar kernel (ECL_BINOMIAL_VARIANT=1)
+    import os
+    import subprocess
+    import sys
+    outs = []
+    for variant in ("1", "0"):
+        f = tmp_path / f"v{variant}.npy"
+        env = dict(os.environ, ECL_BINOMIAL_VARIANT=variant)
+        r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, str(f)], env=env, capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        outs.append(np.load(f))
+    assert outs[0].view(np.uint32).tolist() == outs[1].view(np.uint32).tolist()
+
+
 def test_binomial_prices_are_sane(gpu_available):
     options = 4 * 256
     rand = W.binomial_inputs(options, seed=3)[0]
