@@ -9,7 +9,7 @@
 // Mapping: one warp per option pair.  Lane l holds lattice nodes
 // t = 8l .. 8l+7 in registers (255 nodes for 254 steps); a backward step
 //   c[t] <- puByr * c[t+1] + pdByr * c[t]      (t < j)
-// is 8 register updates per lane plus one warp shuffle for the neighbour
+// is 8 register FMAs per lane (scaled form, below) plus one warp shuffle for the neighbour
 // node c[8l+8] held by lane l+1 — the OpenCL kernel's local-memory lattice
 // and barriers become registers and __shfl_down_sync.  The two options of a
 // warp travel packed in float2 registers through FFMA2/FADD2 (half the
@@ -33,10 +33,12 @@ constexpr int kNodesPerLane = 8;  // 32 x 8 = 256 >= steps + 1 for steps <= 255
 // exactly like __fmaf_rn / __fadd_rn, so the packed kernel's prices are
 // bit-identical to the scalar kernel's; it issues half the FP32
 // instructions, which is what bounds this kernel (ncu: issue-bound).
-__device__ __forceinline__ float lattice_step(float c, float c1, float pu) { return fmaf(pu, c1 - c, c); }
-__device__ __forceinline__ float2 lattice_step(float2 c, float2 c1, float2 pu) {
-  return __ffma2_rn(pu, __fadd2_rn(c1, make_float2(-c.x, -c.y)), c);
-}
+// One FMA per node: the lattice is carried scaled, w = c / pd^m (m = steps
+// since the last rescale), so pd*c + pu*c1 becomes w + (pu/pd)*w1.
+__device__ __forceinline__ float lattice_step(float w, float w1, float r) { return fmaf(r, w1, w); }
+__device__ __forceinline__ float2 lattice_step(float2 w, float2 w1, float2 r) { return __ffma2_rn(r, w1, w); }
+__device__ __forceinline__ float rescale(float w, float s) { return w * s; }
+__device__ __forceinline__ float2 rescale(float2 w, float2 s) { return __fmul2_rn(w, s); }
 __device__ __forceinline__ float shfl_down1(float v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 __device__ __forceinline__ float2 shfl_down1(float2 v) {
   return make_float2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
@@ -47,16 +49,22 @@ __device__ __forceinline__ float2 shfl_from(float2 v, unsigned src) {
 }
 
 // Backward steps j, j-1, ... while j > stop, with NL nodes per lane (lane l
-// holds nodes NL*l .. NL*l+NL-1): c[t] <- c[t] + pu*(c[t+1] - c[t]).  The
-// neighbour of a lane's last node is the next lane's first (one shuffle).
-// Returns the next j.  After it, only nodes t < stop are live.
+// holds nodes NL*l .. NL*l+NL-1): w[t] <- w[t] + r*w[t+1].  The neighbour of
+// a lane's last node is the next lane's first (one shuffle).  Whenever the
+// level reaches a multiple of 32 the lattice is rescaled by pd^32, so w stays
+// within ~pd^-32 of the true value (no f32 overflow).  Returns the next j.
+// After it, only nodes t < stop are live.
 template <int NL, typename V>
-__device__ __forceinline__ int backward(V (&c)[NL], int j, int stop, V pu) {
+__device__ __forceinline__ int backward(V (&c)[NL], int j, int stop, V r, V s32) {
   for (; j > stop; --j) {
     const V right = shfl_down1(c[0]);
 #pragma unroll
-    for (int k = 0; k < NL - 1; ++k) c[k] = lattice_step(c[k], c[k + 1], pu);
-    c[NL - 1] = lattice_step(c[NL - 1], right, pu);
+    for (int k = 0; k < NL - 1; ++k) c[k] = lattice_step(c[k], c[k + 1], r);
+    c[NL - 1] = lattice_step(c[NL - 1], right, r);
+    if (((j - 1) & 31) == 0 && j > 1) {
+#pragma unroll
+      for (int k = 0; k < NL; ++k) c[k] = rescale(c[k], s32);
+    }
   }
   return j;
 }
@@ -77,7 +85,8 @@ __device__ __forceinline__ void repack(const V (&c)[NL], V (&h)[NL / 2], unsigne
 // uniform r, dt = T/steps, u = exp(sigma sqrt(dt)), pu = (a - d)/(u - d).
 struct Option {
   double S, K, T, vsdt, u;
-  float pu;
+  float r, s32;  // pu/pd and pd^32 (the scaled lattice's step and rescale factors)
+  double tail;   // pd^(steps - 32*rescales) * exp(-R T): undoes the remaining scale, discounts
 };
 
 __device__ __forceinline__ Option option_params(double r, int steps) {
@@ -90,16 +99,30 @@ __device__ __forceinline__ Option option_params(double r, int steps) {
   const double a = exp(0.02 * dt);
   o.u = exp(o.vsdt);
   const double d = 1.0 / o.u;
-  o.pu = static_cast<float>((a - d) / (o.u - d));
+  const double pu = (a - d) / (o.u - d), pd = 1.0 - pu;
+  o.r = static_cast<float>(pu / pd);
+  double p32 = pd;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) p32 *= p32;  // pd^32
+  o.s32 = static_cast<float>(p32);
+  // Undo the scale left after the last rescale (pd^e, e = steps - 32 R) and
+  // the f32 rounding of the R rescale factors, then discount exp(-R T).
+  const int rescales = (steps - 1) / 32;
+  const double q = static_cast<double>(o.s32) / p32;
+  double tail = exp(-0.02 * o.T);
+  for (int i = 0; i < steps - 32 * rescales; ++i) tail *= pd;
+  for (int i = 0; i < rescales; ++i) tail /= q;
+  o.tail = tail;
   return o;
 }
 
-// Leaves in FP64, then the lattice in FP32 with the per-step discount 1/a
-// factored out: c <- c0 + pu*(c1 - c0) is the reference's puByr*c1 +
-// pdByr*c0 times a, and a^-steps = exp(-R T) is applied once at the end, so
-// rounding 1/a to f32 does not compound 254 times.  S*exp(vsdt*(2t -
-// steps)) for the lane's 8 nodes: one exp per lane, then successive factors
-// u^2 = exp(2 vsdt) (FP64, ~1e-16 relative drift).
+// Leaves in FP64, then the lattice in FP32.  The per-step discount 1/a is
+// factored out (applied once as exp(-R T) at the end, so rounding it to f32
+// does not compound 254 times) and the lattice is carried scaled by
+// pd^-m: pd*c + pu*c1 becomes one FMA w + (pu/pd)*w1, rescaled by pd^32 at
+// every level that is a multiple of 32; `tail` undoes the rest.  Leaves
+// S*exp(vsdt*(2t - steps)) for the lane's 8 nodes: one exp per lane, then
+// successive factors u^2 (FP64, ~1e-16 relative drift).
 __device__ __forceinline__ void leaves(const Option& o, int steps, unsigned lane, float (&c)[kNodesPerLane]) {
   double st = o.S * exp(o.vsdt * static_cast<double>(2 * static_cast<int>(lane) * kNodesPerLane - steps));
   const double u2 = o.u * o.u;
@@ -116,18 +139,18 @@ __device__ __forceinline__ void leaves(const Option& o, int steps, unsigned lane
 // in 128 / 64 / 32 nodes the warp repacks to 4 / 2 / 1 nodes per lane (one
 // shuffle per register), so later steps cost proportionally less.
 template <typename V>
-__device__ __forceinline__ V lattice(V (&c)[kNodesPerLane], int steps, V pu, unsigned lane) {
+__device__ __forceinline__ V lattice(V (&c)[kNodesPerLane], int steps, V r, V s32, unsigned lane) {
   int j = steps;
-  j = backward<8>(c, j, 128, pu);
+  j = backward<8>(c, j, 128, r, s32);
   V c4[4];
   repack<8>(c, c4, lane);
-  j = backward<4>(c4, j, 64, pu);
+  j = backward<4>(c4, j, 64, r, s32);
   V c2[2];
   repack<4>(c4, c2, lane);
-  j = backward<2>(c2, j, 32, pu);
+  j = backward<2>(c2, j, 32, r, s32);
   V c1[1];
   repack<2>(c2, c1, lane);
-  backward<1>(c1, j, 0, pu);
+  backward<1>(c1, j, 0, r, s32);
   return c1[0];
 }
 
@@ -146,22 +169,36 @@ __global__ void __launch_bounds__(kThreads, 4)
       const Option a = option_params(rand[o], steps);
       float c[kNodesPerLane];
       leaves(a, steps, lane, c);
-      const float v = lattice(c, steps, a.pu, lane);
-      if (lane == 0) out[o] = static_cast<float>(static_cast<double>(v) * exp(-0.02 * a.T));
+      const float v = lattice(c, steps, a.r, a.s32, lane);
+      if (lane == 0) out[o] = static_cast<float>(static_cast<double>(v) * a.tail);
     } else {
       const bool has_b = w * P + 1 < n_opt;
-      const Option a = option_params(rand[o], steps);
-      const Option b = option_params(has_b ? rand[o + 1] : rand[o], steps);
-      float ca[kNodesPerLane], cb[kNodesPerLane];
-      leaves(a, steps, lane, ca);
-      leaves(b, steps, lane, cb);
-      float2 c[kNodesPerLane];
+      float2 c[kNodesPerLane], r, s32;
+      double tail_a, tail_b;
+      {  // one option's FP64 setup at a time (register pressure)
+        const Option a = option_params(rand[o], steps);
+        float ca[kNodesPerLane];
+        leaves(a, steps, lane, ca);
 #pragma unroll
-      for (int k = 0; k < kNodesPerLane; ++k) c[k] = make_float2(ca[k], cb[k]);
-      const float2 v = lattice(c, steps, make_float2(a.pu, b.pu), lane);
+        for (int k = 0; k < kNodesPerLane; ++k) c[k].x = ca[k];
+        r.x = a.r;
+        s32.x = a.s32;
+        tail_a = a.tail;
+      }
+      {
+        const Option b = option_params(has_b ? rand[o + 1] : rand[o], steps);
+        float cb[kNodesPerLane];
+        leaves(b, steps, lane, cb);
+#pragma unroll
+        for (int k = 0; k < kNodesPerLane; ++k) c[k].y = cb[k];
+        r.y = b.r;
+        s32.y = b.s32;
+        tail_b = b.tail;
+      }
+      const float2 v = lattice(c, steps, r, s32, lane);
       if (lane == 0) {
-        out[o] = static_cast<float>(static_cast<double>(v.x) * exp(-0.02 * a.T));
-        if (has_b) out[o + 1] = static_cast<float>(static_cast<double>(v.y) * exp(-0.02 * b.T));
+        out[o] = static_cast<float>(static_cast<double>(v.x) * tail_a);
+        if (has_b) out[o + 1] = static_cast<float>(static_cast<double>(v.y) * tail_b);
       }
     }
   }
