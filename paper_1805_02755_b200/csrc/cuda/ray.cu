@@ -56,6 +56,37 @@ __device__ __forceinline__ float ray_sphere(V3 o, V3 d, float4 s) {
   return t > 1e-3f ? t : -1.0f;
 }
 
+// The same test for spheres s and s+1 at once: the arithmetic up to the
+// discriminant runs on packed pairs (FADD2/FMUL2 round each component like
+// the scalar _rn ops, in the same order), over structure-of-arrays sphere
+// data (x, y, z, r*r) in shared memory.  The sqrt / root selection stays
+// scalar per sphere.
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+// Packed product that ptxas cannot fuse into a following FADD2: it contracts
+// mul.rn.f32x2 + add.rn.f32x2 into FFMA2 (even with -fmad=false), which would
+// break parity.  x*y + (+0) rounds exactly like x*y except that a -0 product
+// becomes +0; only b's sign of zero can change, and b enters the results only
+// as b*b and as -b +/- sqrt(disc), where that sign is absorbed (see test).
+__device__ __forceinline__ float2 pmul(float2 a, float2 b) { return __ffma2_rn(a, b, make_float2(0.0f, 0.0f)); }
+__device__ __forceinline__ float root_of(float b, float disc) {
+  if (disc < 0.0f) return -1.0f;
+  const float sq = __fsqrt_rn(disc);
+  float t = sub(-b, sq);
+  if (t > 1e-3f) return t;
+  t = add(-b, sq);
+  return t > 1e-3f ? t : -1.0f;
+}
+__device__ __forceinline__ float2 ray_sphere2(V3 o, V3 d, float2 X, float2 Y, float2 Z, float2 RR) {
+  const float2 ox = __fadd2_rn(make_float2(o.x, o.x), neg2(X));
+  const float2 oy = __fadd2_rn(make_float2(o.y, o.y), neg2(Y));
+  const float2 oz = __fadd2_rn(make_float2(o.z, o.z), neg2(Z));
+  const float2 b = __fadd2_rn(__fadd2_rn(pmul(ox, make_float2(d.x, d.x)), pmul(oy, make_float2(d.y, d.y))),
+                              pmul(oz, make_float2(d.z, d.z)));
+  const float2 cc = __fadd2_rn(__fadd2_rn(__fadd2_rn(pmul(ox, ox), pmul(oy, oy)), pmul(oz, oz)), neg2(RR));
+  const float2 disc = __fadd2_rn(pmul(b, b), neg2(cc));
+  return make_float2(root_of(b.x, disc.x), root_of(b.y, disc.y));
+}
+
 struct Lane {
   V3 o, d;
   float r, g, b, weight;
@@ -66,10 +97,19 @@ __global__ void __launch_bounds__(kThreads)
     ray_persistent(const float4* __restrict__ scene, uint32_t ns, uint32_t w, uint32_t h, uint32_t max_depth,
                    float4* __restrict__ out, uint64_t first, uint64_t count, unsigned* __restrict__ ctrl) {
   __shared__ float4 sph[kMaxSpheres], mat[kMaxSpheres];
+  __shared__ __align__(8) float sx[kMaxSpheres], sy[kMaxSpheres], sz[kMaxSpheres], srr[kMaxSpheres];
   for (uint32_t i = threadIdx.x; i < ns; i += kThreads) {
-    sph[i] = scene[i];
+    const float4 c = scene[i];
+    sph[i] = c;
     mat[i] = scene[ns + i];
+    sx[i] = c.x;
+    sy[i] = c.y;
+    sz[i] = c.z;
+    srr[i] = mul(c.w, c.w);
   }
+  // sphere pairs [0, pairs_end) go through ray_sphere2, an odd last one alone
+  const uint32_t pairs_end = ns & ~1u;
+
   const float4* cam4 = scene + 2 * ns;
   const float4 cam = cam4[0];
   const float4 lights[3] = {cam4[1], cam4[2], cam4[3]};
@@ -132,11 +172,24 @@ __global__ void __launch_bounds__(kThreads)
       // ---- one bounce (oracle: trace_pixel loop body) ----
       float tmin = 1e30f;
       int hit = -1;
-      for (uint32_t s = 0; s < ns; ++s) {
-        const float t = ray_sphere(L.o, L.d, sph[s]);
+      for (uint32_t s = 0; s < pairs_end; s += 2) {
+        const float2 t = ray_sphere2(L.o, L.d, *reinterpret_cast<const float2*>(sx + s),
+                                     *reinterpret_cast<const float2*>(sy + s), *reinterpret_cast<const float2*>(sz + s),
+                                     *reinterpret_cast<const float2*>(srr + s));
+        if (t.x > 0.0f && t.x < tmin) {
+          tmin = t.x;
+          hit = static_cast<int>(s);
+        }
+        if (t.y > 0.0f && t.y < tmin) {
+          tmin = t.y;
+          hit = static_cast<int>(s + 1);
+        }
+      }
+      if (pairs_end < ns) {
+        const float t = ray_sphere(L.o, L.d, sph[pairs_end]);
         if (t > 0.0f && t < tmin) {
           tmin = t;
-          hit = static_cast<int>(s);
+          hit = static_cast<int>(pairs_end);
         }
       }
       if (L.d.y < 0.0f) {
@@ -180,8 +233,15 @@ __global__ void __launch_bounds__(kThreads)
           const float ndl = vdot(n, ln);
           if (ndl <= 0.0f) continue;
           bool shadow = false;
-          for (uint32_t s = 0; s < ns && !shadow; ++s) {
-            const float t = ray_sphere(p, ln, sph[s]);
+          for (uint32_t s = 0; s < pairs_end && !shadow; s += 2) {
+            const float2 t = ray_sphere2(p, ln, *reinterpret_cast<const float2*>(sx + s),
+                                         *reinterpret_cast<const float2*>(sy + s),
+                                         *reinterpret_cast<const float2*>(sz + s),
+                                         *reinterpret_cast<const float2*>(srr + s));
+            shadow = (t.x > 0.0f && t.x < dist) || (t.y > 0.0f && t.y < dist);
+          }
+          if (!shadow && pairs_end < ns) {
+            const float t = ray_sphere(p, ln, sph[pairs_end]);
             shadow = t > 0.0f && t < dist;
           }
           if (shadow) continue;
