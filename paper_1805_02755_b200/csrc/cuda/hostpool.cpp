@@ -145,6 +145,7 @@ void widen_async(int device, cudaEvent_t ready, const uint32_t* src, uint32_t* d
 }
 
 bool widen_wait(WidenTicket* ticket) {
+  if (ticket->pending.load() == 0) return !ticket->failed.load();  // idle ticket: no lock
   std::unique_lock lock(ticket->m);
   ticket->cv.wait(lock, [&] { return ticket->pending.load() == 0; });
   return !ticket->failed.load();

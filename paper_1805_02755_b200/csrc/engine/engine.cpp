@@ -296,9 +296,12 @@ struct Engine::Impl {
       std::lock_guard lock(rs.completion);
       rs.completed.push_back(std::move(pkg));
     }
-    // Outputs complete in host memory: pending copies and widening drained.
-    if (const int rc = ecl_gpu_sync(dev.gpu); rc != ECL_OK)
-      fail(rs, Error(code_of_status(rc), std::string("device '") + profile.id + "': " + ecl_last_error()));
+    // Outputs complete in host memory: pending copies and widening drained
+    // (device-resident runs have nothing in flight once the kernels ended).
+    if (host_out) {
+      if (const int rc = ecl_gpu_sync(dev.gpu); rc != ECL_OK)
+        fail(rs, Error(code_of_status(rc), std::string("device '") + profile.id + "': " + ecl_last_error()));
+    }
   }
 
   ExecutionTrace run_wall(std::span<const void* const> inputs, std::span<void* const> outputs) {
