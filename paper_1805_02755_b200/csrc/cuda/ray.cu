@@ -26,6 +26,10 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = 128;  // Table 2: lws 128
 constexpr uint64_t kChunk = 32;
 constexpr int kMaxSpheres = 256;
+#ifndef ECL_RAY_MIN_BLOCKS
+#define ECL_RAY_MIN_BLOCKS 8
+#endif
+constexpr int kMinBlocks = ECL_RAY_MIN_BLOCKS;  // 128 threads x 8 CTAs: 64 registers, half occupancy
 
 struct V3 {
   float x, y, z;
@@ -93,7 +97,7 @@ struct Lane {
   uint32_t depth, bounces;
 };
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
     ray_persistent(const float4* __restrict__ scene, uint32_t ns, uint32_t w, uint32_t h, uint32_t max_depth,
                    float4* __restrict__ out, uint64_t first, uint64_t count, unsigned* __restrict__ ctrl) {
   __shared__ float4 sph[kMaxSpheres], mat[kMaxSpheres];
