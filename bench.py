@@ -380,6 +380,32 @@ def merge_clocks(*cs):
 # ---------------------------------------------------------------------------
 # arms
 
+NCU_KERNEL = {"mandelbrot": "mandel_persistent<double", "mandelbrot_f32": "mandel_persistent<float",
+              "gaussian": "gaussian_tiled", "binomial": "binomial_warp", "nbody": "nbody_step",
+              "ray": "ray_persistent"}
+
+
+def ncu_traffic(workload):
+    """DRAM bytes (read + write) of the workload's kernel from the committed
+    ncu --set full capture of one launch (profiles/r1/ncu_summary.json)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1", "ncu_summary.json")
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    try:
+        rows = json.load(open(path))
+    except (OSError, ValueError):
+        return None, "no ncu capture committed"
+    for r in rows:
+        if NCU_KERNEL.get(workload, "?") in r.get("kernel", ""):
+            def val(k):
+                v, u = r[k].split()
+                return float(v) * scale[u]
+            t = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
+            return t, (f"dram__bytes_read.sum + dram__bytes_write.sum of one captured launch "
+                       f"({r['gpu__time_duration.sum']}) of {NCU_KERNEL[workload]}, bytes per launch "
+                       f"(profiles/r1/ncu_summary.json; compute-bound: the bytes are the launch's outputs)")
+    return None, "kernel not in the committed ncu capture"
+
+
 def init_dist():
     return env_int("WORLD_SIZE", 1), env_int("RANK", 0), env_int("LOCAL_RANK", 0)
 
@@ -622,6 +648,7 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
             cpu = {"value": None, "unit": "work-items/s", "cores": cpu_threads(), "kind": "reference",
                    "sample": f"unavailable: {exc}"}
 
+    traffic, traffic_basis = ncu_traffic(wl.name)
     units = wl.units()
     line = {
         "metric": METRIC, "value": units / (ms_dev * 1e-3), "unit": "work-items/s", "n_gpus": n,
@@ -637,7 +664,7 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
         "e2e": {"value": units / (ms_e2e * 1e-3), "unit": "work-items/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
         "roofline": {"bound": wl.bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_basis": traffic_basis,
                      "algorithmic_flops_per_step": wl.flops(),
                      "achieved_basis": "algorithmic flops per step / device-resident step time (packages overlap "
                                        "on two compute lanes, so summed launch time double-counts)",
