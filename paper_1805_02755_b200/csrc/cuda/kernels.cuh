@@ -16,7 +16,7 @@
 
 namespace ecl {
 
-enum class KernelKind { VecScale, Mandelbrot, MandelbrotF32, Synthetic, Gaussian, NBody, Binomial, Ray };
+enum class KernelKind { VecScale, Mandelbrot, MandelbrotF32, Synthetic, Gaussian, NBody, Binomial, Ray, Fault };
 
 enum class SyntheticProfile { Constant = 0, Ramp = 1, Step = 2 };
 
@@ -62,6 +62,7 @@ struct KernelSpec {
   double a = 0.0, b = 0.0;  // vecscale
   double synth_param = 1.0;
   bool synth_has_param = false;
+  uint64_t fault_item = 0;  // "fault" test kernel: the work-item that traps
   GaussianParams gauss;
   NBodyParams nbody;
   BinomialParams binom;
@@ -103,6 +104,9 @@ cudaError_t launch_binomial(const KernelSpec& spec, const LaunchEnv& env, uint64
 cudaError_t launch_ray(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
 
 // Exactly-once tally: tally[i] += 1 for i in [first, first + count).
+// Test hook (ECL_FAULT_INJECTION=1 only): the work-item `fault_item` executes
+// a trap, so the device faults mid-run (reference test_engine.cpp:236-254).
+cudaError_t launch_fault(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
 cudaError_t launch_tally(uint32_t* tally, uint64_t first, uint64_t count, cudaStream_t stream);
 
 }  // namespace ecl

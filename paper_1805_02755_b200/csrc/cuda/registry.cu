@@ -5,6 +5,8 @@
 // the paper's other benchmarks (Table 2).
 #include <cstring>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace ecl {
@@ -69,6 +71,8 @@ int resolve_kernel(KernelSpec& s, std::string* err) {
     s.kind = KernelKind::Binomial;
   } else if (id == "ray") {
     s.kind = KernelKind::Ray;
+  } else if (id == "fault" && std::getenv("ECL_FAULT_INJECTION") && std::string(std::getenv("ECL_FAULT_INJECTION")) == "1") {
+    s.kind = KernelKind::Fault;  // test hook only, see kernels.cuh
   } else {
     *err = "no kernel registered as '" + id + "'";
     return ECL_UNKNOWN_KERNEL;
@@ -162,6 +166,12 @@ int resolve_kernel(KernelSpec& s, std::string* err) {
       s.binom = BinomialParams{static_cast<uint32_t>(steps), groups * 4};
       return ECL_OK;
     }
+    case KernelKind::Fault:
+      // args [item]; one double output, 1:1 (the synthetic kernels' shape).
+      if (!s.inputs.empty() || s.outputs.size() != 1 || s.outputs[0].element_size_bytes != 8 || !one_to_one(s))
+        return bad(err, "fault expects no inputs and one double output, 1:1");
+      if (!arg_u64(s, 0, &s.fault_item, err)) return ECL_BAD_KERNEL_ARGS;
+      return ECL_OK;
     case KernelKind::Ray: {
       // args [W, H, spheres, max_depth]; in: scene float4 buffer; out: float4 RGBA per pixel.
       uint64_t w, h, ns, depth;
@@ -209,6 +219,7 @@ cudaError_t launch_kernel(const KernelSpec& spec, const LaunchEnv& env, uint64_t
     case KernelKind::NBody: return launch_nbody(spec, env, first, count);
     case KernelKind::Binomial: return launch_binomial(spec, env, first, count);
     case KernelKind::Ray: return launch_ray(spec, env, first, count);
+    case KernelKind::Fault: return launch_fault(spec, env, first, count);
   }
   return cudaErrorInvalidValue;
 }

@@ -8,6 +8,8 @@
 // (synthetic).  Each thread handles two consecutive items so the 8-byte
 // elements move as 16-byte vectors; the grid is sized to a whole number of
 // waves (SMs x resident blocks) and strides over the package.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace ecl {
@@ -90,6 +92,24 @@ cudaError_t launch_synthetic(const KernelSpec& spec, const LaunchEnv& env, uint6
   synthetic_kernel<<<stride_grid(env, count), kThreads, 0, env.stream>>>(
       static_cast<double*>(env.out[0]), static_cast<int>(spec.profile), spec.gws, spec.synth_param,
       spec.synth_has_param, first, count);
+  return cudaGetLastError();
+}
+
+namespace {
+__global__ void fault_kernel(double* __restrict__ out, uint64_t first, uint64_t count, uint64_t trap_item) {
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < count;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (first + k == trap_item) __trap();
+    out[first + k] = 0.0;
+  }
+}
+}  // namespace
+
+cudaError_t launch_fault(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
+  if (count == 0) return cudaSuccess;
+  const uint64_t blocks = std::min<uint64_t>((count + 255) / 256, static_cast<uint64_t>(env.sms) * 8);
+  fault_kernel<<<static_cast<unsigned>(blocks), 256, 0, env.stream>>>(static_cast<double*>(env.out[0]), first, count,
+                                                                     spec.fault_item);
   return cudaGetLastError();
 }
 

@@ -210,3 +210,42 @@ def test_repeated_runs_reuse_engine(gpu_available, oracle):
             r = e.run([])
             assert np.array_equal(r.outputs[0].view(np.uint32), exp)
             assert P.tiles_exactly(r.trace.packages, prog.total_work_groups())
+
+
+_FAULT_SCRIPT = """
+import paper_1805_02755_b200 as P
+spec = P.ProgramSpec(1 << 16, 256, out_buffers=[P.BufferDesc("out", 8, 1 << 16)], kernel="fault", args=[40000])
+prog = P.validate_program(spec)
+devs = [P.cuda_device("gpu0", 0)]
+try:
+    with P.Engine(P.EngineConfig(devs, P.DynamicConfig(8)), prog) as e:
+        e.run()
+    print("NO-ERROR")
+except P.EngineFailure as f:
+    print("FAILURE", [x.code.name for x in f.errors])
+except P.Error as x:
+    print("ERROR", x.code.name)
+"""
+
+
+def test_device_fault_becomes_kernel_panic(gpu_available):
+    # reference test_engine.cpp:236-254 (a throwing kernel -> KernelPanic):
+    # a work-item traps on the device; the run must fail with KernelPanic
+    # instead of hanging on the faulted context.  Subprocess: a device trap
+    # poisons the CUDA context for the rest of its process.
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, ECL_FAULT_INJECTION="1")
+    r = subprocess.run([sys.executable, "-c", _FAULT_SCRIPT], env=env, capture_output=True, text=True, timeout=120)
+    out = r.stdout + r.stderr
+    assert "FAILURE" in r.stdout or "ERROR" in r.stdout, out
+    assert "KernelPanic" in r.stdout, out
+
+
+def test_fault_kernel_is_not_registered_by_default(gpu_available):
+    spec = P.ProgramSpec(1 << 10, 256, out_buffers=[P.BufferDesc("out", 8, 1 << 10)], kernel="fault", args=[1])
+    with pytest.raises(P.Error) as e:
+        with P.Engine(P.EngineConfig([P.cuda_device("gpu0", 0)], P.StaticConfig()), P.validate_program(spec)) as eng:
+            eng.run()
+    assert e.value.code == P.ErrorCode.UnknownKernel

@@ -142,3 +142,36 @@ def test_wall_clock_b200_experiment(tmp_path, gpu_available):
         assert P.tiles_exactly(t.packages, t.raw["program"]["total_work_groups"])
     pgm = sorted(glob.glob(str(tmp_path / "out" / "*.pgm")))
     assert pgm and open(pgm[0], "rb").read(2) == b"P5"
+
+
+def test_summary_recomputes_from_median_trace_and_reruns_are_identical(tmp_path):
+    # reference test_harness.cpp:182-218: byte-identical virtual reruns, and
+    # the summary's metrics are make_report(median trace, solo times)
+    cfg = os.path.join(GOLD, "vecscale-batel", "experiment.json")
+    a = P.run_experiment(cfg, out_dir=str(tmp_path / "a"))
+    b = P.run_experiment(cfg, out_dir=str(tmp_path / "b"))
+    for f in sorted(os.listdir(tmp_path / "a")):
+        assert open(tmp_path / "a" / f, "rb").read() == open(tmp_path / "b" / f, "rb").read(), f
+    solo = [a["solo_ms"][k] for k in sorted(a["solo_ms"])]
+    for o in a["outcomes"]:
+        assert len(o["t_totals_ms"]) == a["repetitions"] - a["warmup_discard"]
+        t = P.ExecutionTrace(json.load(open(tmp_path / "a" / o["median_trace"])))
+        r, m = P.make_report(t, solo), o["metrics"]
+        assert (r.balance, r.speedup, r.s_max, r.efficiency, r.work_share, r.notes) == \
+            (m["balance"], m["speedup"], m["s_max"], m["efficiency"], m["work_share"], m["notes"])
+
+
+@pytest.mark.gpu
+def test_acceptance_balance_and_efficiency_criteria(tmp_path, gpu_available):
+    # reference acceptance.cpp criteria 3-4 on the reference's own experiment
+    # files, through this harness (costs from the B200 kernel):
+    # HGuided balance >= 0.95, image-order static <= 0.80,
+    # HGuided efficiency >= 0.85 (batel-like) and >= 0.78 (remo-like)
+    batel = P.run_experiment(os.path.join(GOLD, "mandelbrot-batel", "experiment.json"), out_dir=str(tmp_path / "b"))
+    remo = P.run_experiment(os.path.join(GOLD, "mandelbrot-remo", "experiment.json"), out_dir=str(tmp_path / "r"))
+    by = {o["name"]: o["metrics"] for o in batel["outcomes"]}
+    assert by["s4-hguided"]["balance"] >= 0.95
+    assert by["s0-static"]["balance"] <= 0.80
+    assert by["s4-hguided"]["efficiency"] >= 0.85
+    hg = [o["metrics"] for o in remo["outcomes"] if o["name"].endswith("hguided")][0]
+    assert hg["efficiency"] >= 0.78
