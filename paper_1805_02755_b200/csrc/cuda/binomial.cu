@@ -81,38 +81,46 @@ __device__ __forceinline__ void repack(const V (&c)[NL], V (&h)[NL / 2], unsigne
   }
 }
 
-// Per-option CRR parameters in FP64: S, K, T from the
-// uniform r, dt = T/steps, u = exp(sigma sqrt(dt)), pu = (a - d)/(u - d).
+// x^e for a warp-uniform e >= 0 (square and multiply).
+__device__ __forceinline__ double upow(double x, int e) {
+  double p = 1.0;
+  for (; e > 0; e >>= 1, x *= x)
+    if (e & 1) p *= x;
+  return p;
+}
+
+// Per-option quantities in FP64 (CRR parameters: S, K, T
+// from the uniform r, dt = T/steps, u = exp(sigma sqrt(dt)),
+// pu = (a - d)/(u - d)), reduced to what the leaves and the lattice need.
 struct Option {
-  double S, K, T, vsdt, u;
-  float r, s32;  // pu/pd and pd^32 (the scaled lattice's step and rescale factors)
-  double tail;   // pd^(steps - 32*rescales) * exp(-R T): undoes the remaining scale, discounts
+  double K, base, f16, u2;  // leaf of node t = 16 l + k: base * f16^l * u2^k - K
+  float r, s32;             // pu/pd and pd^32 (the scaled lattice's step and rescale factors)
+  double tail;              // pd^(steps - 32 R) * exp(-R T) / q^R: undoes the remaining scale, discounts
 };
 
-__device__ __forceinline__ Option option_params(double r, int steps) {
+__device__ __forceinline__ Option option_params(double rv, int steps) {
   Option o;
-  o.S = 5.0 * (1.0 - r) + 30.0 * r;
-  o.K = 1.0 * (1.0 - r) + 100.0 * r;
-  o.T = 0.25 * (1.0 - r) + 10.0 * r;
-  const double dt = o.T / steps;
-  o.vsdt = 0.30 * sqrt(dt);
+  const double S = 5.0 * (1.0 - rv) + 30.0 * rv;
+  o.K = 1.0 * (1.0 - rv) + 100.0 * rv;
+  const double T = 0.25 * (1.0 - rv) + 10.0 * rv;
+  const double dt = T / steps;
+  const double vsdt = 0.30 * sqrt(dt);
   const double a = exp(0.02 * dt);
-  o.u = exp(o.vsdt);
-  const double d = 1.0 / o.u;
-  const double pu = (a - d) / (o.u - d), pd = 1.0 - pu;
+  const double u = exp(vsdt);
+  const double d = 1.0 / u;
+  const double pu = (a - d) / (u - d), pd = 1.0 - pu;
   o.r = static_cast<float>(pu / pd);
-  double p32 = pd;
-#pragma unroll
-  for (int i = 0; i < 5; ++i) p32 *= p32;  // pd^32
+  const double p32 = upow(pd, 32);
   o.s32 = static_cast<float>(p32);
-  // Undo the scale left after the last rescale (pd^e, e = steps - 32 R) and
-  // the f32 rounding of the R rescale factors, then discount exp(-R T).
+  // R rescales by the f32-rounded pd^32; q is that rounding's factor.
   const int rescales = (steps - 1) / 32;
   const double q = static_cast<double>(o.s32) / p32;
-  double tail = exp(-0.02 * o.T);
-  for (int i = 0; i < steps - 32 * rescales; ++i) tail *= pd;
-  for (int i = 0; i < rescales; ++i) tail /= q;
-  o.tail = tail;
+  o.tail = upow(pd, steps - 32 * rescales) * exp(-0.02 * T) / upow(q, rescales);
+  // S*exp(vsdt*(2t - steps)) = S*exp(-vsdt*steps) * (u^16)^l * (u^2)^k:
+  // one exp per option instead of one per lane.
+  o.base = S * exp(-vsdt * static_cast<double>(steps));
+  o.u2 = u * u;
+  o.f16 = upow(o.u2, 8);
   return o;
 }
 
@@ -120,19 +128,36 @@ __device__ __forceinline__ Option option_params(double r, int steps) {
 // factored out (applied once as exp(-R T) at the end, so rounding it to f32
 // does not compound 254 times) and the lattice is carried scaled by
 // pd^-m: pd*c + pu*c1 becomes one FMA w + (pu/pd)*w1, rescaled by pd^32 at
-// every level that is a multiple of 32; `tail` undoes the rest.  Leaves
-// S*exp(vsdt*(2t - steps)) for the lane's 8 nodes: one exp per lane, then
-// successive factors u^2 (FP64, ~1e-16 relative drift).
+// every level that is a multiple of 32; `tail` undoes the rest.  The lane's
+// first leaf price is base * f16^lane (lane-divergent square-and-multiply
+// with selects), then successive factors u^2 (~1e-15 relative drift).
 __device__ __forceinline__ void leaves(const Option& o, int steps, unsigned lane, float (&c)[kNodesPerLane]) {
-  double st = o.S * exp(o.vsdt * static_cast<double>(2 * static_cast<int>(lane) * kNodesPerLane - steps));
-  const double u2 = o.u * o.u;
+  double st = o.base, f = o.f16;
+#pragma unroll
+  for (int bit = 0; bit < 5; ++bit, f *= f) {
+    const double m = st * f;
+    st = ((lane >> bit) & 1u) ? m : st;
+  }
 #pragma unroll
   for (int k = 0; k < kNodesPerLane; ++k) {
     const int t = static_cast<int>(lane) * kNodesPerLane + k;
     const double leaf = st - o.K;
     c[k] = (t <= steps && leaf > 0.0) ? static_cast<float>(leaf) : 0.0f;
-    st *= u2;
+    st *= o.u2;
   }
+}
+
+// Broadcast of an Option computed on lane `src` to the whole warp.
+__device__ __forceinline__ Option shfl_option(const Option& x, int src) {
+  Option o;
+  o.K = __shfl_sync(0xffffffffu, x.K, src);
+  o.base = __shfl_sync(0xffffffffu, x.base, src);
+  o.f16 = __shfl_sync(0xffffffffu, x.f16, src);
+  o.u2 = __shfl_sync(0xffffffffu, x.u2, src);
+  o.r = __shfl_sync(0xffffffffu, x.r, src);
+  o.s32 = __shfl_sync(0xffffffffu, x.s32, src);
+  o.tail = __shfl_sync(0xffffffffu, x.tail, src);
+  return o;
 }
 
 // The live part of the lattice shrinks by one node per step: once it fits
@@ -175,8 +200,11 @@ __global__ void __launch_bounds__(kThreads, 4)
       const bool has_b = w * P + 1 < n_opt;
       float2 c[kNodesPerLane], r, s32;
       double tail_a, tail_b;
-      {  // one option's FP64 setup at a time (register pressure)
-        const Option a = option_params(rand[o], steps);
+      // Lanes 0-15 set up option A, lanes 16-31 option B (one pass of the
+      // FP64 setup for both), then each half's result is broadcast.
+      const Option mine = option_params(rand[o + ((lane >> 4) != 0u && has_b ? 1 : 0)], steps);
+      {
+        const Option a = shfl_option(mine, 0);
         float ca[kNodesPerLane];
         leaves(a, steps, lane, ca);
 #pragma unroll
@@ -186,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 4)
         tail_a = a.tail;
       }
       {
-        const Option b = option_params(has_b ? rand[o + 1] : rand[o], steps);
+        const Option b = shfl_option(mine, 16);
         float cb[kNodesPerLane];
         leaves(b, steps, lane, cb);
 #pragma unroll
