@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -50,34 +51,47 @@ __device__ __forceinline__ float2 shfl_from(float2 v, unsigned src) {
 
 // Backward steps j, j-1, ... while j > stop, with NL nodes per lane (lane l
 // holds nodes NL*l .. NL*l+NL-1): w[t] <- w[t] + r*w[t+1].  The neighbour of
-// a lane's last node is the next lane's first (one shuffle).  Whenever the
-// level reaches a multiple of 32 the lattice is rescaled by pd^32, so w stays
-// within ~pd^-32 of the true value (no f32 overflow).  Returns the next j.
-// After it, only nodes t < stop are live.
+// a lane's last node is the next lane's first (one shuffle).  Returns the
+// next j.
 template <int NL, typename V>
-__device__ __forceinline__ int backward(V (&c)[NL], int j, int stop, V r, V s32) {
+__device__ __forceinline__ int backward(V (&c)[NL], int j, int stop, V r) {
   for (; j > stop; --j) {
     const V right = shfl_down1(c[0]);
 #pragma unroll
     for (int k = 0; k < NL - 1; ++k) c[k] = lattice_step(c[k], c[k + 1], r);
     c[NL - 1] = lattice_step(c[NL - 1], right, r);
-    if (((j - 1) & 31) == 0 && j > 1) {
-#pragma unroll
-      for (int k = 0; k < NL; ++k) c[k] = rescale(c[k], s32);
-    }
   }
   return j;
 }
 
-// NL -> NL/2 nodes per lane: lane l's new nodes (NL/2)*l + k live in lane
-// l/2 at register (l%2)*NL/2 + k.
+// The live lattice (nodes 0..j at level j) shrinks by one node per step, so
+// the levels run in phases of 32: phase NL keeps NL nodes per lane until the
+// live nodes fit in 32*(NL-1), then the lattice is rescaled by pd^32 (w stays
+// within pd^-32 of the true value: no f32 overflow) and repacked to NL-1
+// nodes per lane through a warp-private shared-memory buffer.  Phases above
+// ceil((steps+1)/32) run no steps and neither rescale nor repack anything
+// that matters.  Slots beyond the live nodes carry don't-care values.
 template <int NL, typename V>
-__device__ __forceinline__ void repack(const V (&c)[NL], V (&h)[NL / 2], unsigned lane) {
+__device__ __forceinline__ V phases(V (&c)[NL], int j, V r, V s32, V* buf, unsigned lane) {
+  const int stop = NL > 1 ? 32 * (NL - 1) - 1 : 0;
+  if (j > stop) {
+    j = backward<NL>(c, j, stop, r);
+    if constexpr (NL > 1) {
 #pragma unroll
-  for (int k = 0; k < NL / 2; ++k) {
-    const V lo = shfl_from(c[k], lane >> 1);
-    const V hi = shfl_from(c[NL / 2 + k], lane >> 1);
-    h[k] = (lane & 1u) ? hi : lo;
+      for (int k = 0; k < NL; ++k) c[k] = rescale(c[k], s32);
+    }
+  }
+  if constexpr (NL == 1) {
+    return c[0];
+  } else {
+#pragma unroll
+    for (int k = 0; k < NL; ++k) buf[NL * lane + k] = c[k];
+    __syncwarp();
+    V h[NL - 1];
+#pragma unroll
+    for (int k = 0; k < NL - 1; ++k) h[k] = buf[(NL - 1) * lane + k];
+    __syncwarp();
+    return phases<NL - 1>(h, j, r, s32, buf, lane);
   }
 }
 
@@ -113,7 +127,7 @@ __device__ __forceinline__ Option option_params(double rv, int steps) {
   const double p32 = upow(pd, 32);
   o.s32 = static_cast<float>(p32);
   // R rescales by the f32-rounded pd^32; q is that rounding's factor.
-  const int rescales = (steps - 1) / 32;
+  const int rescales = steps / 32;  // = ceil((steps + 1) / 32) - 1 phase boundaries
   const double q = static_cast<double>(o.s32) / p32;
   o.tail = upow(pd, steps - 32 * rescales) * exp(-0.02 * T) / upow(q, rescales);
   // S*exp(vsdt*(2t - steps)) = S*exp(-vsdt*steps) * (u^16)^l * (u^2)^k:
@@ -160,23 +174,9 @@ __device__ __forceinline__ Option shfl_option(const Option& x, int src) {
   return o;
 }
 
-// The live part of the lattice shrinks by one node per step: once it fits
-// in 128 / 64 / 32 nodes the warp repacks to 4 / 2 / 1 nodes per lane (one
-// shuffle per register), so later steps cost proportionally less.
 template <typename V>
-__device__ __forceinline__ V lattice(V (&c)[kNodesPerLane], int steps, V r, V s32, unsigned lane) {
-  int j = steps;
-  j = backward<8>(c, j, 128, r, s32);
-  V c4[4];
-  repack<8>(c, c4, lane);
-  j = backward<4>(c4, j, 64, r, s32);
-  V c2[2];
-  repack<4>(c4, c2, lane);
-  j = backward<2>(c2, j, 32, r, s32);
-  V c1[1];
-  repack<2>(c2, c1, lane);
-  backward<1>(c1, j, 0, r, s32);
-  return c1[0];
+__device__ __forceinline__ V lattice(V (&c)[kNodesPerLane], int steps, V r, V s32, V* buf, unsigned lane) {
+  return phases<kNodesPerLane>(c, steps, r, s32, buf, lane);
 }
 
 // P = options per warp (1: scalar lattice, 2: two options packed per lane).
@@ -184,7 +184,10 @@ template <int P>
 __global__ void __launch_bounds__(kThreads, 4)
     binomial_warp(const float* __restrict__ rand, float* __restrict__ out, int steps, uint64_t first_opt,
                   uint64_t n_opt) {
+  using V = std::conditional_t<P == 2, float2, float>;
+  __shared__ V repack_buf[kThreads / 32][32 * kNodesPerLane];
   const unsigned lane = threadIdx.x & 31u;
+  V* const buf = repack_buf[threadIdx.x >> 5];
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (kThreads / 32);
   const uint64_t groups = (n_opt + P - 1) / P;
   for (uint64_t w = blockIdx.x * static_cast<uint64_t>(kThreads / 32) + (threadIdx.x >> 5); w < groups;
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 4)
       const Option a = option_params(rand[o], steps);
       float c[kNodesPerLane];
       leaves(a, steps, lane, c);
-      const float v = lattice(c, steps, a.r, a.s32, lane);
+      const float v = lattice(c, steps, a.r, a.s32, buf, lane);
       if (lane == 0) out[o] = static_cast<float>(static_cast<double>(v) * a.tail);
     } else {
       const bool has_b = w * P + 1 < n_opt;
@@ -223,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 4)
         s32.y = b.s32;
         tail_b = b.tail;
       }
-      const float2 v = lattice(c, steps, r, s32, lane);
+      const float2 v = lattice(c, steps, r, s32, buf, lane);
       if (lane == 0) {
         out[o] = static_cast<float>(static_cast<double>(v.x) * tail_a);
         if (has_b) out[o + 1] = static_cast<float>(static_cast<double>(v.y) * tail_b);
