@@ -180,8 +180,8 @@ __device__ __forceinline__ V lattice(V (&c)[kNodesPerLane], int steps, V r, V s3
 }
 
 // P = options per warp (1: scalar lattice, 2: two options packed per lane).
-template <int P>
-__global__ void __launch_bounds__(kThreads, 4)
+template <int P, int MB>
+__global__ void __launch_bounds__(kThreads, MB)
     binomial_warp(const float* __restrict__ rand, float* __restrict__ out, int steps, uint64_t first_opt,
                   uint64_t n_opt) {
   using V = std::conditional_t<P == 2, float2, float>;
@@ -235,14 +235,14 @@ __global__ void __launch_bounds__(kThreads, 4)
   }
 }
 
-template <int P>
+template <int P, int MB>
 cudaError_t launch(const KernelSpec& spec, const LaunchEnv& env, uint64_t first_opt, uint64_t n_opt) {
   const uint64_t warps_per_block = kThreads / 32;
   const uint64_t groups = (n_opt + P - 1) / P;
   uint64_t blocks = (groups + warps_per_block - 1) / warps_per_block;
   const uint64_t cap = static_cast<uint64_t>(env.sms) * 8 * 16;
   if (blocks > cap) blocks = cap;
-  binomial_warp<P><<<static_cast<unsigned>(blocks), kThreads, 0, env.stream>>>(
+  binomial_warp<P, MB><<<static_cast<unsigned>(blocks), kThreads, 0, env.stream>>>(
       static_cast<const float*>(env.in[0]), static_cast<float*>(env.out[0]), static_cast<int>(spec.binom.steps),
       first_opt, n_opt);
   return cudaGetLastError();
@@ -259,7 +259,16 @@ cudaError_t launch_binomial(const KernelSpec& spec, const LaunchEnv& env, uint64
     const char* v = std::getenv("ECL_BINOMIAL_VARIANT");
     return v ? std::atoi(v) : 0;
   }();
-  return variant == 1 ? launch<1>(spec, env, first_opt, n_opt) : launch<2>(spec, env, first_opt, n_opt);
+  static const int mb = [] {  // ECL_BINOMIAL_MB: resident CTAs per SM the registers are sized for
+    const char* v = std::getenv("ECL_BINOMIAL_MB");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (variant == 1) return launch<1, 4>(spec, env, first_opt, n_opt);
+  switch (mb) {  // measured: 4 (52 registers) 18.8 ms, 5 19.1 ms, 6 19.2 ms
+    case 5: return launch<2, 5>(spec, env, first_opt, n_opt);
+    case 6: return launch<2, 6>(spec, env, first_opt, n_opt);
+    default: return launch<2, 4>(spec, env, first_opt, n_opt);
+  }
 }
 
 }  // namespace ecl
