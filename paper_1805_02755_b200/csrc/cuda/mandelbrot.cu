@@ -239,6 +239,187 @@ __global__ void __launch_bounds__(kThreads, MB)
   }
 }
 
+// ---- FP32 variant, two pixels per lane ------------------------------------
+// The FP32 kernel above is issue-bound (6 FP32 + 1 integer instruction per
+// pixel-iteration, ncu: 94 % issue, 58 % FMA pipe).  Here every lane carries
+// two pixels ("slots" A and B) in float2 registers and iterates them with
+// packed FFMA2/FADD2: per pixel-iteration 3 FP32 + 1 integer instruction.
+// Parity: packed ops round each component like the scalar _rn ops.  Products
+// are formed as fma(x, y, +0) because ptxas contracts a packed multiply into
+// a following packed add (FFMA2) even with -fmad=false; x*y + 0 equals the
+// rounded product except that a -0 product becomes +0, and the only -0
+// product here (zx*zy) feeds 2t + cy with cy != -0 (a sum y0 + k*span never
+// rounds to -0), so the counts stay bit-identical to the FP32 restatement.
+__device__ __forceinline__ float2 pmul0(float2 a, float2 b) { return __ffma2_rn(a, b, make_float2(0.0f, 0.0f)); }
+
+struct Slot2 {
+  uint64_t idx = 0;
+  uint32_t n = 0;
+  bool valid = false, alive = false;
+};
+
+template <int R, int MB>
+__global__ void __launch_bounds__(kThreads, MB)
+    mandel_f32x2(const Viewport<float> vp, const float* __restrict__ tab, uint64_t first, uint64_t count,
+                 uint4* __restrict__ out, uint32_t* __restrict__ compact, unsigned* __restrict__ ctrl) {
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned below = (1u << lane) - 1u;
+  const uint64_t big = (count - count / 8) / kBigChunk;
+  const uint64_t tail_start = big * kBigChunk;
+  const uint64_t nclaims = big + (count - tail_start + kTailChunk - 1) / kTailChunk;
+  const float* __restrict__ cxs = tab;
+  const float* __restrict__ cys = tab + vp.width;
+
+  uint64_t next = 0, end = 0, px0 = 0, py0 = 0;
+  bool more = true;
+  auto claim = [&]() {
+    unsigned c = 0;
+    if (lane == 0) c = atomicAdd(ctrl, 1u);
+    c = __shfl_sync(kFull, c, 0);
+    if (c >= nclaims) {
+      more = false;
+      next = end = 0;
+      return;
+    }
+    next = c < big ? c * kBigChunk : tail_start + (c - big) * kTailChunk;
+    const uint64_t size = c < big ? kBigChunk : kTailChunk;
+    end = next + size < count ? next + size : count;
+    const uint64_t g = first + next;
+    py0 = g / vp.width;
+    px0 = g - py0 * vp.width;
+  };
+  claim();
+
+  Slot2 sa, sb;
+  float2 cx = make_float2(0.f, 0.f), cy = cx, zx = cx, zy = cx;
+  const uint32_t max_it = vp.max_iterations;
+  constexpr uint32_t kFour = 0x40800000u;  // 4.0f
+
+  // Gives pixel `rank` of the chunk's remaining range to a slot.
+  auto assign = [&](Slot2& s, float& scx, float& scy, float& szx, float& szy, unsigned rank) {
+    s.idx = first + next + rank;
+    uint64_t px = px0 + rank, py = py0;
+    while (px >= vp.width) {
+      px -= vp.width;
+      ++py;
+    }
+    scx = cxs[px];
+    scy = cys[py];
+    szx = 0.f;
+    szy = 0.f;
+    s.n = 0;
+    s.valid = true;
+    s.alive = true;
+  };
+
+  for (;;) {
+    // Refill idle slots: the 64 slots of the warp in order A0..A31, B0..B31.
+    unsigned need_a = __ballot_sync(kFull, !sa.valid), need_b = __ballot_sync(kFull, !sb.valid);
+    while ((need_a | need_b) && more) {
+      const uint64_t avail = end - next;
+      const unsigned na = __popc(need_a);
+      const unsigned ra = __popc(need_a & below), rb = na + __popc(need_b & below);
+      if (!sa.valid && ra < avail) assign(sa, cx.x, cy.x, zx.x, zy.x, ra);
+      if (!sb.valid && rb < avail) assign(sb, cx.y, cy.y, zx.y, zy.y, rb);
+      const uint64_t want = na + __popc(need_b);
+      const uint64_t take = want < avail ? want : avail;
+      next += take;
+      px0 += take;
+      while (px0 >= vp.width) {
+        px0 -= vp.width;
+        ++py0;
+      }
+      if (next >= end) claim();
+      need_a = __ballot_sync(kFull, !sa.valid);
+      need_b = __ballot_sync(kFull, !sb.valid);
+    }
+    if (!__any_sync(kFull, sa.valid || sb.valid)) break;
+
+    // Speculative block on both slots (see mandel_persistent).
+    const float2 zx0 = zx, zy0 = zy;
+    const uint32_t na0 = sa.n, nb0 = sb.n;
+    uint32_t acc_a = 0, acc_b = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const float2 xx = pmul0(zx, zx);
+      const float2 yy = pmul0(zy, zy);
+      acc_a |= __float_as_uint(xx.x) | __float_as_uint(yy.x);
+      acc_b |= __float_as_uint(xx.y) | __float_as_uint(yy.y);
+      const float2 t = pmul0(zx, zy);
+      zy = __ffma2_rn(t, make_float2(2.0f, 2.0f), cy);
+      zx = __fadd2_rn(__fadd2_rn(xx, make_float2(-yy.x, -yy.y)), cx);
+    }
+    const bool fast_a = sa.alive && na0 + R <= max_it && (acc_a & 0x40000000u) == 0u;
+    const bool fast_b = sb.alive && nb0 + R <= max_it && (acc_b & 0x40000000u) == 0u;
+    if (fast_a) {
+      sa.n = na0 + R;
+      sa.alive = sa.n < max_it;
+    }
+    if (fast_b) {
+      sb.n = nb0 + R;
+      sb.alive = sb.n < max_it;
+    }
+    bool live_a = sa.alive && !fast_a, live_b = sb.alive && !fast_b;
+    if (__any_sync(kFull, live_a || live_b)) {
+      if (live_a) {
+        zx.x = zx0.x;
+        zy.x = zy0.x;
+        sa.n = na0;
+      }
+      if (live_b) {
+        zx.y = zx0.y;
+        zy.y = zy0.y;
+        sb.n = nb0;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const float2 xx = pmul0(zx, zx);
+        const float2 yy = pmul0(zy, zy);
+        const float2 s = __fadd2_rn(xx, yy);  // >= +0: integer order == FP order
+        live_a = live_a && __float_as_uint(s.x) <= kFour;
+        live_b = live_b && __float_as_uint(s.y) <= kFour;
+        const float2 t = pmul0(zx, zy);
+        const float2 nzy = __ffma2_rn(t, make_float2(2.0f, 2.0f), cy);
+        const float2 nzx = __fadd2_rn(__fadd2_rn(xx, make_float2(-yy.x, -yy.y)), cx);
+        if (live_a) {
+          zx.x = nzx.x;
+          zy.x = nzy.x;
+          sa.n += 1u;
+        }
+        if (live_b) {
+          zx.y = nzx.y;
+          zy.y = nzy.y;
+          sb.n += 1u;
+        }
+        live_a = live_a && sa.n < max_it;
+        live_b = live_b && sb.n < max_it;
+      }
+      if (sa.alive && !fast_a) sa.alive = live_a;
+      if (sb.alive && !fast_b) sb.alive = live_b;
+    }
+    if (sa.valid && !sa.alive) {
+      out[sa.idx] = make_uint4(sa.n, sa.n, sa.n, sa.n);
+      if (compact) compact[sa.idx] = sa.n;
+      sa.valid = false;
+    }
+    if (sb.valid && !sb.alive) {
+      out[sb.idx] = make_uint4(sb.n, sb.n, sb.n, sb.n);
+      if (compact) compact[sb.idx] = sb.n;
+      sb.valid = false;
+    }
+  }
+
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned done = atomicAdd(ctrl + 1, 1u);
+    if (done == gridDim.x - 1) {
+      atomicExch(ctrl, 0u);
+      atomicExch(ctrl + 1, 0u);
+    }
+  }
+}
+
 template <typename Real>
 Viewport<Real> make_viewport(const MandelParams& p) {
   Viewport<Real> vp;
@@ -280,6 +461,26 @@ cudaError_t launch_real(const MandelParams& p, const LaunchEnv& env, uint64_t fi
   return cudaGetLastError();
 }
 
+template <int R, int MB>
+cudaError_t launch_f32x2(const MandelParams& p, const LaunchEnv& env, uint64_t first, uint64_t count) {
+  static int blocks_per_sm = 0;
+  if (blocks_per_sm == 0) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, mandel_f32x2<R, MB>, kThreads, 0);
+    if (e != cudaSuccess) return e;
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  const Viewport<float> vp = make_viewport<float>(p);
+  const uint64_t claims = (count + kTailChunk - 1) / kTailChunk;
+  const uint64_t blocks_needed = (claims + kThreads / 32 - 1) / (kThreads / 32);
+  uint64_t grid = static_cast<uint64_t>(env.sms) * static_cast<uint64_t>(blocks_per_sm);
+  if (blocks_needed < grid) grid = blocks_needed;
+  if (grid == 0) return cudaSuccess;
+  mandel_f32x2<R, MB><<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
+      vp, static_cast<const float*>(env.scratch), first, count, static_cast<uint4*>(env.out[0]), env.compact,
+      env.ctrl);
+  return cudaGetLastError();
+}
+
 template <typename Real>
 cudaError_t tables(const MandelParams& p, const LaunchEnv& env) {
   const uint64_t n = p.width + p.height;
@@ -300,7 +501,22 @@ cudaError_t prepare_mandelbrot(const KernelSpec& spec, const LaunchEnv& env) {
 
 cudaError_t launch_mandelbrot(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
   if (count == 0) return cudaSuccess;
-  if (spec.kind == KernelKind::MandelbrotF32) return launch_real<float, 16>(spec.mandel, env, first, count);
+  if (spec.kind == KernelKind::MandelbrotF32) {
+    static const bool scalar = [] {  // ECL_MANDEL_F32_SCALAR=1: one pixel per lane
+      const char* v = std::getenv("ECL_MANDEL_F32_SCALAR");
+      return v && std::atoi(v) == 1;
+    }();
+    static const int mb = [] {  // ECL_MANDEL_F32_MB: resident CTAs per SM
+      const char* v = std::getenv("ECL_MANDEL_F32_MB");
+      return v ? std::atoi(v) : 0;
+    }();
+    if (scalar) return launch_real<float, 16>(spec.mandel, env, first, count);
+    switch (mb) {
+      case 4: return launch_f32x2<16, 4>(spec.mandel, env, first, count);
+      case 6: return launch_f32x2<16, 6>(spec.mandel, env, first, count);
+      default: return launch_f32x2<16, 5>(spec.mandel, env, first, count);
+    }
+  }
   // Tuning hook (ECL_MANDEL_VARIANT): block length R and resident CTAs per SM.
   static const int variant = [] {
     const char* v = std::getenv("ECL_MANDEL_VARIANT");
