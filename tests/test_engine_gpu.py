@@ -91,6 +91,20 @@ def test_mandelbrot_config_checksum(gpu_available, oracle):
     assert oracle.fnv1a64(counts) == 0xc19e9aef35d040ac
 
 
+def test_mandelbrot_f32_config_checksum(gpu_available):
+    """16384^2 x 2048 FP32 variant: the sum of counts of the FP32 restatement
+    measured in SURVEY.md §8c (96,141,248,575)."""
+    w, it = 16384, 2048
+    prog = P.validate_program(W.mandelbrot_spec(w, w, it, kernel="mandelbrot_f32"))
+    with P.Engine(P.EngineConfig(devices(1), P.HGuidedConfig()), prog) as e:
+        e.run_into([], None)
+        out = np.empty(w * w * 4, np.uint32)
+        e.gather([out])
+    counts = out.reshape(-1, 4)
+    assert (counts == counts[:, :1]).all()
+    assert int(counts[:, 0].sum(dtype=np.uint64)) == 96141248575
+
+
 def test_mandelbrot_f32_bit_exact(gpu_available, oracle):
     _, res = run_engine(W.mandelbrot_spec(1024, 1024, 2048, kernel="mandelbrot_f32"), P.HGuidedConfig(), n_dev=2)
     got = res.outputs[0].view(np.uint32)
