@@ -674,8 +674,14 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
                      "fp64_dfma_tflops": f64.value, "fp64_dadd_tinstr_s": add.value, "fp32_ffma_tflops": f32.value},
         "coexec": {"balance": bal, "packages_per_step": len(last.packages), "native_kernel_ms": k_native,
                    "engine_ms": ms_dev, "native_e2e_ms": t_native_e2e, "engine_e2e_ms": ms_e2e,
-                   "overhead_pct_device": (ms_dev - k_native) / k_native * 100.0 if k_native else None,
-                   "overhead_pct_e2e": (ms_e2e - t_native_e2e) / t_native_e2e * 100.0 if t_native_e2e else None,
+                   # speedup over one native single-kernel launch of the whole grid on one GPU, and the
+                   # paper's efficiency speedup / s_max with s_max = N identical devices
+                   "speedup_vs_native_1gpu": k_native / ms_dev if k_native else None,
+                   "efficiency": k_native / (n * ms_dev) if k_native else None,
+                   # runtime overhead of co-execution vs that native run (work-normalised: N * T_N vs T_1)
+                   "overhead_pct_device": (n * ms_dev - k_native) / k_native * 100.0 if k_native else None,
+                   "overhead_pct_e2e": (ms_e2e - t_native_e2e) / t_native_e2e * 100.0
+                   if t_native_e2e and n == 1 else None,
                    "kernel_ms_per_step": kernel_ms / args.steps, "outputs_sane": bool(sane),
                    "e2e_last_kernel_end_ms": e2e_last_kernel_end},
         "gpu_launches": launches,
