@@ -101,15 +101,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     ray_persistent(const float4* __restrict__ scene, uint32_t ns, uint32_t w, uint32_t h, uint32_t max_depth,
                    float4* __restrict__ out, uint64_t first, uint64_t count, unsigned* __restrict__ ctrl) {
   __shared__ float4 sph[kMaxSpheres], mat[kMaxSpheres];
-  __shared__ __align__(8) float sx[kMaxSpheres], sy[kMaxSpheres], sz[kMaxSpheres], srr[kMaxSpheres];
+  // Sphere pairs as two 16-byte records: (x0, x1, y0, y1), (z0, z1, r0^2, r1^2),
+  // so a pair test reads 2 LDS.128 off one pointer (packed operands aligned).
+  __shared__ float4 pair_rec[kMaxSpheres / 2][2];
   for (uint32_t i = threadIdx.x; i < ns; i += kThreads) {
     const float4 c = scene[i];
     sph[i] = c;
     mat[i] = scene[ns + i];
-    sx[i] = c.x;
-    sy[i] = c.y;
-    sz[i] = c.z;
-    srr[i] = mul(c.w, c.w);
+    float* rec = reinterpret_cast<float*>(pair_rec[i / 2]);
+    const uint32_t h = i & 1u;
+    rec[0 + h] = c.x;
+    rec[2 + h] = c.y;
+    rec[4 + h] = c.z;
+    rec[6 + h] = mul(c.w, c.w);
   }
   // sphere pairs [0, pairs_end) go through ray_sphere2, an odd last one alone
   const uint32_t pairs_end = ns & ~1u;
@@ -177,9 +181,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       float tmin = 1e30f;
       int hit = -1;
       for (uint32_t s = 0; s < pairs_end; s += 2) {
-        const float2 t = ray_sphere2(L.o, L.d, *reinterpret_cast<const float2*>(sx + s),
-                                     *reinterpret_cast<const float2*>(sy + s), *reinterpret_cast<const float2*>(sz + s),
-                                     *reinterpret_cast<const float2*>(srr + s));
+        const float4 r0 = pair_rec[s / 2][0], r1 = pair_rec[s / 2][1];
+        const float2 t = ray_sphere2(L.o, L.d, make_float2(r0.x, r0.y), make_float2(r0.z, r0.w),
+                                     make_float2(r1.x, r1.y), make_float2(r1.z, r1.w));
         if (t.x > 0.0f && t.x < tmin) {
           tmin = t.x;
           hit = static_cast<int>(s);
@@ -238,10 +242,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
           if (ndl <= 0.0f) continue;
           bool shadow = false;
           for (uint32_t s = 0; s < pairs_end && !shadow; s += 2) {
-            const float2 t = ray_sphere2(p, ln, *reinterpret_cast<const float2*>(sx + s),
-                                         *reinterpret_cast<const float2*>(sy + s),
-                                         *reinterpret_cast<const float2*>(sz + s),
-                                         *reinterpret_cast<const float2*>(srr + s));
+            const float4 r0 = pair_rec[s / 2][0], r1 = pair_rec[s / 2][1];
+            const float2 t = ray_sphere2(p, ln, make_float2(r0.x, r0.y), make_float2(r0.z, r0.w),
+                                         make_float2(r1.x, r1.y), make_float2(r1.z, r1.w));
             shadow = (t.x > 0.0f && t.x < dist) || (t.y > 0.0f && t.y < dist);
           }
           if (!shadow && pairs_end < ns) {
