@@ -17,6 +17,8 @@
 // deepest reflection.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace ecl {
@@ -26,10 +28,6 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = 128;  // Table 2: lws 128
 constexpr uint64_t kChunk = 32;
 constexpr int kMaxSpheres = 256;
-#ifndef ECL_RAY_MIN_BLOCKS
-#define ECL_RAY_MIN_BLOCKS 8
-#endif
-constexpr int kMinBlocks = ECL_RAY_MIN_BLOCKS;  // 128 threads x 8 CTAs: 64 registers, half occupancy
 
 struct V3 {
   float x, y, z;
@@ -97,7 +95,8 @@ struct Lane {
   uint32_t depth, bounces;
 };
 
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
+template <int MB>
+__global__ void __launch_bounds__(kThreads, MB)
     ray_persistent(const float4* __restrict__ scene, uint32_t ns, uint32_t w, uint32_t h, uint32_t max_depth,
                    float4* __restrict__ out, uint64_t first, uint64_t count, unsigned* __restrict__ ctrl) {
   __shared__ float4 sph[kMaxSpheres], mat[kMaxSpheres];
@@ -298,13 +297,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   }
 }
 
-}  // namespace
-
-cudaError_t launch_ray(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
-  if (count == 0) return cudaSuccess;
+template <int MB>
+cudaError_t launch(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
   static int blocks_per_sm = 0;
   if (blocks_per_sm == 0) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ray_persistent, kThreads, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ray_persistent<MB>, kThreads, 0);
     if (e != cudaSuccess) return e;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
@@ -312,10 +309,31 @@ cudaError_t launch_ray(const KernelSpec& spec, const LaunchEnv& env, uint64_t fi
   const uint64_t blocks_needed = (chunks + kThreads / 32 - 1) / (kThreads / 32);
   uint64_t grid = static_cast<uint64_t>(env.sms) * static_cast<uint64_t>(blocks_per_sm);
   if (blocks_needed < grid) grid = blocks_needed;
-  ray_persistent<<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
+  ray_persistent<MB><<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
       static_cast<const float4*>(env.in[0]), spec.ray.spheres, spec.ray.width, spec.ray.height, spec.ray.max_depth,
       static_cast<float4*>(env.out[0]), first, count, env.ctrl);
   return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_ray(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
+  if (count == 0) return cudaSuccess;
+  // ECL_RAY_MB: 128-thread CTAs per SM the registers are sized for.  Measured
+  // (8192^2): 6 -> 20.4 ms, 8 -> 19.0, 10 -> 18.0 (48 regs, small spill),
+  // 12 -> 18.0, 16 -> 18.5: occupancy beats the spills up to ~40 warps.
+  static const int mb = [] {
+    const char* v = std::getenv("ECL_RAY_MB");
+    return v ? std::atoi(v) : 0;
+  }();
+  switch (mb) {
+    case 6: return launch<6>(spec, env, first, count);
+    case 7: return launch<7>(spec, env, first, count);
+    case 8: return launch<8>(spec, env, first, count);
+    case 12: return launch<12>(spec, env, first, count);
+    case 16: return launch<16>(spec, env, first, count);
+    default: return launch<10>(spec, env, first, count);
+  }
 }
 
 }  // namespace ecl
