@@ -46,8 +46,8 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
 // coordinate): every interaction step is an FADD2/FFMA2/FMUL2 on the pair
 // (the source body is a broadcast .F32 operand), halving the FP32 issue
 // slots; only the two MUFU.RSQ stay scalar.
-template <int S, int B2>
-__global__ void __launch_bounds__(kThreads)
+template <int S, int B2, int MB>
+__global__ void __launch_bounds__(kThreads, MB)
     nbody_step(const float4* __restrict__ pos, const float4* __restrict__ vel, uint64_t n, float dt, float eps2,
                float4* __restrict__ npos, float4* __restrict__ nvel, uint64_t first, uint64_t count) {
   constexpr int T = kThreads / S, B = 2 * B2;
@@ -130,11 +130,11 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-template <int S, int B2>
+template <int S, int B2, int MB = 1>
 cudaError_t launch(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
   const uint64_t per_block = static_cast<uint64_t>(kThreads / S) * 2 * B2;
   const uint64_t blocks = (count + per_block - 1) / per_block;
-  nbody_step<S, B2><<<static_cast<unsigned>(blocks), kThreads, 0, env.stream>>>(
+  nbody_step<S, B2, MB><<<static_cast<unsigned>(blocks), kThreads, 0, env.stream>>>(
       static_cast<const float4*>(env.in[0]), static_cast<const float4*>(env.in[1]), spec.nbody.bodies,
       spec.nbody.dt, spec.nbody.eps2, static_cast<float4*>(env.out[0]), static_cast<float4*>(env.out[1]), first,
       count);
@@ -162,12 +162,42 @@ cudaError_t launch_nbody(const KernelSpec& spec, const LaunchEnv& env, uint64_t 
     split = 1;
     while (split < 8 && (count + (kThreads / split) * B - 1) / ((kThreads / split) * B) < want) split *= 2;
   }
+  // ECL_NBODY_MB: resident CTAs per SM the registers are sized for.  Measured
+  // per 1M-body step: 2 (108 regs) 426.0 ms, 4 (64) 427.7, 5 435.2, 6 451.6.
+  static const int mb = [] {
+    const char* v = std::getenv("ECL_NBODY_MB");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (pairs == 2 && mb == 5) {
+    switch (split) {
+      case 1: return launch<1, 2, 5>(spec, env, first, count);
+      case 2: return launch<2, 2, 5>(spec, env, first, count);
+      case 4: return launch<4, 2, 5>(spec, env, first, count);
+      default: return launch<8, 2, 5>(spec, env, first, count);
+    }
+  }
+  if (pairs == 2 && mb == 6) {
+    switch (split) {
+      case 1: return launch<1, 2, 6>(spec, env, first, count);
+      case 2: return launch<2, 2, 6>(spec, env, first, count);
+      case 4: return launch<4, 2, 6>(spec, env, first, count);
+      default: return launch<8, 2, 6>(spec, env, first, count);
+    }
+  }
+  if (pairs == 2 && mb == 2) {
+    switch (split) {
+      case 1: return launch<1, 2, 2>(spec, env, first, count);
+      case 2: return launch<2, 2, 2>(spec, env, first, count);
+      case 4: return launch<4, 2, 2>(spec, env, first, count);
+      default: return launch<8, 2, 2>(spec, env, first, count);
+    }
+  }
   if (pairs == 2) {
     switch (split) {
-      case 1: return launch<1, 2>(spec, env, first, count);
-      case 2: return launch<2, 2>(spec, env, first, count);
-      case 4: return launch<4, 2>(spec, env, first, count);
-      default: return launch<8, 2>(spec, env, first, count);
+      case 1: return launch<1, 2, 4>(spec, env, first, count);
+      case 2: return launch<2, 2, 4>(spec, env, first, count);
+      case 4: return launch<4, 2, 4>(spec, env, first, count);
+      default: return launch<8, 2, 4>(spec, env, first, count);
     }
   }
   switch (split) {
