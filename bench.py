@@ -380,7 +380,9 @@ def merge_clocks(*cs):
 # ---------------------------------------------------------------------------
 # arms
 
-NCU_KERNEL = {"mandelbrot": "mandel_persistent<double", "mandelbrot_f32": "mandel_persistent<float",
+L2_FLUSH_BYTES = 512 << 20
+
+NCU_KERNEL = {"mandelbrot": "mandel_persistent<double", "mandelbrot_f32": "mandel_x2<float",
               "gaussian": "gaussian_tiled", "binomial": "binomial_warp", "nbody": "nbody_step",
               "ray": "ray_persistent"}
 
@@ -573,16 +575,26 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
         else:
             eng.run_into(inputs, outputs, want_trace=False)
 
+    # L2 flush between timed steps: a 512 MiB write (4x the 126 MB L2) on this
+    # rank's GPU before every step, outside the step's events.
+    flush_buf = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=torch.device("cuda", torch.cuda.current_device()))
+
     def timed(fn, steps):
-        barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        total = 0.0
         for _ in range(steps):
+            flush_buf.zero_()
+            torch.cuda.synchronize()
+            barrier()
+            e0.record(stream)
             fn()
-        e1.record(stream)
+            e1.record(stream)
+            e1.synchronize()
+            total += e0.elapsed_time(e1)
+        torch.cuda.synchronize()
         barrier()
-        return e0.elapsed_time(e1) / steps
+        return total / steps
 
     # --- device-resident (value): inputs uploaded once before timing ---
     run(in_arrays, None)
@@ -616,6 +628,8 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
     native_k, native_e2e = [], []
     if wl.steps_per_run == 1:
         for _ in range(args.warmup + args.steps):
+            flush_buf.zero_()  # same L2 state as the timed engine steps
+            torch.cuda.synchronize()
             native_k.append(eng.native_run(None, None)[0])
         for _ in range(max(1, args.steps)):
             native_e2e.append(eng.native_run(in_arrays, out_arrays)[1])
@@ -660,7 +674,7 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
                    "parallelism": f"coexec{n}" + ("-processes" if shared else ""),
                    "coordination": ("one process per GPU, shared-memory decision log" if shared else
                                     "one process, one host thread per GPU"),
-                   "l2": "no L2 flush: per-step outputs (and inputs) are streamed once; Mandelbrot writes 4 GiB/step"},
+                   "l2": "L2 flushed before every timed step (512 MiB write, outside the step's CUDA events)"},
         "e2e": {"value": units / (ms_e2e * 1e-3), "unit": "work-items/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
         "roofline": {"bound": wl.bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

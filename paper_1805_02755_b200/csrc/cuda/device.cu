@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -122,9 +123,18 @@ struct ecl_gpu {
     return n > 0 ? static_cast<uint64_t>(n) : ~uint64_t{0};
   }();
   uint64_t piece_counter = 0;
+  uint64_t input_gen = 0;  // see next_input_gen()
 };
 
 namespace {
+
+// Process-unique ids of input contents: a kernel that derives per-device
+// state from its inputs (Gaussian's constant-bank filter) redoes it only when
+// the id or the buffer changes.
+uint64_t next_input_gen() {
+  static std::atomic<uint64_t> gen{0};
+  return ++gen;
+}
 
 Slot* find_slot(ecl_gpu* g, uint64_t seq) {
   for (auto& s : g->slots)
@@ -145,6 +155,8 @@ ecl::LaunchEnv env_of(const ecl_gpu* g, int lane) {
   env.out = g->out.data();
   env.ctrl = g->ctrl + lane * kCtrlWordsPerLane;
   env.scratch = g->scratch;
+  env.device = g->ordinal;
+  env.input_gen = g->input_gen;
   return env;
 }
 
@@ -402,6 +414,7 @@ int ecl_gpu_swap_io(ecl_gpu* g, uint32_t i, uint32_t o) {
   if (int rc = set_device(g)) return rc;
   if (int rc = sync_all(g)) return rc;
   std::swap(g->in[i], g->out[o]);
+  g->input_gen = next_input_gen();
   return ECL_OK;
 }
 
@@ -411,6 +424,7 @@ int ecl_gpu_upload_inputs(ecl_gpu* g, const void* const* host_inputs) {
   for (size_t i = 0; i < g->in.size(); ++i) {
     if (!host_inputs || !host_inputs[i]) continue;
     ECL_CK(cudaMemcpyAsync(g->in[i], host_inputs[i], g->in_bytes[i], cudaMemcpyHostToDevice, g->lane[0]));
+    g->input_gen = next_input_gen();
   }
   return fan_out_lane0(g);
 }
@@ -434,6 +448,7 @@ int ecl_replicate_inputs(ecl_gpu* const* gpus, uint32_t n, uint32_t root) {
       for (size_t b = 0; b < dst->in.size(); ++b)
         ECL_CK(cudaMemcpyPeerAsync(dst->in[b], dst->ordinal, src->in[b], src->ordinal, dst->in_bytes[b],
                                    dst->lane[0]));
+      dst->input_gen = next_input_gen();
       if (int rc = fan_out_lane0(dst)) return rc;
     }
   }

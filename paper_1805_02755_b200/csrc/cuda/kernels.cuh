@@ -78,6 +78,8 @@ struct LaunchEnv {
   unsigned* ctrl = nullptr;    // zeroed per-device control words (work counters)
   void* scratch = nullptr;     // per-device, per-binding kernel scratch (scratch_bytes())
   uint32_t* compact = nullptr;  // replicate > 1 and host copies pending: one value per item
+  int device = 0;               // CUDA ordinal
+  uint64_t input_gen = 0;       // process-unique id of the current input contents (changes on upload)
 };
 
 // Device scratch a kernel needs per binding (e.g. Mandelbrot coordinate tables),
@@ -103,10 +105,10 @@ cudaError_t launch_nbody(const KernelSpec& spec, const LaunchEnv& env, uint64_t 
 cudaError_t launch_binomial(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
 cudaError_t launch_ray(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
 
-// Exactly-once tally: tally[i] += 1 for i in [first, first + count).
 // Test hook (ECL_FAULT_INJECTION=1 only): the work-item `fault_item` executes
 // a trap, so the device faults mid-run (reference test_engine.cpp:236-254).
 cudaError_t launch_fault(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
+// Exactly-once tally: tally[i] += 1 for i in [first, first + count).
 cudaError_t launch_tally(uint32_t* tally, uint64_t first, uint64_t count, cudaStream_t stream);
 
 }  // namespace ecl

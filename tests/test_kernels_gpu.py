@@ -184,3 +184,29 @@ def test_nbody_multi_step_exchange(gpu_available, oracle, n_dev, sched):
     assert ok, worst
     scale = float(np.abs(ev[:, :3]).max())
     assert float(np.abs(out[1][:, :3] - ev[:, :3]).max()) <= 2e-4 * scale
+
+
+def test_gaussian_filters_of_two_live_engines_do_not_mix(gpu_available, oracle):
+    # the packed filter lives in the device's constant bank and is rebuilt
+    # only when the filter buffer or its contents change: two engines with
+    # different filters, alternating device-resident runs, must each see
+    # their own filter
+    w, h = 256, 128
+    img, f31 = W.gaussian_inputs(w, h, 31, seed=5)
+    f_sharp = W.gaussian_filter(31, 1.5).ravel()
+    progs = [P.validate_program(W.gaussian_spec(w, h, 31)) for _ in range(2)]
+    engines = [P.Engine(P.EngineConfig(devices(1), P.StaticConfig()), p) for p in progs]
+    try:
+        filters = [f31, f_sharp]
+        for e, f in zip(engines, filters):
+            e.run_into([img, f], None)
+        for _ in range(2):
+            for e, f in zip(engines, filters):
+                e.run_into(None, None)  # resident inputs
+                out = np.zeros(w * h, np.float32)
+                e.gather([out])
+                ok, worst = rel_close(out, oracle.gaussian(img, f, w, h, 31), 1e-5)
+                assert ok, worst
+    finally:
+        for e in engines:
+            e.close()

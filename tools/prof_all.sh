@@ -12,4 +12,4 @@ cap gaussian gaussian_tiled
 cap binomial binomial_warp
 cap nbody nbody_step "--steps-override 1"
 cap ray ray_persistent
-cap mandelbrot_f32 mandel_persistent
+cap mandelbrot_f32 mandel_x2
