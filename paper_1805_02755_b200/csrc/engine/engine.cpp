@@ -102,7 +102,10 @@ struct Engine::Impl {
   bool stop = false;
   RunState* current = nullptr;
 
-  Impl(EngineConfig c, ValidatedProgram p) : cfg(std::move(c)), prog(std::move(p)) {}
+  Impl(EngineConfig c, ValidatedProgram p)
+      : cfg(std::move(c)), prog(std::move(p)), summary(summarize(prog)), sched_desc(describe(cfg.scheduler)) {}
+  const ProgramSummary summary;  // per-run trace fields that never change
+  const std::string sched_desc;
 
   double now_ms() const { return std::chrono::duration<double, std::milli>(Clock::now() - epoch).count(); }
   static double clock_cb(void* self) { return static_cast<Impl*>(self)->now_ms(); }
@@ -490,9 +493,9 @@ struct Engine::Impl {
 
   ExecutionTrace assemble(std::vector<Package> completed) {
     ExecutionTrace t;
-    t.program = summarize(prog);
+    t.program = summary;
     t.devices = cfg.devices;
-    t.scheduler = describe(cfg.scheduler);
+    t.scheduler = sched_desc;
     t.clock_mode = cfg.clock_mode;
     t.seed = cfg.seed;
     t.init_ms = wall() ? init_ms : 0.0;
