@@ -85,11 +85,15 @@ class DeviceProfile:
     bandwidth_bytes_per_ms: float = 1.0
     backend: Backend = field(default_factory=Backend)
     min_package_work_groups: int = 1
+    kernel: str = ""  # per-device specialization "<kernel>@<variant>"; "" = the program's kernel
 
     def to_json(self):
-        return {"id": self.id, "name": self.name or self.id, "computing_power": self.computing_power,
-                "launch_overhead_ms": self.launch_overhead_ms, "bandwidth_bytes_per_ms": self.bandwidth_bytes_per_ms,
-                "backend": self.backend.to_json(), "min_package_work_groups": self.min_package_work_groups}
+        j = {"id": self.id, "name": self.name or self.id, "computing_power": self.computing_power,
+             "launch_overhead_ms": self.launch_overhead_ms, "bandwidth_bytes_per_ms": self.bandwidth_bytes_per_ms,
+             "backend": self.backend.to_json(), "min_package_work_groups": self.min_package_work_groups}
+        if self.kernel:
+            j["kernel"] = self.kernel
+        return j
 
     @staticmethod
     def from_json(j) -> "DeviceProfile":
@@ -98,15 +102,15 @@ class DeviceProfile:
                           b.get("copy_split_items", 1 << 23), b.get("widen_per_8", 8))
         return DeviceProfile(j["id"], j.get("name", j["id"]), j.get("computing_power", 1.0),
                              j.get("launch_overhead_ms", 0.0), j.get("bandwidth_bytes_per_ms", 1.0), backend,
-                             j.get("min_package_work_groups", 0))
+                             j.get("min_package_work_groups", 0), j.get("kernel", ""))
 
 
 def cuda_device(id: str, ordinal: int = 0, power: float = 1.0, queue_depth: int = 2,
                 min_package_work_groups: int = 1, widen_per_8: int = 8,
-                copy_split_items: int = 1 << 23) -> DeviceProfile:
+                copy_split_items: int = 1 << 23, kernel: str = "") -> DeviceProfile:
     return DeviceProfile(id, id, power, 0.0, 1.0,
                          Backend(BackendKind.Cuda, ordinal, queue_depth, copy_split_items, widen_per_8),
-                         min_package_work_groups)
+                         min_package_work_groups, kernel)
 
 
 def simulated_device(id: str, power: float, overhead_ms: float = 0.0, bandwidth: float = float(1 << 20),

@@ -41,10 +41,14 @@ struct Device {
   explicit Device(int ordinal = 0, double power = 1.0, std::uint32_t queue_depth = 2,
                   std::uint64_t min_package_work_groups = 0)
       : ordinal(ordinal), power(power), queue_depth(queue_depth), min_package_work_groups(min_package_work_groups) {}
+  /// Paper: Device(platform, device, kernel) — this device runs its own
+  /// specialization of the program's kernel ("<kernel>@<variant>").
+  Device(int ordinal, std::string kernel) : Device(ordinal) { this->kernel = std::move(kernel); }
   int ordinal;
   double power;
   std::uint32_t queue_depth;
   std::uint64_t min_package_work_groups;  // 0 = coexec's power-ratio heuristic
+  std::string kernel;                     // "" = the program's kernel
 };
 
 /// Scheduler selection.
@@ -188,6 +192,7 @@ class EngineCL {
       d.backend.ordinal = devices_[i].ordinal;
       d.backend.queue_depth = devices_[i].queue_depth;
       d.min_package_work_groups = devices_[i].min_package_work_groups;
+      d.kernel = devices_[i].kernel;
       cfg.devices.push_back(d);
     }
     if (cfg.devices.empty()) {

@@ -53,13 +53,15 @@ inline Backend backend_from_json(const json& j) {
 }
 
 inline json to_json(const DeviceProfile& d) {
-  return json{{"id", d.id},
-              {"name", d.name},
-              {"computing_power", d.computing_power},
-              {"launch_overhead_ms", d.launch_overhead_ms},
-              {"bandwidth_bytes_per_ms", d.bandwidth_bytes_per_ms},
-              {"backend", to_json(d.backend)},
-              {"min_package_work_groups", d.min_package_work_groups}};
+  json j{{"id", d.id},
+         {"name", d.name},
+         {"computing_power", d.computing_power},
+         {"launch_overhead_ms", d.launch_overhead_ms},
+         {"bandwidth_bytes_per_ms", d.bandwidth_bytes_per_ms},
+         {"backend", to_json(d.backend)},
+         {"min_package_work_groups", d.min_package_work_groups}};
+  if (!d.kernel.empty()) j["kernel"] = d.kernel;  // absent for reference-shaped profiles
+  return j;
 }
 
 inline DeviceProfile device_from_json(const json& j) {
@@ -71,6 +73,7 @@ inline DeviceProfile device_from_json(const json& j) {
   d.bandwidth_bytes_per_ms = j.value("bandwidth_bytes_per_ms", 1.0);
   if (j.contains("backend")) d.backend = backend_from_json(j.at("backend"));
   d.min_package_work_groups = j.value("min_package_work_groups", std::uint64_t{0});  // 0 = heuristic
+  d.kernel = j.value("kernel", std::string());
   return d;
 }
 

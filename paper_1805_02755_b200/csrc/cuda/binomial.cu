@@ -255,10 +255,11 @@ cudaError_t launch_binomial(const KernelSpec& spec, const LaunchEnv& env, uint64
   if (spec.binom.steps + 1 > 32 * kNodesPerLane) return cudaErrorInvalidValue;
   // work-items -> work-groups -> scalar options (4 per float4 work-group)
   const uint64_t first_opt = first / spec.lws * 4, n_opt = count / spec.lws * 4;
-  static const int variant = [] {  // ECL_BINOMIAL_VARIANT=1: scalar lattice
+  static const int env_variant = [] {  // ECL_BINOMIAL_VARIANT=1: scalar lattice
     const char* v = std::getenv("ECL_BINOMIAL_VARIANT");
     return v ? std::atoi(v) : 0;
   }();
+  const int variant = spec.variant >= 0 ? spec.variant : env_variant;
   static const int mb = [] {  // ECL_BINOMIAL_MB: resident CTAs per SM the registers are sized for
     const char* v = std::getenv("ECL_BINOMIAL_MB");
     return v ? std::atoi(v) : 0;

@@ -50,6 +50,7 @@ struct KernelSpec {
   KernelKind kind = KernelKind::VecScale;
   SyntheticProfile profile = SyntheticProfile::Constant;
   std::string id;
+  int variant = -1;  // "<kernel>@<n>" tuning variant; -1 = default (or the ECL_* env hook)
   uint64_t gws = 0, lws = 1, out_indices = 1, out_work_items = 1;
   // > 1: each work-item's out_indices uint32 outputs are identical copies
   // (Mandelbrot's 4:1 pattern); the kernel also writes one compact value per

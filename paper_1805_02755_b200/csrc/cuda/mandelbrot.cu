@@ -535,10 +535,11 @@ cudaError_t prepare_mandelbrot(const KernelSpec& spec, const LaunchEnv& env) {
 cudaError_t launch_mandelbrot(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
   if (count == 0) return cudaSuccess;
   if (spec.kind == KernelKind::MandelbrotF32) {
-    static const bool scalar = [] {  // ECL_MANDEL_F32_SCALAR=1: one pixel per lane
+    static const bool scalar_env = [] {  // ECL_MANDEL_F32_SCALAR=1: one pixel per lane
       const char* v = std::getenv("ECL_MANDEL_F32_SCALAR");
       return v && std::atoi(v) == 1;
     }();
+    const bool scalar = spec.variant >= 0 ? spec.variant == 1 : scalar_env;
     static const int mb = [] {  // ECL_MANDEL_F32_MB: resident CTAs per SM
       const char* v = std::getenv("ECL_MANDEL_F32_MB");
       return v ? std::atoi(v) : 0;
@@ -551,11 +552,11 @@ cudaError_t launch_mandelbrot(const KernelSpec& spec, const LaunchEnv& env, uint
     }
   }
   // Tuning hook (ECL_MANDEL_VARIANT): block length R and resident CTAs per SM.
-  static const int variant = [] {
+  static const int env_variant = [] {
     const char* v = std::getenv("ECL_MANDEL_VARIANT");
     return v ? std::atoi(v) : 0;
   }();
-  switch (variant) {
+  switch (spec.variant >= 0 ? spec.variant : env_variant) {
     case 1: return launch_real<double, 16, 6>(spec.mandel, env, first, count);
     case 2: return launch_real<double, 32, 4>(spec.mandel, env, first, count);
     case 3: return launch_real<double, 8, 4>(spec.mandel, env, first, count);

@@ -151,10 +151,11 @@ cudaError_t launch_nbody(const KernelSpec& spec, const LaunchEnv& env, uint64_t 
     const char* v = std::getenv("ECL_NBODY_SPLIT");
     return v ? std::atoi(v) : 0;
   }();
-  static const int pairs = [] {  // ECL_NBODY_PAIRS: target pairs per thread (2 measured 4.6 % faster than 1)
+  static const int env_pairs = [] {  // ECL_NBODY_PAIRS: target pairs per thread (2 measured 4.6 % faster than 1)
     const char* v = std::getenv("ECL_NBODY_PAIRS");
     return v && std::atoi(v) == 1 ? 1 : 2;
   }();
+  const int pairs = spec.variant == 1 ? 1 : spec.variant == 0 ? 2 : env_pairs;  // nbody@1: one pair
   const int B = 2 * pairs;
   const uint64_t want = 4ull * static_cast<uint64_t>(env.sms > 0 ? env.sms : 148);
   int split = forced;

@@ -322,10 +322,12 @@ cudaError_t launch_ray(const KernelSpec& spec, const LaunchEnv& env, uint64_t fi
   // ECL_RAY_MB: 128-thread CTAs per SM the registers are sized for.  Measured
   // (8192^2): 6 -> 20.4 ms, 8 -> 19.0, 10 -> 18.0 (48 regs, small spill),
   // 12 -> 18.0, 16 -> 18.5: occupancy beats the spills up to ~40 warps.
-  static const int mb = [] {
+  static const int env_mb = [] {
     const char* v = std::getenv("ECL_RAY_MB");
     return v ? std::atoi(v) : 0;
   }();
+  // ray@1: 8 CTAs/SM (no-spill register budget), ray@2: 6
+  const int mb = spec.variant == 1 ? 8 : spec.variant == 2 ? 6 : spec.variant == 0 ? 10 : env_mb;
   switch (mb) {
     case 6: return launch<6>(spec, env, first, count);
     case 7: return launch<7>(spec, env, first, count);

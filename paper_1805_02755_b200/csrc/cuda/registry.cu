@@ -46,7 +46,21 @@ int bad(std::string* err, const std::string& msg) {
 }  // namespace
 
 int resolve_kernel(KernelSpec& s, std::string* err) {
-  const std::string& id = s.id;
+  // "<kernel>@<n>": the same kernel's tuning variant n (per-device kernel
+  // specialization) — identical results, different code.
+  std::string id = s.id;
+  s.variant = -1;
+  if (const auto at = id.find('@'); at != std::string::npos) {
+    const std::string v = id.substr(at + 1);
+    char* end = nullptr;
+    const long n = v.empty() ? -1 : std::strtol(v.c_str(), &end, 10);
+    if (v.empty() || *end != '\0' || n < 0 || n > 15) {
+      *err = "kernel variant must be '<kernel>@<0..15>', got '" + s.id + "'";
+      return ECL_UNKNOWN_KERNEL;
+    }
+    s.variant = static_cast<int>(n);
+    id = id.substr(0, at);
+  }
   if (id == "vecscale") {
     s.kind = KernelKind::VecScale;
   } else if (id == "mandelbrot") {
@@ -76,6 +90,22 @@ int resolve_kernel(KernelSpec& s, std::string* err) {
   } else {
     *err = "no kernel registered as '" + id + "'";
     return ECL_UNKNOWN_KERNEL;
+  }
+
+  {
+    int max_variant = 0;  // per kind: the variants its launcher implements
+    switch (s.kind) {
+      case KernelKind::Mandelbrot: max_variant = 6; break;
+      case KernelKind::MandelbrotF32: max_variant = 1; break;
+      case KernelKind::Binomial: max_variant = 1; break;
+      case KernelKind::NBody: max_variant = 1; break;
+      case KernelKind::Ray: max_variant = 2; break;
+      default: break;
+    }
+    if (s.variant > max_variant) {
+      *err = "kernel '" + id + "' has variants 0.." + std::to_string(max_variant);
+      return ECL_UNKNOWN_KERNEL;
+    }
   }
 
   switch (s.kind) {

@@ -86,6 +86,7 @@ struct Engine::Impl {
   double init_ms = 0.0;
   bool init_charged = false;
   ecl_kernel* kernel = nullptr;
+  std::vector<std::pair<std::string, ecl_kernel*>> special;  // per-device specializations
   std::vector<std::unique_ptr<Device>> devices;  // the devices this process drives
   std::vector<int> local_of;                     // global device index -> devices[] slot or -1
   std::unique_ptr<SharedCoordinator> shared;     // one process per GPU (cfg.shared)
@@ -125,7 +126,28 @@ struct Engine::Impl {
     }
   }
 
+  // The program's kernel plus any per-device specializations (distinct ids).
+  ecl_kernel* kernel_for(const std::string& id) {
+    for (auto& [k, h] : special)
+      if (k == id) return h;
+    ecl_kernel* h = nullptr;
+    create_kernel(id, &h);
+    special.emplace_back(id, h);
+    return h;
+  }
+
+  static std::string base_id(const std::string& id) { return id.substr(0, id.find('@')); }
+
   void make_kernel() {
+    create_kernel(prog.spec().kernel, &kernel);
+    for (const DeviceProfile& d : cfg.devices)
+      if (!d.kernel.empty() && base_id(d.kernel) != base_id(prog.spec().kernel))
+        throw Error(ErrorCode::ConfigError, "device '" + d.id + "': kernel '" + d.kernel +
+                                                "' is not a variant of the program's kernel '" +
+                                                prog.spec().kernel + "'");
+  }
+
+  void create_kernel(const std::string& id, ecl_kernel** out) {
     const ProgramSpec& s = prog.spec();
     std::vector<ecl_arg> args;
     for (const ArgValue& a : s.args) {
@@ -140,11 +162,11 @@ struct Engine::Impl {
     std::vector<ecl_buffer_geom> ins, outs;
     for (const BufferDesc& b : s.in_buffers) ins.push_back({b.element_size_bytes, b.element_count});
     for (const BufferDesc& b : s.out_buffers) outs.push_back({b.element_size_bytes, b.element_count});
-    check(ecl_kernel_create(s.kernel.c_str(), s.global_work_size, s.local_work_size, args.data(),
+    check(ecl_kernel_create(id.c_str(), s.global_work_size, s.local_work_size, args.data(),
                             static_cast<std::uint32_t>(args.size()), ins.data(), static_cast<std::uint32_t>(ins.size()),
                             outs.data(), static_cast<std::uint32_t>(outs.size()), s.out_pattern.out_indices,
-                            s.out_pattern.work_items, &kernel),
-          "kernel '" + s.kernel + "'");
+                            s.out_pattern.work_items, out),
+          "kernel '" + id + "'");
   }
 
   // Index into `devices` of global device i, -1 if a peer process drives it.
@@ -170,7 +192,8 @@ struct Engine::Impl {
       check(ecl_gpu_set_copy_split(d->gpu, be.copy_split_items), "copy split");
       check(ecl_gpu_set_widen_fraction(d->gpu, be.widen_per_8), "widen fraction");
       devices.push_back(std::move(d));
-      check(ecl_gpu_bind(devices.back()->gpu, kernel), "bind '" + cfg.devices[i].id + "'");
+      ecl_kernel* k = cfg.devices[i].kernel.empty() ? kernel : kernel_for(cfg.devices[i].kernel);
+      check(ecl_gpu_bind(devices.back()->gpu, k), "bind '" + cfg.devices[i].id + "'");
     }
     for (auto& d : devices) d->thread = std::thread([this, dev = d.get()] { device_loop(*dev); });
   }
@@ -187,6 +210,8 @@ struct Engine::Impl {
     devices.clear();
     if (kernel) ecl_kernel_destroy(kernel);
     kernel = nullptr;
+    for (auto& [id, h] : special) ecl_kernel_destroy(h);
+    special.clear();
   }
 
   // ---- wall mode ---------------------------------------------------------

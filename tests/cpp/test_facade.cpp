@@ -118,7 +118,9 @@ static void mandelbrot_hguided(int ng) {
   const uint64_t w = 512, h = 384;
   std::vector<uint32_t> counts(w * h * 4);
   ecl::EngineCL engine;
-  engine.use(ecl::Device(0 % ng), ecl::Device(1 % ng));
+  // the second device runs a specialization of the kernel (two pixels per
+  // lane), the paper's Device(platform, device, kernel)
+  engine.use(ecl::Device(0 % ng), ecl::Device(1 % ng, "mandelbrot@5"));
   engine.work_items(w * h, 256);
   engine.scheduler(ecl::Scheduler::HGuided(2.0));
   ecl::Program program;

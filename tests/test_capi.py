@@ -96,3 +96,34 @@ def test_kernel_registry_validates_shapes():
     assert create("binomial", 255 * 8, 255, [254], [(16, 8)], [(16, 8)], 1, 255) == 0
     assert create("gaussian", 64 * 32, 128, [64, 32, 31], [(4, 64 * 32), (4, 31 * 31)], [(4, 64 * 32)]) == 0
     assert create("nbody", 1024, 64, [1024, 0.005, 500.0], [(16, 1024)] * 2, [(16, 1024)] * 2) == 0
+
+
+def test_kernel_variant_ids():
+    # per-device specialization ids "<kernel>@<n>", resolved
+    # by the device layer without a GPU
+    lib = ctypes.CDLL(N.CUDA_LIB_PATH)
+    lib.ecl_kernel_create.restype = ctypes.c_int
+
+    class Geom(ctypes.Structure):
+        _fields_ = [("element_size_bytes", ctypes.c_uint64), ("element_count", ctypes.c_uint64)]
+
+    class Arg(ctypes.Structure):
+        _fields_ = [("is_double", ctypes.c_int32), ("reserved", ctypes.c_int32), ("i", ctypes.c_int64),
+                    ("d", ctypes.c_double)]
+
+    def create(kid):
+        vals = [64, 64, 16, -2.5, -1.25, 1.0, 1.25]
+        a = (Arg * 7)(*[Arg(int(isinstance(x, float)), 0, int(x) if isinstance(x, int) else 0, float(x))
+                        for x in vals])
+        go = (Geom * 1)(Geom(4, 64 * 64 * 4))
+        k = ctypes.c_void_p()
+        rc = lib.ecl_kernel_create(kid.encode(), ctypes.c_uint64(64 * 64), ctypes.c_uint64(256), a, 7, None, 0,
+                                   go, 1, ctypes.c_uint64(4), ctypes.c_uint64(1), ctypes.byref(k))
+        if rc == 0:
+            lib.ecl_kernel_destroy(k)
+        return rc
+
+    for ok in ("mandelbrot", "mandelbrot@0", "mandelbrot@5", "mandelbrot@6"):
+        assert create(ok) == 0, ok
+    for bad in ("mandelbrot@7", "mandelbrot@", "mandelbrot@x", "mandelbrot@-1"):
+        assert N.code_name(create(bad)) == "UnknownKernel", bad

@@ -263,3 +263,27 @@ def test_fault_kernel_is_not_registered_by_default(gpu_available):
         with P.Engine(P.EngineConfig([P.cuda_device("gpu0", 0)], P.StaticConfig()), P.validate_program(spec)) as eng:
             eng.run()
     assert e.value.code == P.ErrorCode.UnknownKernel
+
+
+@pytest.mark.parametrize("variants", [("mandelbrot", "mandelbrot@5"), ("mandelbrot@3", "mandelbrot@6")])
+def test_per_device_kernel_specialization_is_bit_exact(gpu_available, oracle, variants):
+    # SURVEY §8f row 4 / PAPER.md:395-421: each device runs its own variant of
+    # the program's kernel; the co-executed image is still the reference's
+    w, h, it = 512, 384, 512
+    ng = P.gpu_count()
+    devs = [P.cuda_device(f"gpu{i}", i % ng, kernel=k) for i, k in enumerate(variants)]
+    prog = P.validate_program(W.mandelbrot_spec(w, h, it))
+    with P.Engine(P.EngineConfig(devs, P.HGuidedConfig()), prog) as e:
+        res = e.run()
+    assert P.tiles_exactly(res.trace.packages, prog.total_work_groups())
+    assert len({p.device_id for p in res.trace.packages}) == 2
+    assert np.array_equal(res.outputs[0].view(np.uint32), expand_4to1(oracle.mandelbrot(w, h, it)))
+    assert res.trace.raw["devices"][1]["kernel"] == variants[1]
+
+
+def test_specialization_must_be_a_variant_of_the_program_kernel(gpu_available):
+    devs = [P.cuda_device("gpu0", 0), P.cuda_device("gpu1", 0, kernel="vecscale")]
+    prog = P.validate_program(W.mandelbrot_spec(64, 64, 16))
+    with pytest.raises(P.Error) as e:
+        P.Engine(P.EngineConfig(devs, P.StaticConfig()), prog).close()
+    assert e.value.code == P.ErrorCode.ConfigError
