@@ -641,6 +641,9 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
     # --- roofline: vector peaks measured on this device ---
     f64, add, f32 = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
     N.lib.ecl_probe_vector_peaks(my_gpu, ctypes.byref(f64), ctypes.byref(add), ctypes.byref(f32))
+    mix = ctypes.c_double(0.0)
+    if wl.name == "mandelbrot":
+        N.lib.ecl_probe_mandel_mix(my_gpu, ctypes.byref(mix))
     peak = (f64.value if wl.bound == "fp64" else f32.value) * n  # whole job: N GPUs
     achieved = wl.flops() / (ms_dev * 1e-3) / 1e12
     eng.close()
@@ -707,6 +710,11 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
         # DFMA (2 flop/instr) peak is 8/12
         line["roofline"]["nonfma_ceiling_frac"] = 8.0 / 12.0
         line["roofline"]["frac_of_nonfma_ceiling"] = (achieved / peak) / (8.0 / 12.0)
+        if mix.value > 0:
+            # what the iteration's own DMUL/DADD/DFMA mix sustains on this GPU
+            # with no control flow (ecl_probe_mandel_mix): the attainable roof
+            line["roofline"]["mix_ceiling_tflops"] = mix.value * n
+            line["roofline"]["frac_of_mix_ceiling"] = achieved / (mix.value * n)
     if cpu is not None:
         line["cpu_baseline"] = cpu
     return line

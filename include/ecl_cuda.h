@@ -11,7 +11,8 @@
  * (workloads.hpp:170-233).  Plain C types only: no C++ or torch types cross it,
  * no exception crosses it.
  *
- * One ecl_gpu = one B200: a compute stream, a copy stream, a ring of timing
+ * One ecl_gpu = one B200: two compute streams ("lanes", consecutive packages
+ * alternate), one copy stream per lane, a notify stream, a ring of timing
  * events, this device's replica of every read-only input and its own output
  * partition.  Each ecl_gpu is driven by exactly one host thread.
  *
@@ -86,9 +87,10 @@ int ecl_gpu_ordinal(const ecl_gpu* gpu, int* ordinal);
 
 /* ---- kernel registry (replaces kernel_for / check_buffer_shapes) ------ */
 /* Kernel ids: "mandelbrot", "mandelbrot_f32", "vecscale",
- * "synthetic[:constant|ramp|step]", "gaussian", "nbody", "binomial", "ray".
- * Validates argument and buffer shapes once (ECL_UNKNOWN_KERNEL,
- * ECL_UNKNOWN_PROFILE, ECL_BAD_KERNEL_ARGS). */
+ * "synthetic[:constant|ramp|step]", "gaussian", "nbody", "binomial", "ray",
+ * optionally suffixed "@<n>" for a tuning variant of the same kernel (same
+ * results; per-device specialization).  Validates argument and buffer shapes
+ * once (ECL_UNKNOWN_KERNEL, ECL_UNKNOWN_PROFILE, ECL_BAD_KERNEL_ARGS). */
 int ecl_kernel_create(const char* kernel_id, uint64_t global_work_size, uint64_t local_work_size,
                       const ecl_arg* args, uint32_t n_args, const ecl_buffer_geom* inputs, uint32_t n_inputs,
                       const ecl_buffer_geom* outputs, uint32_t n_outputs, uint64_t out_indices,
@@ -182,6 +184,11 @@ int ecl_gpu_kernel_time(ecl_gpu* gpu, double* total_ms, uint64_t* launches, int 
 /* Measured vector peaks of device `ordinal` (roofline denominators for the
  * FP64/FP32-pipe kernels): DFMA TFLOP/s, DADD Tinstr/s, FFMA TFLOP/s. */
 int ecl_probe_vector_peaks(int ordinal, double* fp64_fma_tflops, double* fp64_add_tinstr, double* fp32_fma_tflops);
+/* FP64 TFLOP/s (8 flops per iteration) the Mandelbrot iteration's own
+ * instruction mix sustains on device `ordinal` without control flow: the
+ * attainable ceiling for the exact kernel (DMUL/DADD streams run below the
+ * DFMA-chain peak). */
+int ecl_probe_mandel_mix(int ordinal, double* tflops);
 
 const char* ecl_last_error(void);
 

@@ -58,7 +58,68 @@ float time_chain(int sms, int iters, cudaStream_t st, double* sink) {
   return best;
 }
 
+// The Mandelbrot iteration's own instruction mix and dependency chain
+// (3 DMUL, 1 DFMA, 2 DADD, 1 LOP3 per iteration, two pixels per thread, no
+// control flow): the FP64 rate the exact kernel can reach at best on this
+// device — DMUL/DADD streams sustain less than the DFMA-chain peak.
+__global__ void __launch_bounds__(256) mandel_mix(double* sink, unsigned* flag, int iters) {
+  double zx[2] = {0, 0}, zy[2] = {0, 0}, cx[2], cy[2];
+  unsigned acc = 0;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    cx[k] = -0.1 + 1e-9 * (threadIdx.x + k);
+    cy[k] = 0.1;
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const double xx = __dmul_rn(zx[k], zx[k]);
+        const double yy = __dmul_rn(zy[k], zy[k]);
+        acc |= static_cast<unsigned>(__double2hiint(xx)) | static_cast<unsigned>(__double2hiint(yy));
+        const double t = __dmul_rn(zx[k], zy[k]);
+        zy[k] = __fma_rn(t, 2.0, cy[k]);
+        zx[k] = __dadd_rn(__dsub_rn(xx, yy), cx[k]);
+      }
+    }
+  }
+  if (zx[0] + zx[1] + zy[0] + zy[1] == 12345.678) sink[0] = zx[0];
+  if (acc == 0x12345u) *flag = acc;
+}
+
 }  // namespace
+
+extern "C" int ecl_probe_mandel_mix(int ordinal, double* tflops) {
+  if (cudaSetDevice(ordinal) != cudaSuccess) return ECL_CONFIG_ERROR;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ordinal);
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  double* sink = nullptr;
+  cudaMalloc(&sink, 64);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 256, blocks = sms * 4;
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0, st);
+    mandel_mix<<<blocks, 256, 0, st>>>(sink, reinterpret_cast<unsigned*>(sink + 1), iters);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0 && ms < best) best = ms;
+  }
+  // 8 algorithmic flops per iteration (the roofline's Mandelbrot convention)
+  *tflops = 8.0 * 16 * iters * 2 * double(blocks) * 256 / (best * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  cudaStreamDestroy(st);
+  return cudaGetLastError() == cudaSuccess ? ECL_OK : ECL_KERNEL_PANIC;
+}
 
 extern "C" int ecl_probe_vector_peaks(int ordinal, double* fp64_fma_tflops, double* fp64_add_tinstr,
                                       double* fp32_fma_tflops) {
