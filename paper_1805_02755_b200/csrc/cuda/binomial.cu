@@ -55,6 +55,7 @@ __device__ __forceinline__ float2 shfl_from(float2 v, unsigned src) {
 // next j.
 template <int NL, typename V>
 __device__ __forceinline__ int backward(V (&c)[NL], int j, int stop, V r) {
+#pragma unroll 8
   for (; j > stop; --j) {
     const V right = shfl_down1(c[0]);
 #pragma unroll
