@@ -66,6 +66,7 @@ class Workload:
     bound = "fp32"
     steps_per_run = 1
     swaps = ()
+    copy_split = 1 << 23  # work-items per sub-launch when copies / streamed inputs pipeline
 
     def __init__(self, P, W, np):
         self.P, self.W, self.np = P, W, np
@@ -148,6 +149,7 @@ class Gaussian(Workload):
     WIDTH = HEIGHT = 4096
     F = 31
     workload = "gaussian 4096x4096 float image, 31x31 filter (sigma 5), clamp-to-edge, static, single device"
+    copy_split = 1 << 21  # 8 row bands: H2D of band k+1 and D2H of band k-1 overlap band k
 
     def spec(self):
         return self.W.gaussian_spec(self.WIDTH, self.HEIGHT, self.F)
@@ -532,10 +534,11 @@ def run_ours(args, world, rank, local):
 
 def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, rank):
     min_wg = args.min_package if args.min_package else wl.min_package(n)
+    copy_split = args.copy_split if args.copy_split else wl.copy_split
     ngpu = P.gpu_count()
     devs = [P.cuda_device(f"gpu{i}", ordinal=i % ngpu, power=1.0, queue_depth=args.queue_depth,
                           min_package_work_groups=min_wg, widen_per_8=args.widen,
-                          copy_split_items=args.copy_split) for i in range(n)]
+                          copy_split_items=copy_split) for i in range(n)]
     sched = wl.scheduler(n)
     if isinstance(sched, P.HGuidedConfig):
         sched.k = args.k
@@ -673,7 +676,7 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
         "scaling": "strong", "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic",
         "config": {"workload": wl.workload, "scheduler": P.describe(sched), "lws": prog.local_work_size(),
                    "work_items_per_step": units, "min_package_work_groups": min_wg, "queue_depth": args.queue_depth,
-                   "widen_per_8": args.widen, "copy_split_items": args.copy_split,
+                   "widen_per_8": args.widen, "copy_split_items": copy_split,
                    "parallelism": f"coexec{n}" + ("-processes" if shared else ""),
                    "coordination": ("one process per GPU, shared-memory decision log" if shared else
                                     "one process, one host thread per GPU"),
@@ -733,8 +736,9 @@ def main(argv=None):
     ap.add_argument("--min-package", type=int, default=0, help="HGuided minimum package (work-groups)")
     ap.add_argument("--widen", type=int, default=8,
                     help="replicated outputs: pieces of 8 copied compact and widened on the host")
-    ap.add_argument("--copy-split", type=int, default=1 << 23,
-                    help="work-items per sub-launch when a package copies to the host (D2H pipelining)")
+    ap.add_argument("--copy-split", type=int, default=0,
+                    help="work-items per sub-launch when a package copies to the host or streams its inputs up "
+                         "(0: the workload's default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
     if args.impl == "ours":

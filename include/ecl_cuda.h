@@ -108,6 +108,13 @@ int ecl_gpu_buffer(ecl_gpu* gpu, int is_output, uint32_t index, void** device_pt
 int ecl_gpu_swap_io(ecl_gpu* gpu, uint32_t input_index, uint32_t output_index);
 /* Async H2D of every input (host_inputs[i] may be NULL to skip one). */
 int ecl_gpu_upload_inputs(ecl_gpu* gpu, const void* const* host_inputs);
+/* Streamed inputs (single-device runs): ecl_gpu_upload_inputs only records
+ * the host sources; every package piece then uploads, on a dedicated H2D
+ * stream, the input prefix its work-items read (Gaussian rows + halo,
+ * Binomial options, vecscale elements; whole buffers otherwise) and its
+ * kernel waits for exactly that, so uploads overlap compute.  The host
+ * inputs must stay valid until ecl_gpu_sync (which uploads any rest). */
+int ecl_gpu_set_streamed_inputs(ecl_gpu* gpu, int enable);
 /* Replicates every bound input from gpus[root] to the others over NVLink
  * (cudaMemcpyPeerAsync, binary doubling tree); ordered after root's upload. */
 int ecl_replicate_inputs(ecl_gpu* const* gpus, uint32_t n, uint32_t root);

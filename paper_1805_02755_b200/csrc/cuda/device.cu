@@ -124,6 +124,14 @@ struct ecl_gpu {
   }();
   uint64_t piece_counter = 0;
   uint64_t input_gen = 0;  // see next_input_gen()
+  // Streamed inputs (ecl_gpu_set_streamed_inputs): uploads are enqueued on
+  // `h2d` piece by piece, each piece's kernel waiting for the prefix it reads.
+  bool streamed = false;
+  cudaStream_t h2d = nullptr;
+  cudaEvent_t up_ev = nullptr;         // after the latest streamed upload
+  bool up_live = false;                // up_ev recorded in this run
+  std::vector<const char*> pending_in;  // host source still streaming (nullptr: complete/resident)
+  std::vector<uint64_t> up_bytes;       // bytes of each input already enqueued
 };
 
 namespace {
@@ -176,7 +184,24 @@ int join_lanes(ecl_gpu* g) {
   return ECL_OK;
 }
 
+// Enqueues the rest of every streamed input (nothing left pending).
+int flush_streamed(ecl_gpu* g) {
+  for (size_t i = 0; i < g->pending_in.size(); ++i) {
+    if (!g->pending_in[i]) continue;
+    const uint64_t up = g->up_bytes[i];
+    if (g->in_bytes[i] > up)
+      ECL_CK(cudaMemcpyAsync(static_cast<char*>(g->in[i]) + up, g->pending_in[i] + up, g->in_bytes[i] - up,
+                             cudaMemcpyHostToDevice, g->h2d));
+    g->up_bytes[i] = g->in_bytes[i];
+    g->pending_in[i] = nullptr;
+  }
+  return ECL_OK;
+}
+
 int sync_all(ecl_gpu* g) {
+  if (int rc = flush_streamed(g)) return rc;
+  ECL_CK(cudaStreamSynchronize(g->h2d));
+  g->up_live = false;
   for (int l = 0; l < g->lanes; ++l) {
     ECL_CK(cudaStreamSynchronize(g->lane[l]));
     ECL_CK(cudaStreamSynchronize(g->copy[l]));
@@ -262,8 +287,10 @@ int ecl_gpu_open(int ordinal, uint32_t queue_depth, ecl_gpu** out) {
   }
   if ((e = cudaStreamCreateWithFlags(&g->notify, cudaStreamNonBlocking)) != cudaSuccess)
     return undo(cuda_fail(e, "cudaStreamCreate(notify)"));
+  if ((e = cudaStreamCreateWithFlags(&g->h2d, cudaStreamNonBlocking)) != cudaSuccess)
+    return undo(cuda_fail(e, "cudaStreamCreate(h2d)"));
   if ((e = cudaEventCreate(&g->epoch)) != cudaSuccess) return undo(cuda_fail(e, "cudaEventCreate"));
-  for (cudaEvent_t* ev : {&g->ready, &g->piece[0], &g->piece[1], &g->copied[0], &g->copied[1]})
+  for (cudaEvent_t* ev : {&g->ready, &g->piece[0], &g->piece[1], &g->copied[0], &g->copied[1], &g->up_ev})
     if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess)
       return undo(cuda_fail(e, "cudaEventCreate"));
   for (auto& s : g->slots) {
@@ -287,6 +314,7 @@ int ecl_gpu_close(ecl_gpu* g) {
     if (g->copy[l]) cudaStreamSynchronize(g->copy[l]);
   }
   if (g->notify) cudaStreamSynchronize(g->notify);
+  if (g->h2d) cudaStreamSynchronize(g->h2d);
   for (auto& s : g->slots) ecl::widen_wait(&s.widen);
   free_buffers(g);
   if (g->scratch) cudaFree(g->scratch);
@@ -302,8 +330,9 @@ int ecl_gpu_close(ecl_gpu* g) {
     if (s.done) cudaEventDestroy(s.done);
     for (cudaEvent_t ev : s.piece_done) cudaEventDestroy(ev);
   }
-  for (cudaEvent_t ev : {g->epoch, g->ready, g->piece[0], g->piece[1], g->copied[0], g->copied[1]})
+  for (cudaEvent_t ev : {g->epoch, g->ready, g->piece[0], g->piece[1], g->copied[0], g->copied[1], g->up_ev})
     if (ev) cudaEventDestroy(ev);
+  if (g->h2d) cudaStreamDestroy(g->h2d);
   for (int l = 0; l < kLanes; ++l) {
     if (g->lane[l]) cudaStreamDestroy(g->lane[l]);
     if (g->copy[l]) cudaStreamDestroy(g->copy[l]);
@@ -418,9 +447,30 @@ int ecl_gpu_swap_io(ecl_gpu* g, uint32_t i, uint32_t o) {
   return ECL_OK;
 }
 
+int ecl_gpu_set_streamed_inputs(ecl_gpu* g, int enable) {
+  g->streamed = enable != 0;
+  return ECL_OK;
+}
+
 int ecl_gpu_upload_inputs(ecl_gpu* g, const void* const* host_inputs) {
   if (int rc = set_device(g)) return rc;
   if (int rc = join_lanes(g)) return rc;  // no kernel of an earlier run still reads the inputs
+  if (g->streamed) {
+    // Nothing moves yet: each piece enqueues (on h2d) the prefix it reads
+    // and its kernel waits for it (ecl_gpu_submit); ecl_gpu_sync uploads
+    // whatever no piece needed.
+    if (int rc = flush_streamed(g)) return rc;  // a previous run's leftovers first
+    ECL_CK(cudaEventRecord(g->ready, g->lane[0]));
+    ECL_CK(cudaStreamWaitEvent(g->h2d, g->ready, 0));
+    g->pending_in.assign(g->in.size(), nullptr);
+    g->up_bytes.assign(g->in.size(), 0);
+    for (size_t i = 0; i < g->in.size(); ++i) {
+      if (!host_inputs || !host_inputs[i]) continue;
+      g->pending_in[i] = static_cast<const char*>(host_inputs[i]);
+      g->input_gen = next_input_gen();
+    }
+    return ECL_OK;
+  }
   for (size_t i = 0; i < g->in.size(); ++i) {
     if (!host_inputs || !host_inputs[i]) continue;
     ECL_CK(cudaMemcpyAsync(g->in[i], host_inputs[i], g->in_bytes[i], cudaMemcpyHostToDevice, g->lane[0]));
@@ -561,7 +611,9 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
   // overlaps the next piece's ramp (the timing events bracket the package
   // across both lanes).
   uint64_t piece_wg = size_wg;
-  if (copies && g->d2h_split_items > 0) {
+  bool streaming = false;
+  for (const char* p : g->pending_in) streaming = streaming || p != nullptr;
+  if ((copies || streaming) && g->d2h_split_items > 0) {
     piece_wg = std::max<uint64_t>(1, g->d2h_split_items / s.lws);
     uint64_t po = 0, pc = 0;
     if (out_range(s, offset_wg, std::min(piece_wg, size_wg), &po, &pc) != ECL_OK) piece_wg = size_wg;
@@ -585,6 +637,25 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
     if (widen) env.compact = g->compact_dev;
     const uint64_t n_wg = std::min(piece_wg, offset_wg + size_wg - wg);
     const uint64_t first = wg * s.lws, count = n_wg * s.lws;
+    if (streaming || g->up_live) {  // inputs this piece reads: enqueue the missing prefix, wait for it
+      bool moved = false;
+      for (uint32_t i = 0; i < g->pending_in.size(); ++i) {
+        if (!g->pending_in[i]) continue;
+        const uint64_t need = ecl::input_bytes_needed(s, i, first, count), up = g->up_bytes[i];
+        if (need > up) {
+          ECL_CK(cudaMemcpyAsync(static_cast<char*>(g->in[i]) + up, g->pending_in[i] + up, need - up,
+                                 cudaMemcpyHostToDevice, g->h2d));
+          g->up_bytes[i] = need;
+          moved = true;
+        }
+        if (g->up_bytes[i] >= g->in_bytes[i]) g->pending_in[i] = nullptr;
+      }
+      if (moved) {
+        ECL_CK(cudaEventRecord(g->up_ev, g->h2d));
+        g->up_live = true;
+      }
+      if (g->up_live) ECL_CK(cudaStreamWaitEvent(st, g->up_ev, 0));
+    }
     cudaError_t e = ecl::launch_kernel(s, env, first, count);
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     if (g->tally_on) {
@@ -761,6 +832,11 @@ int ecl_gpu_native_run(ecl_gpu* g, float* kernel_ms) {
   if (!g->spec) return fail(ECL_CONFIG_ERROR, "native run before bind");
   if (int rc = set_device(g)) return rc;
   if (int rc = join_lanes(g)) return rc;
+  // Inputs whole before the one launch (streamed uploads finish first; the
+  // kernel timing below starts after them).
+  if (int rc = flush_streamed(g)) return rc;
+  ECL_CK(cudaEventRecord(g->up_ev, g->h2d));
+  ECL_CK(cudaStreamWaitEvent(g->lane[0], g->up_ev, 0));
   Slot& slot = g->slots[kSlots - 1];
   ECL_CK(cudaEventRecord(slot.start, g->lane[0]));
   cudaError_t e = ecl::launch_kernel(*g->spec, env_of(g, 0), 0, g->spec->gws);

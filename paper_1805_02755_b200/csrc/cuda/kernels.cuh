@@ -90,6 +90,12 @@ cudaError_t prepare_kernel(const KernelSpec& spec, const LaunchEnv& env);
 uint64_t mandelbrot_scratch_bytes(const KernelSpec& spec);
 cudaError_t prepare_mandelbrot(const KernelSpec& spec, const LaunchEnv& env);
 
+// Prefix of input `input` (bytes) the work-items [first, first+count) read:
+// lets the device layer stream an input up ahead of the pieces that need it
+// (Gaussian rows + halo, Binomial options, vecscale elements); other
+// kernels read whole buffers.
+uint64_t input_bytes_needed(const KernelSpec& spec, uint32_t input, uint64_t first, uint64_t count);
+
 // Parses and validates (kernel_for + check_buffer_shapes semantics).
 // Returns ECL_OK or a negative status with *err filled.
 int resolve_kernel(KernelSpec& spec, std::string* err);

@@ -3,6 +3,7 @@
 // Mirrors parse_kernel_id / check_buffer_shapes / kernel_for
 // (workloads.hpp:154-233) for the reference's kernels and fixes the shapes of
 // the paper's other benchmarks (Table 2).
+#include <algorithm>
 #include <cstring>
 
 #include <cstdlib>
@@ -236,6 +237,26 @@ cudaError_t prepare_kernel(const KernelSpec& spec, const LaunchEnv& env) {
     case KernelKind::Mandelbrot:
     case KernelKind::MandelbrotF32: return prepare_mandelbrot(spec, env);
     default: return cudaSuccess;
+  }
+}
+
+uint64_t input_bytes_needed(const KernelSpec& spec, uint32_t input, uint64_t first, uint64_t count) {
+  const ecl_buffer_geom& g = spec.inputs[input];
+  const uint64_t whole = g.element_size_bytes * g.element_count;
+  const uint64_t end = first + count;  // work-items [first, end)
+  switch (spec.kind) {
+    case KernelKind::VecScale:  // in[i] for item i
+      return std::min(whole, end * g.element_size_bytes);
+    case KernelKind::Gaussian: {
+      if (input != 0) return whole;  // the filter
+      const uint64_t w = spec.gauss.width, r = spec.gauss.filter / 2;
+      const uint64_t last_row = (end - 1) / w;  // clamp-to-edge reads rows up to last_row + R
+      return std::min(whole, (last_row + r + 1) * w * g.element_size_bytes);
+    }
+    case KernelKind::Binomial:  // one float4 of options per work-group
+      return std::min(whole, ((end + spec.lws - 1) / spec.lws) * g.element_size_bytes);
+    default:
+      return whole;
   }
 }
 

@@ -86,6 +86,7 @@ struct Engine::Impl {
   double init_ms = 0.0;
   bool init_charged = false;
   ecl_kernel* kernel = nullptr;
+  bool inputs_streaming = false;  // this run's inputs stream up piece by piece (one device)
   std::vector<std::pair<std::string, ecl_kernel*>> special;  // per-device specializations
   std::vector<std::unique_ptr<Device>> devices;  // the devices this process drives
   std::vector<int> local_of;                     // global device index -> devices[] slot or -1
@@ -195,6 +196,9 @@ struct Engine::Impl {
       ecl_kernel* k = cfg.devices[i].kernel.empty() ? kernel : kernel_for(cfg.devices[i].kernel);
       check(ecl_gpu_bind(devices.back()->gpu, k), "bind '" + cfg.devices[i].id + "'");
     }
+    // One device in this process: stream its inputs up piece by piece so
+    // the H2D overlaps the first packages (replication needs them whole).
+    if (devices.size() == 1 && !shared) check(ecl_gpu_set_streamed_inputs(devices[0]->gpu, 1), "streamed inputs");
     for (auto& d : devices) d->thread = std::thread([this, dev = d.get()] { device_loop(*dev); });
   }
 
@@ -326,7 +330,7 @@ struct Engine::Impl {
     }
     // Outputs complete in host memory: pending copies and widening drained
     // (device-resident runs have nothing in flight once the kernels ended).
-    if (host_out) {
+    if (host_out || inputs_streaming) {  // copies / widening / the rest of streamed inputs
       if (const int rc = ecl_gpu_sync(dev.gpu); rc != ECL_OK)
         fail(rs, Error(code_of_status(rc), std::string("device '") + profile.id + "': " + ecl_last_error()));
     }
@@ -341,7 +345,14 @@ struct Engine::Impl {
       throw Error(ErrorCode::ConfigError, "expected " + std::to_string(s.out_buffers.size()) + " output buffers");
 
     const bool tally = begin_run(inputs);
-    std::vector<Package> done = co_execute(resident ? std::span<void* const>() : outputs, 0, tally);
+    std::vector<Package> done;
+    try {
+      done = co_execute(resident ? std::span<void* const>() : outputs, 0, tally);
+    } catch (...) {
+      inputs_streaming = false;
+      throw;
+    }
+    inputs_streaming = false;
     last_resident = resident;
     last_packages = done;
     ExecutionTrace t = assemble(std::move(done));
@@ -382,6 +393,7 @@ struct Engine::Impl {
       check(ecl_gpu_set_epoch(d->gpu, nullptr, nullptr), "epoch");
     }
     if (!inputs.empty()) {
+      inputs_streaming = devices.size() == 1 && !shared;
       check(ecl_gpu_upload_inputs(g[0], const_cast<const void* const*>(inputs.data())), "upload");
       if (g.size() > 1) check(ecl_replicate_inputs(g.data(), static_cast<std::uint32_t>(g.size()), 0), "replicate");
       inputs_resident = true;
@@ -468,7 +480,13 @@ struct Engine::Impl {
     for (std::uint32_t k = 0; k < steps; ++k) {
       if (tally && k > 0)
         for (auto& d : devices) check(ecl_gpu_enable_tally(d->gpu, 1), "tally");
-      step = co_execute({}, all.size(), tally);
+      try {
+        step = co_execute({}, all.size(), tally);
+      } catch (...) {
+        inputs_streaming = false;
+        throw;
+      }
+      inputs_streaming = false;  // streamed up during the first step
       if (k + 1 < steps) {
         if (g.size() > 1)
           for (const Package& p : step) {

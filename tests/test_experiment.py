@@ -136,7 +136,9 @@ def test_wall_clock_b200_experiment(tmp_path, gpu_available):
     assert s["clock_mode"] == "wall" and len(s["outcomes"]) == len(cfg["schedulers"])
     for o in s["outcomes"]:
         m = o["metrics"]
-        assert 0 < m["balance"] <= 1.0 and m["speedup"] > 0 and abs(sum(m["work_share"].values()) - 1) < 1e-9
+        # balance = span of the first finisher / span of the last (metrics.hpp:25-48):
+        # a first finisher that started earlier can exceed 1 by a hair
+        assert 0 < m["balance"] <= 1.01 and m["speedup"] > 0 and abs(sum(m["work_share"].values()) - 1) < 1e-9
         assert len(o["t_totals_ms"]) == cfg["repetitions"] - cfg["warmup_discard"]
         t = P.ExecutionTrace(json.load(open(tmp_path / "out" / o["median_trace"])))
         assert P.tiles_exactly(t.packages, t.raw["program"]["total_work_groups"])
