@@ -149,7 +149,7 @@ class Gaussian(Workload):
     WIDTH = HEIGHT = 4096
     F = 31
     workload = "gaussian 4096x4096 float image, 31x31 filter (sigma 5), clamp-to-edge, static, single device"
-    copy_split = 1 << 21  # 8 row bands: H2D of band k+1 and D2H of band k-1 overlap band k
+    copy_split = 1 << 20  # 16 row bands: H2D of band k+1 and D2H of band k-1 overlap band k
 
     def spec(self):
         return self.W.gaussian_spec(self.WIDTH, self.HEIGHT, self.F)
