@@ -349,7 +349,7 @@ struct Engine::Impl {
     try {
       done = co_execute(resident ? std::span<void* const>() : outputs, 0, tally);
     } catch (...) {
-      inputs_streaming = false;
+      abandon_streamed_inputs();
       throw;
     }
     inputs_streaming = false;
@@ -384,6 +384,16 @@ struct Engine::Impl {
 
   // Run start: clock epoch, tally reset, one H2D into the first device and an
   // NVLink doubling tree to the others (ecl_replicate_inputs).
+  // A run that failed while its inputs were still streaming: finish the
+  // uploads while the caller's buffers are still valid (we are inside the
+  // run call), and stop treating the device copies as resident.
+  void abandon_streamed_inputs() {
+    if (inputs_streaming)
+      for (auto& d : devices) (void)ecl_gpu_sync(d->gpu);
+    inputs_streaming = false;
+    inputs_resident = false;
+  }
+
   bool begin_run(std::span<const void* const> inputs) {
     epoch = Clock::now();
     const bool tally = cfg.tally || tally_from_env();
@@ -483,7 +493,7 @@ struct Engine::Impl {
       try {
         step = co_execute({}, all.size(), tally);
       } catch (...) {
-        inputs_streaming = false;
+        abandon_streamed_inputs();
         throw;
       }
       inputs_streaming = false;  // streamed up during the first step
