@@ -388,10 +388,11 @@ struct Engine::Impl {
   // uploads while the caller's buffers are still valid (we are inside the
   // run call), and stop treating the device copies as resident.
   void abandon_streamed_inputs() {
-    if (inputs_streaming)
+    if (inputs_streaming) {
       for (auto& d : devices) (void)ecl_gpu_sync(d->gpu);
+      inputs_resident = false;
+    }
     inputs_streaming = false;
-    inputs_resident = false;
   }
 
   bool begin_run(std::span<const void* const> inputs) {
