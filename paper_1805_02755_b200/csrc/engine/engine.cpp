@@ -198,7 +198,10 @@ struct Engine::Impl {
     }
     // One device in this process: stream its inputs up piece by piece so
     // the H2D overlaps the first packages (replication needs them whole).
-    if (devices.size() == 1 && !shared) check(ecl_gpu_set_streamed_inputs(devices[0]->gpu, 1), "streamed inputs");
+    // (ECL_NO_STREAMED_INPUTS=1 turns it off, e.g. so a profiler sees whole-package launches.)
+    const char* no_stream = std::getenv("ECL_NO_STREAMED_INPUTS");
+    if (devices.size() == 1 && !shared && !(no_stream && std::string_view(no_stream) == "1"))
+      check(ecl_gpu_set_streamed_inputs(devices[0]->gpu, 1), "streamed inputs");
     for (auto& d : devices) d->thread = std::thread([this, dev = d.get()] { device_loop(*dev); });
   }
 

@@ -210,3 +210,38 @@ def test_gaussian_filters_of_two_live_engines_do_not_mix(gpu_available, oracle):
     finally:
         for e in engines:
             e.close()
+
+
+@pytest.mark.parametrize("split", [1000, 5 * 640 + 17, 1 << 20])
+def test_gaussian_streamed_inputs_single_device(gpu_available, oracle, split):
+    # one device: the image streams up per piece (rows + 15-row halo ahead of
+    # each piece); pieces of arbitrary size start mid-row
+    w, h, f = 640, 200, 31
+    img, filt = W.gaussian_inputs(w, h, f, seed=9)
+    prog = P.validate_program(W.gaussian_spec(w, h, f))
+    devs = [P.cuda_device("gpu0", 0, copy_split_items=split)]
+    out = P.PinnedBuffer(w * h * 4, np.float32)
+    try:
+        with P.Engine(P.EngineConfig(devs, P.DynamicConfig(7)), prog) as e:
+            e.run_into([img, filt], [out.array])
+            ok, worst = rel_close(out.array.copy(), oracle.gaussian(img, filt, w, h, f), 1e-5)
+            assert ok, worst
+            # device-resident rerun on the streamed-up inputs
+            e.run_into(None, None)
+            res = np.zeros(w * h, np.float32)
+            e.gather([res])
+            ok, worst = rel_close(res, oracle.gaussian(img, filt, w, h, f), 1e-5)
+            assert ok, worst
+    finally:
+        out.free()
+
+
+def test_binomial_streamed_inputs_single_device(gpu_available, oracle):
+    options, steps = 4 * 3000, 254
+    rand = W.binomial_inputs(options, seed=13)[0]
+    prog = P.validate_program(W.binomial_spec(options, steps))
+    devs = [P.cuda_device("gpu0", 0, copy_split_items=255 * 97)]
+    with P.Engine(P.EngineConfig(devs, P.HGuidedConfig()), prog) as e:
+        res = e.run([rand])
+    ok, worst = rel_close(res.outputs[0].view(np.float32), oracle.binomial(rand, steps), 1e-5, atol=1e-6)
+    assert ok, worst

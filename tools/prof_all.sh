@@ -1,6 +1,7 @@
 # ncu --set full capture of one launch of every hot kernel (each after the
 # same command ran clean without ncu); summaries -> profiles/<round>/.
 set -x
+export ECL_NO_STREAMED_INPUTS=1  # whole-package launches, as in the timed resident runs
 cap() {  # workload kernel-regex extra-args
   python tools/profile_run.py --workload $1 $3 > gpurun_out/plain_$1.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:$2 -s 1 -c 1 -o gpurun_out/ncu_$1 \
