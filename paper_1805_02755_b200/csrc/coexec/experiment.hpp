@@ -76,8 +76,9 @@ ExperimentConfig experiment_from_json(const json& j, const std::filesystem::path
 std::vector<DeviceProfile> load_device_profiles(const std::filesystem::path& path);
 
 /// Reference input recipe (workloads.hpp:261-283): splitmix64(seed) doubles
-/// in [0,1) for 8-byte elements, random bytes otherwise.  B200 addition:
-/// 4- and 16-byte elements (f32 / float4 kernels) get floats in [0,1).
+/// in [0,1) for 8-byte elements, random bytes otherwise.  B200 additions:
+/// 4- and 16-byte elements (f32 / float4 kernels) get floats in [0,1), and
+/// Gaussian's filter is a normalized Gaussian with sigma = F/6.
 std::vector<std::vector<std::byte>> fill_default_inputs(const ValidatedProgram& prog, std::uint64_t seed);
 
 /// Per-work-item virtual-clock costs (reference cost model,

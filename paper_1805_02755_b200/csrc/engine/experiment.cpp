@@ -4,6 +4,7 @@
 #include "coexec/experiment.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -168,7 +169,28 @@ ExperimentConfig load_experiment(const std::filesystem::path& path) {
 std::vector<std::vector<std::byte>> fill_default_inputs(const ValidatedProgram& prog, std::uint64_t seed) {
   std::vector<std::vector<std::byte>> inputs;
   std::uint64_t state = seed;  // one stream across buffers, in buffer order
-  for (const BufferDesc& b : prog.spec().in_buffers) {
+  const ProgramSpec& spec = prog.spec();
+  for (std::size_t bi = 0; bi < spec.in_buffers.size(); ++bi) {
+    const BufferDesc& b = spec.in_buffers[bi];
+    if (spec.kernel == "gaussian" && bi == 1 && b.element_size_bytes == 4) {
+      // the filter: a normalized Gaussian, sigma = F/6 (F = 31 -> 5, the paper's config)
+      const std::uint64_t f = static_cast<std::uint64_t>(std::llround(std::sqrt(double(b.element_count))));
+      std::vector<std::byte> bytes(b.size_bytes());
+      std::vector<double> w(b.element_count);
+      const double sigma = double(f) / 6.0, r = double(f / 2);
+      double sum = 0;
+      for (std::uint64_t i = 0; i < b.element_count; ++i) {
+        const double y = double(i / f) - r, x = double(i % f) - r;
+        w[i] = std::exp(-(x * x + y * y) / (2 * sigma * sigma));
+        sum += w[i];
+      }
+      for (std::uint64_t i = 0; i < b.element_count; ++i) {
+        const float v = static_cast<float>(w[i] / sum);
+        std::memcpy(bytes.data() + 4 * i, &v, 4);
+      }
+      inputs.push_back(std::move(bytes));
+      continue;
+    }
     std::vector<std::byte> bytes(b.size_bytes());
     if (b.element_size_bytes == 8) {
       for (std::uint64_t i = 0; i < b.element_count; ++i) {
