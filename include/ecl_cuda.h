@@ -129,7 +129,9 @@ int ecl_gpu_download_slice(ecl_gpu* gpu, uint32_t index, uint64_t elem_offset, u
                            void* host_dst);
 int ecl_host_register(void* ptr, size_t bytes);
 int ecl_host_unregister(void* ptr);
-/* Page-locked host allocation (cudaHostAlloc, portable across devices). */
+/* Page-locked host allocation, portable across devices: anonymous memory on
+ * transparent huge pages registered with CUDA (falls back to cudaHostAlloc);
+ * release with ecl_host_free. */
 int ecl_host_alloc(size_t bytes, void** ptr);
 int ecl_host_free(void* ptr);
 
