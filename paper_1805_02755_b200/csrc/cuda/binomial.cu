@@ -40,9 +40,14 @@ __device__ __forceinline__ float lattice_step(float w, float w1, float r) { retu
 __device__ __forceinline__ float2 lattice_step(float2 w, float2 w1, float2 r) { return __ffma2_rn(r, w1, w); }
 __device__ __forceinline__ float rescale(float w, float s) { return w * s; }
 __device__ __forceinline__ float2 rescale(float2 w, float2 s) { return __fmul2_rn(w, s); }
-__device__ __forceinline__ float shfl_down1(float v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+// Next lane's value within lane groups of G (a warp, or a half-warp).
+template <int G>
+__device__ __forceinline__ float shfl_down1(float v) {
+  return __shfl_down_sync(0xffffffffu, v, 1, G);
+}
+template <int G>
 __device__ __forceinline__ float2 shfl_down1(float2 v) {
-  return make_float2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
+  return make_float2(__shfl_down_sync(0xffffffffu, v.x, 1, G), __shfl_down_sync(0xffffffffu, v.y, 1, G));
 }
 __device__ __forceinline__ float shfl_from(float v, unsigned src) { return __shfl_sync(0xffffffffu, v, src); }
 __device__ __forceinline__ float2 shfl_from(float2 v, unsigned src) {
@@ -53,11 +58,11 @@ __device__ __forceinline__ float2 shfl_from(float2 v, unsigned src) {
 // holds nodes NL*l .. NL*l+NL-1): w[t] <- w[t] + r*w[t+1].  The neighbour of
 // a lane's last node is the next lane's first (one shuffle).  Returns the
 // next j.
-template <int NL, typename V>
+template <int G, int NL, typename V>
 __device__ __forceinline__ int backward(V (&c)[NL], int j, int stop, V r) {
 #pragma unroll 8
   for (; j > stop; --j) {
-    const V right = shfl_down1(c[0]);
+    const V right = shfl_down1<G>(c[0]);
 #pragma unroll
     for (int k = 0; k < NL - 1; ++k) c[k] = lattice_step(c[k], c[k + 1], r);
     c[NL - 1] = lattice_step(c[NL - 1], right, r);
@@ -66,20 +71,21 @@ __device__ __forceinline__ int backward(V (&c)[NL], int j, int stop, V r) {
 }
 
 // The live lattice (nodes 0..j at level j) shrinks by one node per step, so
-// the levels run in phases of 32: phase NL keeps NL nodes per lane until the
-// live nodes fit in 32*(NL-1), then the lattice is rescaled by pd^32 (w stays
-// within pd^-32 of the true value: no f32 overflow) and repacked to NL-1
-// nodes per lane through a warp-private shared-memory buffer.  Phases above
-// ceil((steps+1)/32) run no steps and neither rescale nor repack anything
-// that matters.  Slots beyond the live nodes carry don't-care values.
-template <int NL, typename V>
-__device__ __forceinline__ V phases(V (&c)[NL], int j, V r, V s32, V* buf, unsigned lane) {
-  const int stop = NL > 1 ? 32 * (NL - 1) - 1 : 0;
+// the levels run in phases of G (the lane-group width): phase NL keeps NL
+// nodes per lane until the live nodes fit in G*(NL-1), then the lattice is
+// rescaled by pd^G (w stays within pd^-G of the true value: no f32
+// overflow) and repacked to NL-1 nodes per lane through the group's private
+// shared-memory buffer.  Phases above ceil((steps+1)/G) run no steps and
+// neither rescale nor repack anything that matters.  Slots beyond the live
+// nodes carry don't-care values.  `lane` is the lane within its group.
+template <int G, int NL, typename V>
+__device__ __forceinline__ V phases(V (&c)[NL], int j, V r, V s, V* buf, unsigned lane) {
+  const int stop = NL > 1 ? G * (NL - 1) - 1 : 0;
   if (j > stop) {
-    j = backward<NL>(c, j, stop, r);
+    j = backward<G, NL>(c, j, stop, r);
     if constexpr (NL > 1) {
 #pragma unroll
-      for (int k = 0; k < NL; ++k) c[k] = rescale(c[k], s32);
+      for (int k = 0; k < NL; ++k) c[k] = rescale(c[k], s);
     }
   }
   if constexpr (NL == 1) {
@@ -92,7 +98,7 @@ __device__ __forceinline__ V phases(V (&c)[NL], int j, V r, V s32, V* buf, unsig
 #pragma unroll
     for (int k = 0; k < NL - 1; ++k) h[k] = buf[(NL - 1) * lane + k];
     __syncwarp();
-    return phases<NL - 1>(h, j, r, s32, buf, lane);
+    return phases<G, NL - 1>(h, j, r, s, buf, lane);
   }
 }
 
@@ -108,11 +114,13 @@ __device__ __forceinline__ double upow(double x, int e) {
 // from the uniform r, dt = T/steps, u = exp(sigma sqrt(dt)),
 // pu = (a - d)/(u - d)), reduced to what the leaves and the lattice need.
 struct Option {
-  double K, base, f16, u2;  // leaf of node t = 16 l + k: base * f16^l * u2^k - K
-  float r, s32;             // pu/pd and pd^32 (the scaled lattice's step and rescale factors)
-  double tail;              // pd^(steps - 32 R) * exp(-R T) / q^R: undoes the remaining scale, discounts
+  double K, base, f, u2;  // leaf of node t = NL l + k: base * f^l * u2^k - K  (f = u^(2 NL))
+  float r, s;             // pu/pd and pd^G (the scaled lattice's step and rescale factors)
+  double tail;            // pd^(steps - G R) * exp(-R T) / q^R: undoes the remaining scale, discounts
 };
 
+// G = lane-group width (phase length in levels), NL = nodes per lane at the leaves.
+template <int G, int NL>
 __device__ __forceinline__ Option option_params(double rv, int steps) {
   Option o;
   const double S = 5.0 * (1.0 - rv) + 30.0 * rv;
@@ -125,17 +133,17 @@ __device__ __forceinline__ Option option_params(double rv, int steps) {
   const double d = 1.0 / u;
   const double pu = (a - d) / (u - d), pd = 1.0 - pu;
   o.r = static_cast<float>(pu / pd);
-  const double p32 = upow(pd, 32);
-  o.s32 = static_cast<float>(p32);
-  // R rescales by the f32-rounded pd^32; q is that rounding's factor.
-  const int rescales = steps / 32;  // = ceil((steps + 1) / 32) - 1 phase boundaries
-  const double q = static_cast<double>(o.s32) / p32;
-  o.tail = upow(pd, steps - 32 * rescales) * exp(-0.02 * T) / upow(q, rescales);
-  // S*exp(vsdt*(2t - steps)) = S*exp(-vsdt*steps) * (u^16)^l * (u^2)^k:
+  const double pg = upow(pd, G);
+  o.s = static_cast<float>(pg);
+  // R rescales by the f32-rounded pd^G; q is that rounding's factor.
+  const int rescales = steps / G;  // = ceil((steps + 1) / G) - 1 phase boundaries
+  const double q = static_cast<double>(o.s) / pg;
+  o.tail = upow(pd, steps - G * rescales) * exp(-0.02 * T) / upow(q, rescales);
+  // S*exp(vsdt*(2t - steps)) = S*exp(-vsdt*steps) * (u^(2 NL))^l * (u^2)^k:
   // one exp per option instead of one per lane.
   o.base = S * exp(-vsdt * static_cast<double>(steps));
   o.u2 = u * u;
-  o.f16 = upow(o.u2, 8);
+  o.f = upow(o.u2, NL);
   return o;
 }
 
@@ -146,16 +154,17 @@ __device__ __forceinline__ Option option_params(double rv, int steps) {
 // every level that is a multiple of 32; `tail` undoes the rest.  The lane's
 // first leaf price is base * f16^lane (lane-divergent square-and-multiply
 // with selects), then successive factors u^2 (~1e-15 relative drift).
-__device__ __forceinline__ void leaves(const Option& o, int steps, unsigned lane, float (&c)[kNodesPerLane]) {
-  double st = o.base, f = o.f16;
+template <int NL>
+__device__ __forceinline__ void leaves(const Option& o, int steps, unsigned lane, float (&c)[NL]) {
+  double st = o.base, f = o.f;
 #pragma unroll
   for (int bit = 0; bit < 5; ++bit, f *= f) {
     const double m = st * f;
     st = ((lane >> bit) & 1u) ? m : st;
   }
 #pragma unroll
-  for (int k = 0; k < kNodesPerLane; ++k) {
-    const int t = static_cast<int>(lane) * kNodesPerLane + k;
+  for (int k = 0; k < NL; ++k) {
+    const int t = static_cast<int>(lane) * NL + k;
     const double leaf = st - o.K;
     c[k] = (t <= steps && leaf > 0.0) ? static_cast<float>(leaf) : 0.0f;
     st *= o.u2;
@@ -167,17 +176,17 @@ __device__ __forceinline__ Option shfl_option(const Option& x, int src) {
   Option o;
   o.K = __shfl_sync(0xffffffffu, x.K, src);
   o.base = __shfl_sync(0xffffffffu, x.base, src);
-  o.f16 = __shfl_sync(0xffffffffu, x.f16, src);
+  o.f = __shfl_sync(0xffffffffu, x.f, src);
   o.u2 = __shfl_sync(0xffffffffu, x.u2, src);
   o.r = __shfl_sync(0xffffffffu, x.r, src);
-  o.s32 = __shfl_sync(0xffffffffu, x.s32, src);
+  o.s = __shfl_sync(0xffffffffu, x.s, src);
   o.tail = __shfl_sync(0xffffffffu, x.tail, src);
   return o;
 }
 
 template <typename V>
 __device__ __forceinline__ V lattice(V (&c)[kNodesPerLane], int steps, V r, V s32, V* buf, unsigned lane) {
-  return phases<kNodesPerLane>(c, steps, r, s32, buf, lane);
+  return phases<32, kNodesPerLane>(c, steps, r, s32, buf, lane);
 }
 
 // P = options per warp (1: scalar lattice, 2: two options packed per lane).
@@ -195,10 +204,10 @@ __global__ void __launch_bounds__(kThreads, MB)
        w += warps) {
     const uint64_t o = first_opt + w * P;
     if constexpr (P == 1) {
-      const Option a = option_params(rand[o], steps);
+      const Option a = option_params<32, kNodesPerLane>(rand[o], steps);
       float c[kNodesPerLane];
-      leaves(a, steps, lane, c);
-      const float v = lattice(c, steps, a.r, a.s32, buf, lane);
+      leaves<kNodesPerLane>(a, steps, lane, c);
+      const float v = lattice(c, steps, a.r, a.s, buf, lane);
       if (lane == 0) out[o] = static_cast<float>(static_cast<double>(v) * a.tail);
     } else {
       const bool has_b = w * P + 1 < n_opt;
@@ -206,25 +215,25 @@ __global__ void __launch_bounds__(kThreads, MB)
       double tail_a, tail_b;
       // Lanes 0-15 set up option A, lanes 16-31 option B (one pass of the
       // FP64 setup for both), then each half's result is broadcast.
-      const Option mine = option_params(rand[o + ((lane >> 4) != 0u && has_b ? 1 : 0)], steps);
+      const Option mine = option_params<32, kNodesPerLane>(rand[o + ((lane >> 4) != 0u && has_b ? 1 : 0)], steps);
       {
         const Option a = shfl_option(mine, 0);
         float ca[kNodesPerLane];
-        leaves(a, steps, lane, ca);
+        leaves<kNodesPerLane>(a, steps, lane, ca);
 #pragma unroll
         for (int k = 0; k < kNodesPerLane; ++k) c[k].x = ca[k];
         r.x = a.r;
-        s32.x = a.s32;
+        s32.x = a.s;
         tail_a = a.tail;
       }
       {
         const Option b = shfl_option(mine, 16);
         float cb[kNodesPerLane];
-        leaves(b, steps, lane, cb);
+        leaves<kNodesPerLane>(b, steps, lane, cb);
 #pragma unroll
         for (int k = 0; k < kNodesPerLane; ++k) c[k].y = cb[k];
         r.y = b.r;
-        s32.y = b.s32;
+        s32.y = b.s;
         tail_b = b.tail;
       }
       const float2 v = lattice(c, steps, r, s32, buf, lane);
@@ -234,6 +243,63 @@ __global__ void __launch_bounds__(kThreads, MB)
       }
     }
   }
+}
+
+// Four options per warp: each half-warp carries an option pair packed in
+// float2, 16 nodes per lane (16 x 16 = 256 >= steps + 1).  Per lattice level
+// a warp issues 16 FFMA2 (for 4 options) and 2 shuffles: shuffles per option
+// halve against binomial_warp<2>, whose 2 shuffles per 8 FFMA2 co-limit
+// with the FMA pipe (SHFL runs at one warp instruction per cycle per SM,
+// tools/probe/shfl_tp.cu).  Phases are 16 levels long (rescale by pd^16).
+// Measured 18.3 ms vs 17.2 ms for binomial_warp<2> at the config, so it is
+// the "binomial@2" variant, not the default: shuffles were not the binding
+// limit.
+constexpr int kHalf = 16, kHalfNodes = 16;
+
+template <int MB>
+__global__ void __launch_bounds__(kThreads, MB)
+    binomial_half(const float* __restrict__ rand, float* __restrict__ out, int steps, uint64_t first_opt,
+                  uint64_t n_opt) {
+  __shared__ float2 repack_buf[kThreads / kHalf][kHalf * kHalfNodes];
+  const unsigned lane = threadIdx.x & 31u, half = lane >> 4, lh = lane & 15u;
+  float2* const buf = repack_buf[threadIdx.x >> 4];
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (kThreads / 32);
+  const uint64_t groups = (n_opt + 3) / 4;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(kThreads / 32) + (threadIdx.x >> 5); w < groups;
+       w += warps) {
+    const uint64_t o = first_opt + w * 4;
+    const uint64_t left = first_opt + n_opt - o;  // options of this group that exist (>= 1)
+    // Lanes 8q..8q+7 set up option o+q; half h then takes options 2h, 2h+1.
+    const unsigned q = lane >> 3;
+    const Option mine = option_params<kHalf, kHalfNodes>(rand[o + (q < left ? q : 0)], steps);
+    const Option a = shfl_option(mine, static_cast<int>(16 * half));
+    const Option b = shfl_option(mine, static_cast<int>(16 * half + 8));
+    float ca[kHalfNodes], cb[kHalfNodes];
+    leaves<kHalfNodes>(a, steps, lh, ca);
+    leaves<kHalfNodes>(b, steps, lh, cb);
+    float2 c[kHalfNodes];
+#pragma unroll
+    for (int k = 0; k < kHalfNodes; ++k) c[k] = make_float2(ca[k], cb[k]);
+    const float2 v = phases<kHalf, kHalfNodes>(c, steps, make_float2(a.r, b.r), make_float2(a.s, b.s), buf, lh);
+    if (lh == 0) {
+      const uint64_t i = 2 * half;
+      if (i < left) out[o + i] = static_cast<float>(static_cast<double>(v.x) * a.tail);
+      if (i + 1 < left) out[o + i + 1] = static_cast<float>(static_cast<double>(v.y) * b.tail);
+    }
+  }
+}
+
+template <int MB>
+cudaError_t launch_half(const KernelSpec& spec, const LaunchEnv& env, uint64_t first_opt, uint64_t n_opt) {
+  const uint64_t warps_per_block = kThreads / 32;
+  const uint64_t groups = (n_opt + 3) / 4;
+  uint64_t blocks = (groups + warps_per_block - 1) / warps_per_block;
+  const uint64_t cap = static_cast<uint64_t>(env.sms) * 8 * 16;
+  if (blocks > cap) blocks = cap;
+  binomial_half<MB><<<static_cast<unsigned>(blocks), kThreads, 0, env.stream>>>(
+      static_cast<const float*>(env.in[0]), static_cast<float*>(env.out[0]), static_cast<int>(spec.binom.steps),
+      first_opt, n_opt);
+  return cudaGetLastError();
 }
 
 template <int P, int MB>
@@ -266,6 +332,13 @@ cudaError_t launch_binomial(const KernelSpec& spec, const LaunchEnv& env, uint64
     return v ? std::atoi(v) : 0;
   }();
   if (variant == 1) return launch<1, 4>(spec, env, first_opt, n_opt);
+  if (variant == 2) {
+    switch (mb) {
+      case 2: return launch_half<2>(spec, env, first_opt, n_opt);
+      case 4: return launch_half<4>(spec, env, first_opt, n_opt);
+      default: return launch_half<3>(spec, env, first_opt, n_opt);
+    }
+  }
   switch (mb) {  // measured: 4 (52 registers) 18.8 ms, 5 19.1 ms, 6 19.2 ms
     case 5: return launch<2, 5>(spec, env, first_opt, n_opt);
     case 6: return launch<2, 6>(spec, env, first_opt, n_opt);
