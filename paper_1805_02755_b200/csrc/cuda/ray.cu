@@ -95,14 +95,37 @@ struct Lane {
   uint32_t depth, bounces;
 };
 
+// Shadow rays of one warp's bounce, compacted: lanes write the geometry of
+// their up to 3 light rays (direction, distance) and their hit point; the
+// (lane, light) pairs that need a shadow test are queued and the warp then
+// tests them 32 at a time, so lanes whose pixel missed or faces away from a
+// light do not idle through other lanes' shadow loops.  Only scheduling
+// changes: every shadow test and shading term is the same arithmetic.
+struct ShadowQueue {
+  float4 ray[32][3];   // (ln.x, ln.y, ln.z, dist) per lane and light
+  float4 point[32];    // hit point p per lane
+  uint32_t entry[96];  // (lane << 2) | light
+  uint8_t shadowed[32][4];
+};
+
+size_t ray_smem_bytes(uint32_t ns) {
+  return sizeof(float4) * (2 * static_cast<size_t>(ns) + 2 * ((ns + 1) / 2)) +
+         sizeof(ShadowQueue) * (kThreads / 32);
+}
+
 template <int MB>
 __global__ void __launch_bounds__(kThreads, MB)
     ray_persistent(const float4* __restrict__ scene, uint32_t ns, uint32_t w, uint32_t h, uint32_t max_depth,
                    float4* __restrict__ out, uint64_t first, uint64_t count, unsigned* __restrict__ ctrl) {
-  __shared__ float4 sph[kMaxSpheres], mat[kMaxSpheres];
-  // Sphere pairs as two 16-byte records: (x0, x1, y0, y1), (z0, z1, r0^2, r1^2),
-  // so a pair test reads 2 LDS.128 off one pointer (packed operands aligned).
-  __shared__ float4 pair_rec[kMaxSpheres / 2][2];
+  // Dynamic shared memory (ray_smem_bytes): spheres, materials, sphere-pair
+  // records, then one ShadowQueue per warp.  Pair records are two 16-byte
+  // records (x0, x1, y0, y1), (z0, z1, r0^2, r1^2), so a pair test reads two
+  // LDS.128 off one pointer (packed operands aligned).
+  extern __shared__ float4 smem[];
+  float4* const sph = smem;
+  float4* const mat = smem + ns;
+  float4 (*const pair_rec)[2] = reinterpret_cast<float4 (*)[2]>(smem + 2 * ns);
+  ShadowQueue* const sq = reinterpret_cast<ShadowQueue*>(smem + 2 * ns + 2 * ((ns + 1) / 2)) + (threadIdx.x >> 5);
   for (uint32_t i = threadIdx.x; i < ns; i += kThreads) {
     const float4 c = scene[i];
     sph[i] = c;
@@ -175,6 +198,10 @@ __global__ void __launch_bounds__(kThreads, MB)
     if (!__any_sync(kFull, valid)) break;
 
     bool finished = !valid;
+    bool lit = false;  // hit a surface this bounce: shade it
+    V3 p{0.0f, 0.0f, 0.0f}, n{0.0f, 0.0f, 0.0f};
+    float cr = 0.0f, cg = 0.0f, cb = 0.0f, refl = 0.0f;
+    float ndl[3] = {0.0f, 0.0f, 0.0f};
     if (valid) {
       // ---- one bounce (oracle: trace_pixel loop body) ----
       float tmin = 1e30f;
@@ -212,9 +239,8 @@ __global__ void __launch_bounds__(kThreads, MB)
         L.b = add(L.b, mul(L.weight, sky.z));
         finished = true;
       } else {
-        const V3 p{add(L.o.x, mul(tmin, L.d.x)), add(L.o.y, mul(tmin, L.d.y)), add(L.o.z, mul(tmin, L.d.z))};
-        V3 n;
-        float cr, cg, cb, refl;
+        lit = true;
+        p = V3{add(L.o.x, mul(tmin, L.d.x)), add(L.o.y, mul(tmin, L.d.y)), add(L.o.z, mul(tmin, L.d.z))};
         if (hit < static_cast<int>(ns)) {
           const float4 c = sph[hit], m = mat[hit];
           n = vnorm(vsub(p, V3{c.x, c.y, c.z}));
@@ -231,55 +257,89 @@ __global__ void __launch_bounds__(kThreads, MB)
           cb = mul(pmat.z, k);
           refl = pmat.w;
         }
-        float lr = mul(shading.x, cr), lg = mul(shading.x, cg), lb = mul(shading.x, cb);
+        sq->point[lane_id] = make_float4(p.x, p.y, p.z, 0.0f);
 #pragma unroll
         for (int l = 0; l < 3; ++l) {
           const V3 Lv = vsub(V3{lights[l].x, lights[l].y, lights[l].z}, p);
           const float dist = __fsqrt_rn(vdot(Lv, Lv));
           const V3 ln{dvd(Lv.x, dist), dvd(Lv.y, dist), dvd(Lv.z, dist)};
-          const float ndl = vdot(n, ln);
-          if (ndl <= 0.0f) continue;
-          bool shadow = false;
-          for (uint32_t s = 0; s < pairs_end && !shadow; s += 2) {
-            const float4 r0 = pair_rec[s / 2][0], r1 = pair_rec[s / 2][1];
-            const float2 t = ray_sphere2(p, ln, make_float2(r0.x, r0.y), make_float2(r0.z, r0.w),
-                                         make_float2(r1.x, r1.y), make_float2(r1.z, r1.w));
-            shadow = (t.x > 0.0f && t.x < dist) || (t.y > 0.0f && t.y < dist);
-          }
-          if (!shadow && pairs_end < ns) {
-            const float t = ray_sphere(p, ln, sph[pairs_end]);
-            shadow = t > 0.0f && t < dist;
-          }
-          if (shadow) continue;
-          const float two_ndl = mul(2.0f, ndl);
-          const V3 rl{sub(mul(two_ndl, n.x), ln.x), sub(mul(two_ndl, n.y), ln.y), sub(mul(two_ndl, n.z), ln.z)};
-          float sp = -add(add(mul(rl.x, L.d.x), mul(rl.y, L.d.y)), mul(rl.z, L.d.z));
-          sp = sp > 0.0f ? sp : 0.0f;
-          sp = mul(sp, sp);
-          sp = mul(sp, sp);
-          sp = mul(sp, sp);
-          sp = mul(sp, sp);
-          const float I = lights[l].w;
-          lr = add(lr, mul(I, add(mul(cr, ndl), mul(shading.y, sp))));
-          lg = add(lg, mul(I, add(mul(cg, ndl), mul(shading.y, sp))));
-          lb = add(lb, mul(I, add(mul(cb, ndl), mul(shading.y, sp))));
-        }
-        const float keep = mul(L.weight, sub(1.0f, refl));
-        L.r = add(L.r, mul(keep, lr));
-        L.g = add(L.g, mul(keep, lg));
-        L.b = add(L.b, mul(keep, lb));
-        L.bounces = L.depth + 1;
-        L.weight = mul(L.weight, refl);
-        if (!(refl > 0.0f) || L.weight < 1e-3f || L.depth + 1 > max_depth) {
-          finished = true;
-        } else {
-          const float two_dn = mul(2.0f, vdot(L.d, n));
-          L.d = V3{sub(L.d.x, mul(two_dn, n.x)), sub(L.d.y, mul(two_dn, n.y)), sub(L.d.z, mul(two_dn, n.z))};
-          L.o = p;
-          L.depth += 1;
+          ndl[l] = vdot(n, ln);
+          sq->ray[lane_id][l] = make_float4(ln.x, ln.y, ln.z, dist);
         }
       }
     }
+
+    // ---- shadow rays of the whole warp, compacted (all lanes converged) ----
+    __syncwarp();
+    unsigned queued = 0;
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      const bool need = lit && ndl[l] > 0.0f;
+      const unsigned m = __ballot_sync(kFull, need);
+      if (need) sq->entry[queued + __popc(m & below)] = (lane_id << 2) | static_cast<unsigned>(l);
+      queued += __popc(m);
+    }
+    __syncwarp();
+    for (unsigned base = 0; base < queued; base += 32) {
+      const unsigned e = base + lane_id;
+      if (e < queued) {
+        const unsigned code = sq->entry[e], owner = code >> 2, l = code & 3u;
+        const float4 g = sq->ray[owner][l], pp = sq->point[owner];
+        const V3 po{pp.x, pp.y, pp.z}, ln{g.x, g.y, g.z};
+        const float dist = g.w;
+        bool shadow = false;
+        for (uint32_t s = 0; s < pairs_end && !shadow; s += 2) {
+          const float4 r0 = pair_rec[s / 2][0], r1 = pair_rec[s / 2][1];
+          const float2 t = ray_sphere2(po, ln, make_float2(r0.x, r0.y), make_float2(r0.z, r0.w),
+                                       make_float2(r1.x, r1.y), make_float2(r1.z, r1.w));
+          shadow = (t.x > 0.0f && t.x < dist) || (t.y > 0.0f && t.y < dist);
+        }
+        if (!shadow && pairs_end < ns) {
+          const float t = ray_sphere(po, ln, sph[pairs_end]);
+          shadow = t > 0.0f && t < dist;
+        }
+        sq->shadowed[owner][l] = shadow ? 1 : 0;
+      }
+    }
+    __syncwarp();
+
+    if (lit) {
+      float lr = mul(shading.x, cr), lg = mul(shading.x, cg), lb = mul(shading.x, cb);
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        if (ndl[l] <= 0.0f) continue;
+        if (sq->shadowed[lane_id][l]) continue;
+        const float4 g = sq->ray[lane_id][l];
+        const V3 ln{g.x, g.y, g.z};
+        const float two_ndl = mul(2.0f, ndl[l]);
+        const V3 rl{sub(mul(two_ndl, n.x), ln.x), sub(mul(two_ndl, n.y), ln.y), sub(mul(two_ndl, n.z), ln.z)};
+        float sp = -add(add(mul(rl.x, L.d.x), mul(rl.y, L.d.y)), mul(rl.z, L.d.z));
+        sp = sp > 0.0f ? sp : 0.0f;
+        sp = mul(sp, sp);
+        sp = mul(sp, sp);
+        sp = mul(sp, sp);
+        sp = mul(sp, sp);
+        const float I = lights[l].w;
+        lr = add(lr, mul(I, add(mul(cr, ndl[l]), mul(shading.y, sp))));
+        lg = add(lg, mul(I, add(mul(cg, ndl[l]), mul(shading.y, sp))));
+        lb = add(lb, mul(I, add(mul(cb, ndl[l]), mul(shading.y, sp))));
+      }
+      const float keep = mul(L.weight, sub(1.0f, refl));
+      L.r = add(L.r, mul(keep, lr));
+      L.g = add(L.g, mul(keep, lg));
+      L.b = add(L.b, mul(keep, lb));
+      L.bounces = L.depth + 1;
+      L.weight = mul(L.weight, refl);
+      if (!(refl > 0.0f) || L.weight < 1e-3f || L.depth + 1 > max_depth) {
+        finished = true;
+      } else {
+        const float two_dn = mul(2.0f, vdot(L.d, n));
+        L.d = V3{sub(L.d.x, mul(two_dn, n.x)), sub(L.d.y, mul(two_dn, n.y)), sub(L.d.z, mul(two_dn, n.z))};
+        L.o = p;
+        L.depth += 1;
+      }
+    }
+    __syncwarp();  // the queue is rewritten next bounce
     if (valid && finished) {
       out[idx] = make_float4(L.r, L.g, L.b, static_cast<float>(L.bounces));
       valid = false;
@@ -301,7 +361,8 @@ template <int MB>
 cudaError_t launch(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
   static int blocks_per_sm = 0;
   if (blocks_per_sm == 0) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ray_persistent<MB>, kThreads, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ray_persistent<MB>, kThreads,
+                                                                  ray_smem_bytes(spec.ray.spheres));
     if (e != cudaSuccess) return e;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
@@ -309,7 +370,13 @@ cudaError_t launch(const KernelSpec& spec, const LaunchEnv& env, uint64_t first,
   const uint64_t blocks_needed = (chunks + kThreads / 32 - 1) / (kThreads / 32);
   uint64_t grid = static_cast<uint64_t>(env.sms) * static_cast<uint64_t>(blocks_per_sm);
   if (blocks_needed < grid) grid = blocks_needed;
-  ray_persistent<MB><<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
+  const size_t smem = ray_smem_bytes(spec.ray.spheres);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(ray_persistent<MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  ray_persistent<MB><<<static_cast<unsigned>(grid), kThreads, smem, env.stream>>>(
       static_cast<const float4*>(env.in[0]), spec.ray.spheres, spec.ray.width, spec.ray.height, spec.ray.max_depth,
       static_cast<float4*>(env.out[0]), first, count, env.ctrl);
   return cudaGetLastError();
