@@ -72,12 +72,16 @@ def test_nbody_one_and_two_bodies(gpu_available, oracle):
         assert rel_ok(res.outputs[1].view(np.float32).reshape(-1, 4), nvel, 1e-4, atol=1e-6)
 
 
-@pytest.mark.parametrize("steps", [1, 2, 31, 32, 33, 63, 64, 255])
-def test_binomial_depth_edges(gpu_available, oracle, steps):
-    # phase boundaries of the lattice (multiples of 32 levels) and the
-    # maximum depth; 4 options = one work-group
+@pytest.mark.parametrize("kernel", ["binomial", "binomial@1", "binomial@2"])
+@pytest.mark.parametrize("steps", [1, 2, 15, 16, 17, 31, 32, 33, 63, 64, 255])
+def test_binomial_depth_edges(gpu_available, oracle, steps, kernel):
+    # phase boundaries of the lattices (multiples of 32 levels for the warp
+    # kernels, 16 for the half-warp variant @2) and the maximum depth;
+    # 4 options = one work-group
     rand = W.binomial_inputs(4, seed=steps)[0]
-    res = run(W.binomial_spec(4, steps), [rand])
+    spec = W.binomial_spec(4, steps)
+    spec.kernel = kernel
+    res = run(spec, [rand])
     assert rel_ok(res.outputs[0].view(np.float32), oracle.binomial(rand, steps), 1e-5, atol=1e-6)
 
 
