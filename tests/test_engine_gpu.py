@@ -287,3 +287,14 @@ def test_specialization_must_be_a_variant_of_the_program_kernel(gpu_available):
     with pytest.raises(P.Error) as e:
         P.Engine(P.EngineConfig(devs, P.StaticConfig()), prog).close()
     assert e.value.code == P.ErrorCode.ConfigError
+
+
+@pytest.mark.parametrize("kernel", [f"mandelbrot@{v}" for v in range(7)] + ["mandelbrot_f32@0", "mandelbrot_f32@1"])
+def test_every_mandelbrot_variant_is_bit_exact(gpu_available, oracle, kernel):
+    # tuning variants selectable per device must all reproduce the reference
+    w, h, it = 640, 480, 1000
+    spec = W.mandelbrot_spec(w, h, it)
+    spec.kernel = kernel
+    _, res = run_engine(spec, P.HGuidedConfig(), n_dev=2)
+    exp = oracle.mandelbrot(w, h, it, f32=kernel.startswith("mandelbrot_f32"))
+    assert np.array_equal(res.outputs[0].view(np.uint32), expand_4to1(exp))

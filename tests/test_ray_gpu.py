@@ -39,3 +39,16 @@ def test_ray_irregular_depths(oracle):
     depths = np.bincount(out[:, 3].astype(int), minlength=5)
     assert (depths > 0).all()
     assert counts[0] > 0 and counts[2] > 0
+
+
+@pytest.mark.parametrize("kernel", ["ray@0", "ray@1", "ray@2"])
+def test_ray_variants_bit_exact(gpu_available, oracle, kernel):
+    w, h, ns = 96, 64, 17
+    scene = W.ray_scene(ns, seed=4)
+    spec = W.ray_spec(w, h, ns, 4, lws=64)
+    spec.kernel = kernel
+    prog = P.validate_program(spec)
+    with P.Engine(P.EngineConfig([P.cuda_device("gpu0", 0)], P.HGuidedConfig()), prog) as e:
+        res = e.run([scene])
+    exp, _ = oracle.ray(scene, ns, w, h, 4)
+    assert np.array_equal(res.outputs[0].view(np.float32).reshape(-1, 4), exp)
