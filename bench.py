@@ -647,6 +647,8 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
     mix = ctypes.c_double(0.0)
     if wl.name == "mandelbrot":
         N.lib.ecl_probe_mandel_mix(my_gpu, ctypes.byref(mix))
+    elif wl.name == "mandelbrot_f32":
+        N.lib.ecl_probe_mandel_mix_f32(my_gpu, ctypes.byref(mix))
     peak = (f64.value if wl.bound == "fp64" else f32.value) * n  # whole job: N GPUs
     achieved = wl.flops() / (ms_dev * 1e-3) / 1e12
     eng.close()
@@ -707,6 +709,9 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
         "gpu_launches": launches,
         "clocks": merge_clocks(clocks, clocks2),
     }
+    if mix.value > 0 and wl.bound != "fp64":
+        line["roofline"]["mix_ceiling_tflops"] = mix.value * n
+        line["roofline"]["frac_of_mix_ceiling"] = achieved / (mix.value * n)
     if wl.bound == "fp64":
         # bit-exactness forbids contraction: 8 algorithmic flops take 6 FP64
         # pipe instructions on the fast path, so the attainable fraction of the

@@ -198,6 +198,8 @@ int ecl_probe_vector_peaks(int ordinal, double* fp64_fma_tflops, double* fp64_ad
  * attainable ceiling for the exact kernel (DMUL/DADD streams run below the
  * DFMA-chain peak). */
 int ecl_probe_mandel_mix(int ordinal, double* tflops);
+/* The same for the packed FP32 variant (FFMA2/FADD2, two pixels per lane). */
+int ecl_probe_mandel_mix_f32(int ordinal, double* tflops);
 
 const char* ecl_last_error(void);
 

@@ -76,6 +76,7 @@ _sig("ecl_engine_last_error", c_char_p)
 # device layer (subset used from Python)
 _sig("ecl_gpu_count", c_int, ctypes.POINTER(c_int))
 _sig("ecl_probe_mandel_mix", c_int, c_int, ctypes.POINTER(c_dbl))
+_sig("ecl_probe_mandel_mix_f32", c_int, c_int, ctypes.POINTER(c_dbl))
 _sig("ecl_host_register", c_int, c_void_p, ctypes.c_size_t)
 _sig("ecl_host_unregister", c_int, c_void_p)
 _sig("ecl_host_alloc", c_int, ctypes.c_size_t, ctypes.POINTER(c_void_p))
