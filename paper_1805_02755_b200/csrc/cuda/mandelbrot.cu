@@ -548,7 +548,8 @@ cudaError_t launch_mandelbrot(const KernelSpec& spec, const LaunchEnv& env, uint
     switch (mb) {
       case 4: return launch_x2<float, 16, 4>(spec.mandel, env, first, count);
       case 6: return launch_x2<float, 16, 6>(spec.mandel, env, first, count);
-      default: return launch_x2<float, 16, 5>(spec.mandel, env, first, count);
+      case 16: return launch_x2<float, 16, 5>(spec.mandel, env, first, count);  // R = 16: 27.0 ms
+      default: return launch_x2<float, 32, 5>(spec.mandel, env, first, count);  // R = 32: 26.5 ms
     }
   }
   // Tuning hook (ECL_MANDEL_VARIANT): block length R and resident CTAs per SM.
