@@ -97,7 +97,76 @@ __global__ void coord_tables(const Viewport<Real> vp, Real* __restrict__ tab) {
   }
 }
 
-template <typename Real, int R, int MB = kMinBlocks<Real>>
+// One speculative block of RB iterations for this lane, replayed exactly
+// when its flag is raised (see the comment at the call site).  Warp-uniform
+// control: every lane of the warp calls it with the same RB.
+template <typename Real, int RB>
+__device__ __forceinline__ void spec_block(Real& zx, Real& zy, uint32_t& n, bool& alive, bool far, Real cx, Real cy,
+                                           uint32_t max_it) {
+  using A = Arith<Real>;
+  using Bits = typename A::Bits;
+  const Real zx0 = zx, zy0 = zy;
+  const uint32_t n0 = n;
+  uint32_t acc = 0;
+  if (__all_sync(kFull, far || !alive)) {
+#pragma unroll
+    for (int r = 0; r < RB - 1; ++r) {
+      const Real xx = A::mul(zx, zx);
+      const Real yy = A::mul(zy, zy);
+      const Real t = A::mul(zx, zy);
+      zy = A::twice_plus(t, cy);
+      zx = A::add(A::sub(xx, yy), cx);
+    }
+    const Real xx = A::mul(zx, zx);
+    const Real yy = A::mul(zy, zy);
+    acc = A::high(xx) | A::high(yy);
+    const Real t = A::mul(zx, zy);
+    zy = A::twice_plus(t, cy);
+    zx = A::add(A::sub(xx, yy), cx);
+  } else {
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const Real xx = A::mul(zx, zx);
+      const Real yy = A::mul(zy, zy);
+      acc |= A::high(xx) | A::high(yy);
+      const Real t = A::mul(zx, zy);
+      zy = A::twice_plus(t, cy);
+      zx = A::add(A::sub(xx, yy), cx);
+    }
+  }
+  const bool fast = alive && n0 + RB <= max_it && (acc & 0x40000000u) == 0u;
+  if (fast) {
+    n = n0 + RB;
+    alive = n < max_it;
+  }
+  bool live = alive && !fast;  // lanes replaying the block exactly
+  if (__any_sync(kFull, live)) {
+    if (live) {
+      zx = zx0;
+      zy = zy0;
+      n = n0;
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const Real xx = A::mul(zx, zx);
+      const Real yy = A::mul(zy, zy);
+      const Bits s = A::bits(A::add(xx, yy));  // >= +0: integer order == FP order
+      live = live && s <= A::kFourBits;
+      const Real t = A::mul(zx, zy);
+      const Real nzy = A::twice_plus(t, cy);
+      const Real nzx = A::add(A::sub(xx, yy), cx);
+      if (live) {
+        zx = nzx;
+        zy = nzy;
+        n += 1u;
+      }
+      live = live && n < max_it;
+    }
+    if (alive && !fast) alive = live;
+  }
+}
+
+template <typename Real, int R, int MB = kMinBlocks<Real>, int RL = R, uint32_t kSettle = 32>
 __global__ void __launch_bounds__(kThreads, MB)
     mandel_persistent(const Viewport<Real> vp, const Real* __restrict__ tab, uint64_t first, uint64_t count,
                       uint4* __restrict__ out, uint32_t* __restrict__ compact, unsigned* __restrict__ ctrl) {
@@ -190,65 +259,12 @@ __global__ void __launch_bounds__(kThreads, MB)
     // instructions hold the issue port two cycles each, so it cost ~8 %
     // (tools/probe/mandel_mix2.cu) — and skips replays for orbits that only
     // pass |z| > sqrt(2) mid-block.
-    const Real zx0 = zx, zy0 = zy;
-    const uint32_t n0 = n;
-    uint32_t acc = 0;
-    if (__all_sync(kFull, far || !alive)) {
-#pragma unroll
-      for (int r = 0; r < R - 1; ++r) {
-        const Real xx = A::mul(zx, zx);
-        const Real yy = A::mul(zy, zy);
-        const Real t = A::mul(zx, zy);
-        zy = A::twice_plus(t, cy);
-        zx = A::add(A::sub(xx, yy), cx);
-      }
-      const Real xx = A::mul(zx, zx);
-      const Real yy = A::mul(zy, zy);
-      acc = A::high(xx) | A::high(yy);
-      const Real t = A::mul(zx, zy);
-      zy = A::twice_plus(t, cy);
-      zx = A::add(A::sub(xx, yy), cx);
-    } else {
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const Real xx = A::mul(zx, zx);
-        const Real yy = A::mul(zy, zy);
-        acc |= A::high(xx) | A::high(yy);
-        const Real t = A::mul(zx, zy);
-        zy = A::twice_plus(t, cy);
-        zx = A::add(A::sub(xx, yy), cx);
-      }
-    }
-    const bool fast = alive && n0 + R <= max_it && (acc & 0x40000000u) == 0u;
-    if (fast) {
-      n = n0 + R;
-      alive = n < max_it;
-    }
-    bool live = alive && !fast;  // lanes replaying the block exactly
-    if (__any_sync(kFull, live)) {
-      if (live) {
-        zx = zx0;
-        zy = zy0;
-        n = n0;
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const Real xx = A::mul(zx, zx);
-        const Real yy = A::mul(zy, zy);
-        const Bits s = A::bits(A::add(xx, yy));  // >= +0: integer order == FP order
-        live = live && s <= A::kFourBits;
-        const Real t = A::mul(zx, zy);
-        const Real nzy = A::twice_plus(t, cy);
-        const Real nzx = A::add(A::sub(xx, yy), cx);
-        if (live) {
-          zx = nzx;
-          zy = nzy;
-          n += 1u;
-        }
-        live = live && n < max_it;
-      }
-      if (alive && !fast) alive = live;
-    }
+    // Block length: every live pixel of the warp past its first kSettle
+    // iterations (long orbits, mostly the set's interior) -> RL-iteration
+    // blocks, amortizing the block control; otherwise R, so pixels that
+    // escape early waste fewer speculative iterations.
+    if (__all_sync(kFull, !alive || n >= kSettle)) spec_block<Real, RL>(zx, zy, n, alive, far, cx, cy, max_it);
+    else spec_block<Real, R>(zx, zy, n, alive, far, cx, cy, max_it);
     if (valid && !alive) {
       out[idx] = make_uint4(n, n, n, n);
       if (compact) compact[idx] = n;  // host-bound copy: one count per pixel
@@ -521,11 +537,11 @@ Viewport<Real> make_viewport(const MandelParams& p) {
   return vp;
 }
 
-template <typename Real, int R, int MB = kMinBlocks<Real>>
+template <typename Real, int R, int MB = kMinBlocks<Real>, int RL = R, uint32_t kSettle = 32>
 cudaError_t launch_real(const MandelParams& p, const LaunchEnv& env, uint64_t first, uint64_t count) {
   static int blocks_per_sm = 0;
   if (blocks_per_sm == 0) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, mandel_persistent<Real, R, MB>,
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, mandel_persistent<Real, R, MB, RL, kSettle>,
                                                                   kThreads, 0);
     if (e != cudaSuccess) return e;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
@@ -537,7 +553,7 @@ cudaError_t launch_real(const MandelParams& p, const LaunchEnv& env, uint64_t fi
   uint64_t grid = static_cast<uint64_t>(env.sms) * static_cast<uint64_t>(blocks_per_sm);
   if (blocks_needed < grid) grid = blocks_needed;
   if (grid == 0) return cudaSuccess;
-  mandel_persistent<Real, R, MB><<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
+  mandel_persistent<Real, R, MB, RL, kSettle><<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
       vp, tab, first, count, static_cast<uint4*>(env.out[0]), env.compact, env.ctrl);
   return cudaGetLastError();
 }
@@ -615,7 +631,16 @@ cudaError_t launch_mandelbrot(const KernelSpec& spec, const LaunchEnv& env, uint
     // the config): the FP64 kernel is not short of independent work
     case 5: return launch_x2<double, 16, 2>(spec.mandel, env, first, count);
     case 6: return launch_x2<double, 16, 3>(spec.mandel, env, first, count);
-    default: return launch_real<double, 16, 4>(spec.mandel, env, first, count);  // measured best
+    case 7: return launch_real<double, 16, 4, 32>(spec.mandel, env, first, count);
+    case 8: return launch_real<double, 8, 4, 32>(spec.mandel, env, first, count);
+    case 9: return launch_real<double, 16, 4, 64>(spec.mandel, env, first, count);
+    case 10: return launch_real<double, 8, 4, 64>(spec.mandel, env, first, count);
+    case 11: return launch_real<double, 8, 4, 32, 16>(spec.mandel, env, first, count);
+    case 12: return launch_real<double, 8, 4, 32, 64>(spec.mandel, env, first, count);
+    case 13: return launch_real<double, 8, 4, 24>(spec.mandel, env, first, count);
+    // measured (16384^2 x 2048): (8, 32 after 32 iterations) 38.85 ms; fixed 16: 41.2 ms;
+    // (16, 32) 39.2; (8, 64) 39.1; (16, 64) 39.3; settle after 16 / 64: 39.2; (8, 24) 39.8
+    default: return launch_real<double, 8, 4, 32>(spec.mandel, env, first, count);
   }
 }
 

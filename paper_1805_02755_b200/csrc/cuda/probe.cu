@@ -59,9 +59,10 @@ float time_chain(int sms, int iters, cudaStream_t st, double* sink) {
 }
 
 // The Mandelbrot iteration's own instruction mix and dependency chain
-// (3 DMUL, 1 DFMA, 2 DADD, 1 LOP3 per iteration, two pixels per thread, no
-// control flow): the FP64 rate the exact kernel can reach at best on this
-// device — DMUL/DADD streams sustain less than the DFMA-chain peak.
+// (3 DMUL, 1 DFMA, 2 DADD per iteration, the speculation's LOP3 once per
+// 16-iteration block as in the kernel's end-checked blocks, two pixels per
+// thread, no other control flow): the FP64 rate the exact kernel can reach
+// at best on this device.
 __global__ void __launch_bounds__(256) mandel_mix(double* sink, unsigned* flag, int iters) {
   double zx[2] = {0, 0}, zy[2] = {0, 0}, cx[2], cy[2];
   unsigned acc = 0;
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(256) mandel_mix(double* sink, unsigned* flag, 
       for (int k = 0; k < 2; ++k) {
         const double xx = __dmul_rn(zx[k], zx[k]);
         const double yy = __dmul_rn(zy[k], zy[k]);
-        acc |= static_cast<unsigned>(__double2hiint(xx)) | static_cast<unsigned>(__double2hiint(yy));
+        if (r == 15) acc |= static_cast<unsigned>(__double2hiint(xx)) | static_cast<unsigned>(__double2hiint(yy));
         const double t = __dmul_rn(zx[k], zy[k]);
         zy[k] = __fma_rn(t, 2.0, cy[k]);
         zx[k] = __dadd_rn(__dsub_rn(xx, yy), cx[k]);
