@@ -335,7 +335,98 @@ struct Slot2 {
   bool valid = false, alive = false, far = true;  // far: |c| < 1.9 (end-checked blocks allowed)
 };
 
-template <typename Real, int R, int MB>
+// One speculative block of RB iterations on both slots of a lane (see
+// spec_block); warp-uniform RB.
+template <typename Real, int RB>
+__device__ __forceinline__ void spec_block2(typename Pair<Real>::V& zx, typename Pair<Real>::V& zy, Slot2& sa,
+                                            Slot2& sb, typename Pair<Real>::V cx, typename Pair<Real>::V cy,
+                                            uint32_t max_it) {
+  using A = Pair<Real>;
+  using V = typename A::V;
+  const V zx0 = zx, zy0 = zy;
+  const uint32_t na0 = sa.n, nb0 = sb.n;
+  uint32_t acc_a = 0, acc_b = 0;
+  if (__all_sync(kFull, (sa.far || !sa.alive) && (sb.far || !sb.alive))) {  // end-checked block
+#pragma unroll
+    for (int r = 0; r < RB - 1; ++r) {
+      const V xx = A::mul0(zx, zx);
+      const V yy = A::mul0(zy, zy);
+      const V t = A::mul0(zx, zy);
+      zy = A::twice_plus(t, cy);
+      zx = A::add(A::sub(xx, yy), cx);
+    }
+    const V xx = A::mul0(zx, zx);
+    const V yy = A::mul0(zy, zy);
+    acc_a = A::hi(xx.x) | A::hi(yy.x);
+    acc_b = A::hi(xx.y) | A::hi(yy.y);
+    const V t = A::mul0(zx, zy);
+    zy = A::twice_plus(t, cy);
+    zx = A::add(A::sub(xx, yy), cx);
+  } else {
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const V xx = A::mul0(zx, zx);
+      const V yy = A::mul0(zy, zy);
+      acc_a |= A::hi(xx.x) | A::hi(yy.x);
+      acc_b |= A::hi(xx.y) | A::hi(yy.y);
+      const V t = A::mul0(zx, zy);
+      zy = A::twice_plus(t, cy);
+      zx = A::add(A::sub(xx, yy), cx);
+    }
+  }
+  const bool fast_a = sa.alive && na0 + RB <= max_it && (acc_a & 0x40000000u) == 0u;
+  const bool fast_b = sb.alive && nb0 + RB <= max_it && (acc_b & 0x40000000u) == 0u;
+  if (fast_a) {
+    sa.n = na0 + RB;
+    sa.alive = sa.n < max_it;
+  }
+  if (fast_b) {
+    sb.n = nb0 + RB;
+    sb.alive = sb.n < max_it;
+  }
+  bool live_a = sa.alive && !fast_a, live_b = sb.alive && !fast_b;
+  if (__any_sync(kFull, live_a || live_b)) {
+    if (live_a) {
+      zx.x = zx0.x;
+      zy.x = zy0.x;
+      sa.n = na0;
+    }
+    if (live_b) {
+      zx.y = zx0.y;
+      zy.y = zy0.y;
+      sb.n = nb0;
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const V xx = A::mul0(zx, zx);
+      const V yy = A::mul0(zy, zy);
+      const V s = A::add(xx, yy);  // >= +0: integer order == FP order
+      live_a = live_a && A::le4(s.x);
+      live_b = live_b && A::le4(s.y);
+      const V t = A::mul0(zx, zy);
+      const V nzy = A::twice_plus(t, cy);
+      const V nzx = A::add(A::sub(xx, yy), cx);
+      if (live_a) {
+        zx.x = nzx.x;
+        zy.x = nzy.x;
+        sa.n += 1u;
+      }
+      if (live_b) {
+        zx.y = nzx.y;
+        zy.y = nzy.y;
+        sb.n += 1u;
+      }
+      live_a = live_a && sa.n < max_it;
+      live_b = live_b && sb.n < max_it;
+    }
+    if (sa.alive && !fast_a) sa.alive = live_a;
+    if (sb.alive && !fast_b) sb.alive = live_b;
+  }
+}
+
+constexpr uint32_t kSettle2 = 32;
+
+template <typename Real, int R, int MB, int RL = R>
 __global__ void __launch_bounds__(kThreads, MB)
     mandel_x2(const Viewport<Real> vp, const Real* __restrict__ tab, uint64_t first, uint64_t count,
               uint4* __restrict__ out, uint32_t* __restrict__ compact, unsigned* __restrict__ ctrl) {
@@ -414,86 +505,12 @@ __global__ void __launch_bounds__(kThreads, MB)
     }
     if (!__any_sync(kFull, sa.valid || sb.valid)) break;
 
-    // Speculative block on both slots (see mandel_persistent).
-    const V zx0 = zx, zy0 = zy;
-    const uint32_t na0 = sa.n, nb0 = sb.n;
-    uint32_t acc_a = 0, acc_b = 0;
-    if (__all_sync(kFull, (sa.far || !sa.alive) && (sb.far || !sb.alive))) {  // end-checked block
-#pragma unroll
-      for (int r = 0; r < R - 1; ++r) {
-        const V xx = A::mul0(zx, zx);
-        const V yy = A::mul0(zy, zy);
-        const V t = A::mul0(zx, zy);
-        zy = A::twice_plus(t, cy);
-        zx = A::add(A::sub(xx, yy), cx);
-      }
-      const V xx = A::mul0(zx, zx);
-      const V yy = A::mul0(zy, zy);
-      acc_a = A::hi(xx.x) | A::hi(yy.x);
-      acc_b = A::hi(xx.y) | A::hi(yy.y);
-      const V t = A::mul0(zx, zy);
-      zy = A::twice_plus(t, cy);
-      zx = A::add(A::sub(xx, yy), cx);
-    } else {
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const V xx = A::mul0(zx, zx);
-        const V yy = A::mul0(zy, zy);
-        acc_a |= A::hi(xx.x) | A::hi(yy.x);
-        acc_b |= A::hi(xx.y) | A::hi(yy.y);
-        const V t = A::mul0(zx, zy);
-        zy = A::twice_plus(t, cy);
-        zx = A::add(A::sub(xx, yy), cx);
-      }
-    }
-    const bool fast_a = sa.alive && na0 + R <= max_it && (acc_a & 0x40000000u) == 0u;
-    const bool fast_b = sb.alive && nb0 + R <= max_it && (acc_b & 0x40000000u) == 0u;
-    if (fast_a) {
-      sa.n = na0 + R;
-      sa.alive = sa.n < max_it;
-    }
-    if (fast_b) {
-      sb.n = nb0 + R;
-      sb.alive = sb.n < max_it;
-    }
-    bool live_a = sa.alive && !fast_a, live_b = sb.alive && !fast_b;
-    if (__any_sync(kFull, live_a || live_b)) {
-      if (live_a) {
-        zx.x = zx0.x;
-        zy.x = zy0.x;
-        sa.n = na0;
-      }
-      if (live_b) {
-        zx.y = zx0.y;
-        zy.y = zy0.y;
-        sb.n = nb0;
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const V xx = A::mul0(zx, zx);
-        const V yy = A::mul0(zy, zy);
-        const V s = A::add(xx, yy);  // >= +0: integer order == FP order
-        live_a = live_a && A::le4(s.x);
-        live_b = live_b && A::le4(s.y);
-        const V t = A::mul0(zx, zy);
-        const V nzy = A::twice_plus(t, cy);
-        const V nzx = A::add(A::sub(xx, yy), cx);
-        if (live_a) {
-          zx.x = nzx.x;
-          zy.x = nzy.x;
-          sa.n += 1u;
-        }
-        if (live_b) {
-          zx.y = nzx.y;
-          zy.y = nzy.y;
-          sb.n += 1u;
-        }
-        live_a = live_a && sa.n < max_it;
-        live_b = live_b && sb.n < max_it;
-      }
-      if (sa.alive && !fast_a) sa.alive = live_a;
-      if (sb.alive && !fast_b) sb.alive = live_b;
-    }
+    // Speculative block on both slots (see mandel_persistent); long blocks
+    // once every live pixel of the warp has settled.
+    if (__all_sync(kFull, (!sa.alive || sa.n >= kSettle2) && (!sb.alive || sb.n >= kSettle2)))
+      spec_block2<Real, RL>(zx, zy, sa, sb, cx, cy, max_it);
+    else
+      spec_block2<Real, R>(zx, zy, sa, sb, cx, cy, max_it);
     if (sa.valid && !sa.alive) {
       out[sa.idx] = make_uint4(sa.n, sa.n, sa.n, sa.n);
       if (compact) compact[sa.idx] = sa.n;
@@ -558,11 +575,11 @@ cudaError_t launch_real(const MandelParams& p, const LaunchEnv& env, uint64_t fi
   return cudaGetLastError();
 }
 
-template <typename Real, int R, int MB>
+template <typename Real, int R, int MB, int RL = R>
 cudaError_t launch_x2(const MandelParams& p, const LaunchEnv& env, uint64_t first, uint64_t count) {
   static int blocks_per_sm = 0;
   if (blocks_per_sm == 0) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, mandel_x2<Real, R, MB>, kThreads, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, mandel_x2<Real, R, MB, RL>, kThreads, 0);
     if (e != cudaSuccess) return e;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
@@ -572,7 +589,7 @@ cudaError_t launch_x2(const MandelParams& p, const LaunchEnv& env, uint64_t firs
   uint64_t grid = static_cast<uint64_t>(env.sms) * static_cast<uint64_t>(blocks_per_sm);
   if (blocks_needed < grid) grid = blocks_needed;
   if (grid == 0) return cudaSuccess;
-  mandel_x2<Real, R, MB><<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
+  mandel_x2<Real, R, MB, RL><<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
       vp, static_cast<const Real*>(env.scratch), first, count, static_cast<uint4*>(env.out[0]), env.compact,
       env.ctrl);
   return cudaGetLastError();
@@ -610,11 +627,15 @@ cudaError_t launch_mandelbrot(const KernelSpec& spec, const LaunchEnv& env, uint
     }();
     if (scalar) return launch_real<float, 16>(spec.mandel, env, first, count);
     switch (mb) {
-      // measured with end-checked blocks: (R 16, 4 CTAs) 24.8 ms, (32, 5) 25.0, (16, 5) 25.3
+      // measured: adaptive (16 -> 32 after 32 iterations, 4 CTAs) 23.7 ms, (8 -> 32) 23.8,
+      // (16 -> 64) 24.0, fixed 16 25.3, fixed 32 (5 CTAs) 25.0
       case 5: return launch_x2<float, 16, 5>(spec.mandel, env, first, count);
       case 6: return launch_x2<float, 16, 6>(spec.mandel, env, first, count);
       case 32: return launch_x2<float, 32, 5>(spec.mandel, env, first, count);
-      default: return launch_x2<float, 16, 4>(spec.mandel, env, first, count);
+      case 16: return launch_x2<float, 16, 4>(spec.mandel, env, first, count);
+      case 7: return launch_x2<float, 8, 4, 32>(spec.mandel, env, first, count);
+      case 8: return launch_x2<float, 16, 4, 64>(spec.mandel, env, first, count);
+      default: return launch_x2<float, 16, 4, 32>(spec.mandel, env, first, count);
     }
   }
   // Tuning hook (ECL_MANDEL_VARIANT): block length R and resident CTAs per SM.
