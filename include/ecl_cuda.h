@@ -135,6 +135,22 @@ int ecl_host_unregister(void* ptr);
 int ecl_host_alloc(size_t bytes, void** ptr);
 int ecl_host_free(void* ptr);
 
+/* ---- raw executor entry points (SURVEY.md §8b's proposed C-ABI) ------
+ * Thin forms of the calls above for a caller that manages its own device
+ * buffers: plain device allocations, H2D/D2H of raw bytes, and a launch of
+ * the bound kernel over a work-item range (work-group aligned) with an
+ * event-recorded completion. */
+int ecl_gpu_alloc(ecl_gpu* gpu, size_t bytes, void** device_ptr);
+int ecl_gpu_free(ecl_gpu* gpu, void* device_ptr);
+/* Async H2D on the device's first compute lane (later kernels see it). */
+int ecl_gpu_upload(ecl_gpu* gpu, void* device_dst, const void* host_src, size_t bytes);
+/* Blocking D2H after every submitted package. */
+int ecl_gpu_download(ecl_gpu* gpu, void* host_dst, const void* device_src, size_t bytes);
+/* Package of work-items [first_item, first_item + item_count) of the bound
+ * kernel (== ecl_gpu_submit with work-group bounds, no host outputs). */
+int ecl_gpu_launch(ecl_gpu* gpu, const ecl_kernel* kernel, uint64_t first_item, uint64_t item_count, uint64_t seq,
+                   ecl_done_fn done, void* user);
+
 /* ---- packages -------------------------------------------------------- */
 /* Enqueues package `seq` = work-groups [offset_wg, offset_wg+size_wg): the
  * kernel over its work-items on the compute stream between two timing

@@ -623,6 +623,44 @@ int ecl_host_free(void* ptr) {
   return ECL_OK;
 }
 
+int ecl_gpu_alloc(ecl_gpu* g, size_t bytes, void** dptr) {
+  *dptr = nullptr;
+  if (int rc = set_device(g)) return rc;
+  ECL_CK(cudaMalloc(dptr, std::max<size_t>(bytes, 16)));
+  return ECL_OK;
+}
+
+int ecl_gpu_free(ecl_gpu* g, void* dptr) {
+  if (int rc = set_device(g)) return rc;
+  if (int rc = sync_all(g)) return rc;
+  ECL_CK(cudaFree(dptr));
+  return ECL_OK;
+}
+
+int ecl_gpu_upload(ecl_gpu* g, void* dst, const void* src, size_t bytes) {
+  if (int rc = set_device(g)) return rc;
+  if (int rc = join_lanes(g)) return rc;
+  ECL_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g->lane[0]));
+  return fan_out_lane0(g);
+}
+
+int ecl_gpu_download(ecl_gpu* g, void* dst, const void* src, size_t bytes) {
+  if (int rc = set_device(g)) return rc;
+  if (int rc = sync_all(g)) return rc;
+  ECL_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, g->copy[0]));
+  ECL_CK(cudaStreamSynchronize(g->copy[0]));
+  return ECL_OK;
+}
+
+int ecl_gpu_launch(ecl_gpu* g, const ecl_kernel* k, uint64_t first_item, uint64_t item_count, uint64_t seq,
+                   ecl_done_fn done, void* user) {
+  if (!g->spec || &k->spec != g->spec) return fail(ECL_CONFIG_ERROR, "launch: kernel is not the one bound");
+  const uint64_t lws = g->spec->lws;
+  if (item_count == 0 || first_item % lws != 0 || item_count % lws != 0)
+    return fail(ECL_INDIVISIBLE_PACKAGE, "launch: item range must be whole work-groups");
+  return ecl_gpu_submit(g, seq, first_item / lws, item_count / lws, nullptr, done, user);
+}
+
 int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_wg, void* const* host_outputs,
                    ecl_done_fn done, void* user) {
   if (!g->spec) return fail(ECL_CONFIG_ERROR, "submit before bind");
