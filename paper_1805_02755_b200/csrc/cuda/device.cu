@@ -127,6 +127,16 @@ struct ecl_gpu {
     return n > 0 ? static_cast<uint64_t>(n) : ~uint64_t{0};
   }();
   uint64_t piece_counter = 0;
+  // Staging ring for the compact copies (ring_setup): instead of
+  // a gws-sized landing zone, copies land in R page-locked slots of S items
+  // that the widen workers release; a copy stream waits (cuStreamWaitValue32
+  // on the slot's release counter) before it reuses a slot.
+  uint32_t* ring = nullptr;           // R x S items, page-locked
+  uint32_t* ring_released = nullptr;  // R counters, page-locked + mapped (widen workers bump them)
+  void* ring_released_dev = nullptr;  // device address of ring_released
+  std::vector<uint32_t> ring_uses;    // copies issued per slot
+  uint32_t ring_slots = 0, ring_next = 0;
+  uint64_t ring_items = 0;
   uint64_t input_gen = 0;  // see next_input_gen()
   // Streamed inputs (ecl_gpu_set_streamed_inputs): uploads are enqueued on
   // `h2d` piece by piece, each piece's kernel waiting for the prefix it reads.
@@ -189,6 +199,76 @@ cudaError_t pinned_free(void* p) {
 uint64_t next_input_gen() {
   static std::atomic<uint64_t> gen{0};
   return ++gen;
+}
+
+// cuStreamWaitValue32 through the runtime's driver entry point (no libcuda
+// link).  Returns nullptr when the driver does not offer it.
+using WaitValueFn = int (*)(cudaStream_t, unsigned long long, uint32_t, unsigned);
+WaitValueFn wait_value_fn() {
+  static WaitValueFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<WaitValueFn>(nullptr);
+    }
+    return reinterpret_cast<WaitValueFn>(p);
+  }();
+  return fn;
+}
+
+// Sets up the staging ring once per device.  Slots of ECL_WIDEN_RING_SLOT_KB
+// (2 MiB); ECL_WIDEN_RING_SLOTS sets their number, 0 turns the ring off
+// (gws-sized landing zone), unset = two slots per widen worker plus four for
+// copies in flight.  It pins 64 MiB instead of gws x 4 bytes (1 GiB at the
+// Mandelbrot config, per device) and keeps the copies' landing data in the
+// host's last-level cache.  Measured (1 B200, 16-core host, Mandelbrot
+// 16384^2 e2e, three alternating runs): 32 slots 49.6-50.1 ms against
+// 50.5-50.7 ms for the landing zone; one box gave 46.8 vs 49.3.  A ring with
+// barely more slots than workers starves the copies (16 slots: 89 ms), hence
+// the auto size.  The ring stays off when the driver lacks stream memory
+// operations.
+cudaError_t ring_setup(ecl_gpu* g) {
+  static const long long ring_slots = [] {
+    const char* v = std::getenv("ECL_WIDEN_RING_SLOTS");
+    return v ? std::atoll(v) : -1ll;
+  }();
+  static const uint64_t slot_kb = [] {
+    const char* v = std::getenv("ECL_WIDEN_RING_SLOT_KB");
+    const long long n = v ? std::atoll(v) : 2048;
+    return n > 0 ? static_cast<uint64_t>(n) : uint64_t{2048};
+  }();
+  if (g->ring || ring_slots == 0 || !wait_value_fn()) return cudaSuccess;
+  const uint64_t items = slot_kb * 1024 / 4;
+  const uint64_t auto_slots = 2ull * ecl::widen_workers() + 4;
+  const uint32_t slots =
+      static_cast<uint32_t>(ring_slots < 0 ? auto_slots : std::max<long long>(1, ring_slots));
+  void* p = nullptr;
+  cudaError_t e = pinned_alloc(&p, slots * items * 4);
+  if (e != cudaSuccess) return e;
+  void* f = nullptr;
+  e = cudaHostAlloc(&f, slots * sizeof(uint32_t), cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    pinned_free(p);
+    return e;
+  }
+  std::memset(f, 0, slots * sizeof(uint32_t));
+  void* fd = nullptr;
+  e = cudaHostGetDevicePointer(&fd, f, 0);
+  if (e != cudaSuccess) {
+    pinned_free(p);
+    cudaFreeHost(f);
+    return e;
+  }
+  g->ring = static_cast<uint32_t*>(p);
+  g->ring_released = static_cast<uint32_t*>(f);
+  g->ring_released_dev = fd;
+  g->ring_uses.assign(slots, 0);
+  g->ring_slots = slots;
+  g->ring_items = items;
+  g->ring_next = 0;
+  return cudaSuccess;
 }
 
 Slot* find_slot(ecl_gpu* g, uint64_t seq) {
@@ -369,6 +449,8 @@ int ecl_gpu_close(ecl_gpu* g) {
   if (g->tally) cudaFree(g->tally);
   if (g->compact_dev) cudaFree(g->compact_dev);
   if (g->compact_host) pinned_free(g->compact_host);
+  if (g->ring) pinned_free(g->ring);
+  if (g->ring_released) cudaFreeHost(g->ring_released);
   for (auto& s : g->slots) {
     if (s.start) cudaEventDestroy(s.start);
     if (s.end) cudaEventDestroy(s.end);
@@ -708,7 +790,8 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
   const bool widen = copies && s.replicate > 1 && g->compact_dev && s.outputs.size() == 1 &&
                      s.outputs[0].element_size_bytes == 4 && s.out_indices == s.replicate &&
                      s.out_work_items == 1 && g->widen_per_8 > 0;
-  if (widen && !g->compact_host) {
+  if (widen) ECL_CK(ring_setup(g));
+  if (widen && !g->ring && !g->compact_host) {
     void* p = nullptr;
     ECL_CK(pinned_alloc(&p, g->compact_items * 4));
     g->compact_host = static_cast<uint32_t*>(p);
@@ -763,10 +846,25 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
       // soon as it lands.  Measured on the 16-core Xeon host: 2^20-item
       // chunks = whole pieces (54.5 vs 54.9 ms), smaller chunks slower (API
       // cost), so the default is one copy per piece.
-      for (uint64_t c0 = 0; c0 < count; c0 += g->widen_chunk_items) {
-        const uint64_t cn = std::min(g->widen_chunk_items, count - c0);
-        ECL_CK(cudaMemcpyAsync(g->compact_host + first + c0, g->compact_dev + first + c0, cn * sizeof(uint32_t),
-                               cudaMemcpyDeviceToHost, cp));
+      const uint64_t chunk = g->ring ? g->ring_items : g->widen_chunk_items;
+      for (uint64_t c0 = 0; c0 < count; c0 += chunk) {
+        const uint64_t cn = std::min(chunk, count - c0);
+        uint32_t* land = g->compact_host ? g->compact_host + first + c0 : nullptr;
+        uint32_t* release = nullptr;
+        uint32_t release_value = 0;
+        if (g->ring) {  // next staging slot, once its previous contents are widened
+          const uint32_t r = g->ring_next;
+          g->ring_next = (r + 1) % g->ring_slots;
+          const uint32_t uses = g->ring_uses[r]++;
+          const unsigned long long flag = reinterpret_cast<unsigned long long>(g->ring_released_dev) + 4ull * r;
+          if (wait_value_fn()(cp, flag, uses, 0 /* CU_STREAM_WAIT_VALUE_GEQ */) != 0)
+            return fail(ECL_KERNEL_PANIC, "staging ring: stream wait failed");
+          land = g->ring + static_cast<uint64_t>(r) * g->ring_items;
+          release = g->ring_released + r;
+          release_value = uses + 1;
+        }
+        ECL_CK(cudaMemcpyAsync(land, g->compact_dev + first + c0, cn * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                               cp));
         if (slot.piece_done.size() <= piece_no) {
           cudaEvent_t ev;
           // blocking-sync: widen workers sleep on it instead of spinning a core
@@ -775,9 +873,8 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
         }
         cudaEvent_t ev = slot.piece_done[piece_no++];
         ECL_CK(cudaEventRecord(ev, cp));
-        ecl::widen_async(g->ordinal, ev, g->compact_host + first + c0,
-                         static_cast<uint32_t*>(host_outputs[0]) + p_off + c0 * s.replicate, cn, s.replicate,
-                         &slot.widen);
+        ecl::widen_async(g->ordinal, ev, land, static_cast<uint32_t*>(host_outputs[0]) + p_off + c0 * s.replicate,
+                         cn, s.replicate, &slot.widen, release, release_value);
       }
       continue;
     }

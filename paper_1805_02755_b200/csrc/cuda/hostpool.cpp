@@ -3,11 +3,11 @@
 // The Mandelbrot kernel writes four identical uint32 counts per work-item
 // (the reference's 4:1 out pattern, workloads.hpp:217-222).  Shipping all
 // four over PCIe costs 16 B/pixel (4 GiB at the config, ~75 ms at 57 GB/s);
-// the device layer instead copies the one count per pixel (4 B/pixel) into a
-// page-locked staging buffer and this pool widens every piece into the
-// caller's buffer as soon as its copy has landed, with non-temporal 128-bit
-// stores on all host cores, overlapped with the remaining kernels and
-// copies.  The caller's buffer ends up byte-identical to a full D2H.
+// the device layer instead copies the one count per pixel (4 B/pixel) into
+// page-locked staging slots (device.cu ring_setup) and this pool widens
+// every piece into the caller's buffer as soon as its copy has landed, with
+// non-temporal 128-bit stores on all host cores, overlapped with the
+// remaining kernels and copies.  The caller's buffer ends up byte-identical to a full D2H.
 #include <cuda_runtime.h>
 #include <emmintrin.h>
 
@@ -33,6 +33,8 @@ struct Job {
   uint64_t count;
   uint32_t rep;
   WidenTicket* ticket;
+  uint32_t* release;
+  uint32_t release_value;
 };
 
 void widen(const uint32_t* src, uint32_t* dst, uint64_t count, uint32_t rep) {
@@ -66,8 +68,10 @@ class Pool {
   unsigned size() const { return static_cast<unsigned>(threads_.size()); }
 
   void submit(const Job& j) {
-    // split into ~2 MiB-of-output sub-jobs so every core takes part
-    const uint64_t sub = std::max<uint64_t>(1, (1u << 19) / std::max<uint32_t>(1, j.rep));
+    // split into ~2 MiB-of-output sub-jobs so every core takes part (ring
+    // jobs stay whole: one release per staging slot)
+    const uint64_t sub = j.release ? std::max<uint64_t>(1, j.count)
+                                   : std::max<uint64_t>(1, (1u << 19) / std::max<uint32_t>(1, j.rep));
     std::vector<Job> parts;
     for (uint64_t o = 0; o < j.count; o += sub) {
       Job p = j;
@@ -118,6 +122,7 @@ class Pool {
       } else {
         widen(j.src, j.dst, j.count, j.rep);
       }
+      if (j.release) __atomic_store_n(j.release, j.release_value, __ATOMIC_RELEASE);
       if (j.ticket->pending.fetch_sub(1) == 1) {
         std::lock_guard lock(j.ticket->m);
         j.ticket->cv.notify_all();
@@ -140,9 +145,11 @@ Pool& pool() {
 }  // namespace
 
 void widen_async(int device, cudaEvent_t ready, const uint32_t* src, uint32_t* dst, uint64_t count, uint32_t rep,
-                 WidenTicket* ticket) {
-  pool().submit(Job{device, ready, src, dst, count, rep, ticket});
+                 WidenTicket* ticket, uint32_t* release, uint32_t release_value) {
+  pool().submit(Job{device, ready, src, dst, count, rep, ticket, release, release_value});
 }
+
+unsigned widen_workers() { return pool().size(); }
 
 bool widen_wait(WidenTicket* ticket) {
   if (ticket->pending.load() == 0) return !ticket->failed.load();  // idle ticket: no lock

@@ -19,9 +19,15 @@ struct WidenTicket {
 };
 
 // After `ready` completes, writes `rep` copies of src[i] to dst[i*rep .. +rep)
-// for i < count, on the pool's threads.
+// for i < count, on the pool's threads.  With `release`, the job runs as one
+// piece and then stores `release_value` to *release (a page-locked word a
+// copy stream waits on before it reuses src: the staging ring of
+// device.cu) — also when the copy failed, so a waiting stream never hangs.
 void widen_async(int device, cudaEvent_t ready, const uint32_t* src, uint32_t* dst, uint64_t count, uint32_t rep,
-                 WidenTicket* ticket);
+                 WidenTicket* ticket, uint32_t* release = nullptr, uint32_t release_value = 0);
+
+// Number of widen worker threads.
+unsigned widen_workers();
 
 // Blocks until every job of the ticket finished; false if a copy failed.
 bool widen_wait(WidenTicket* ticket);

@@ -298,3 +298,33 @@ def test_every_mandelbrot_variant_is_bit_exact(gpu_available, oracle, kernel):
     _, res = run_engine(spec, P.HGuidedConfig(), n_dev=2)
     exp = oracle.mandelbrot(w, h, it, f32=kernel.startswith("mandelbrot_f32"))
     assert np.array_equal(res.outputs[0].view(np.uint32), expand_4to1(exp))
+
+
+_RING_SCRIPT = """
+import sys, numpy as np
+import paper_1805_02755_b200 as P
+from paper_1805_02755_b200 import workloads as W
+prog = P.validate_program(W.mandelbrot_spec(512, 256, 300))
+devs = [P.cuda_device(f"gpu{i}", 0, copy_split_items=8192) for i in range(2)]
+with P.Engine(P.EngineConfig(devs, P.DynamicConfig(9)), prog) as e:
+    for _ in range(2):
+        out = e.run([]).outputs[0]
+np.save(sys.argv[1], out.view(np.uint32))
+"""
+
+
+@pytest.mark.parametrize("slots", ["1", "2", "5"])
+def test_staging_ring_wraps_and_matches_oracle(gpu_available, oracle, tmp_path, slots):
+    # The compact copies land in a ring of page-locked slots that the widen
+    # workers release (device.cu ring_setup); with 1 KiB-item slots a 512x256
+    # image cycles a 1-, 2- or 5-slot ring dozens of times per run, across
+    # two logical devices with their own rings and two runs.
+    import os
+    import subprocess
+    import sys
+    f = tmp_path / "out.npy"
+    env = dict(os.environ, ECL_WIDEN_RING_SLOTS=slots, ECL_WIDEN_RING_SLOT_KB="4")
+    r = subprocess.run([sys.executable, "-c", _RING_SCRIPT, str(f)], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert np.array_equal(np.load(f), expand_4to1(oracle.mandelbrot(512, 256, 300)))
