@@ -1,0 +1,163 @@
+// What bounds the Binomial lattice?  The packed two-option lattice of
+// binomial.cu (8 nodes per lane, one shuffle per level, phases of 32 levels
+// with a shared-memory repack) timed alone on constants, against variants
+// that each remove one ingredient:
+//   full     — as binomial.cu (254 levels, repack to NL-1 every 32 levels)
+//   noshfl   — the neighbour is the lane's own c[0] (wrong values, no SHFL)
+//   flat     — no repack: all 254 levels at 8 nodes per lane
+//   u4 / u16 — unroll 4 / 16 instead of 8
+//   half     — two pairs per warp, 16 nodes per lane, phases of 16 levels
+//              (binomial.cu's binomial_half: half the shuffles per node)
+// Grid: one warp per option pair, 4.19M pairs (the 8M-option config).
+// Build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a binomial_lattice.cu -o binomial_lattice
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
+constexpr int kThreads = 256;
+
+template <bool Shfl, int U>
+__device__ __forceinline__ int backward8(float2 (&c)[8], int j, int stop, float2 r) {
+#pragma unroll U
+  for (; j > stop; --j) {
+    float2 right;
+    if (Shfl)
+      right = make_float2(__shfl_down_sync(0xffffffffu, c[0].x, 1), __shfl_down_sync(0xffffffffu, c[0].y, 1));
+    else
+      right = c[0];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) c[k] = __ffma2_rn(r, c[k + 1], c[k]);
+    c[7] = __ffma2_rn(r, right, c[7]);
+  }
+  return j;
+}
+
+template <int NL, bool Shfl, int U, int G = 32>
+__device__ __forceinline__ float2 phases(float2 (&c)[NL], int j, float2 r, float2 s, float2* buf, unsigned lane) {
+  const int stop = NL > 1 ? G * (NL - 1) - 1 : 0;
+  if (j > stop) {
+#pragma unroll U
+    for (; j > stop; --j) {
+      float2 right;
+      if (Shfl)
+        right = make_float2(__shfl_down_sync(0xffffffffu, c[0].x, 1, G), __shfl_down_sync(0xffffffffu, c[0].y, 1, G));
+      else
+        right = c[0];
+#pragma unroll
+      for (int k = 0; k < NL - 1; ++k) c[k] = __ffma2_rn(r, c[k + 1], c[k]);
+      c[NL - 1] = __ffma2_rn(r, right, c[NL - 1]);
+    }
+    if constexpr (NL > 1) {
+#pragma unroll
+      for (int k = 0; k < NL; ++k) c[k] = __fmul2_rn(c[k], s);
+    }
+  }
+  if constexpr (NL == 1) {
+    return c[0];
+  } else {
+#pragma unroll
+    for (int k = 0; k < NL; ++k) buf[NL * lane + k] = c[k];
+    __syncwarp();
+    float2 h[NL - 1];
+#pragma unroll
+    for (int k = 0; k < NL - 1; ++k) h[k] = buf[(NL - 1) * lane + k];
+    __syncwarp();
+    return phases<NL - 1, Shfl, U, G>(h, j, r, s, buf, lane);
+  }
+}
+
+template <int Mode, int U>
+__global__ void __launch_bounds__(kThreads, 4) lattice(float* out, uint64_t pairs, int steps) {
+  __shared__ float2 buf_all[kThreads / 32][256];
+  const unsigned lane = threadIdx.x & 31u;
+  float2* buf = buf_all[threadIdx.x >> 5];
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (kThreads / 32);
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(kThreads / 32) + (threadIdx.x >> 5); w < pairs; w += warps) {
+    float2 c[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] = make_float2(1.0f + 1e-3f * (lane * 8 + k) + 1e-9f * w, 2.0f - 1e-3f * k);
+    const float2 r = make_float2(0.999f, 0.998f), s = make_float2(0.97f, 0.96f);
+    float2 v;
+    if (Mode == 0) v = phases<8, true, U>(c, steps, r, s, buf, lane);
+    else if (Mode == 1) v = phases<8, false, U>(c, steps, r, s, buf, lane);
+    else {
+      backward8<true, U>(c, steps, 0, r);
+      v = c[0];
+    }
+    if (lane == 0) out[w] = v.x + v.y;
+  }
+}
+
+template <bool Shfl, int MB>
+__global__ void __launch_bounds__(kThreads, MB) lattice_half(float* out, uint64_t pairs, int steps) {
+  __shared__ float2 buf_all[kThreads / 16][256];
+  const unsigned lane = threadIdx.x & 15u;
+  float2* buf = buf_all[threadIdx.x >> 4];
+  const uint64_t halves = static_cast<uint64_t>(gridDim.x) * (kThreads / 16);
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(kThreads / 16) + (threadIdx.x >> 4); w < pairs;
+       w += halves) {
+    float2 c[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) c[k] = make_float2(1.0f + 1e-3f * (lane * 16 + k) + 1e-9f * w, 2.0f - 1e-3f * k);
+    const float2 r = make_float2(0.999f, 0.998f), s = make_float2(0.97f, 0.96f);
+    const float2 v = phases<16, Shfl, 8, 16>(c, steps, r, s, buf, lane);
+    if (lane == 0) out[w] = v.x + v.y;
+  }
+}
+
+template <bool Shfl, int MB>
+void run_half(const char* name, float* d, uint64_t pairs) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const unsigned blocks = 148 * 8 * 16;
+  float best = 1e9f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(a);
+    lattice_half<Shfl, MB><<<blocks, kThreads>>>(d, pairs, 254);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (rep && ms < best) best = ms;
+  }
+  printf("%-8s MB=%d %.3f ms\n", name, MB, best);
+}
+
+template <int Mode, int U>
+void run(const char* name, float* d, uint64_t pairs) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const unsigned blocks = 148 * 8 * 16;
+  float best = 1e9f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(a);
+    lattice<Mode, U><<<blocks, kThreads>>>(d, pairs, 254);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (rep && ms < best) best = ms;
+  }
+  printf("%-8s %.3f ms\n", name, best);
+}
+
+int main() {
+  const uint64_t pairs = 1ull << 22;
+  float* d;
+  cudaMalloc(&d, pairs * 4);
+  run<0, 8>("full", d, pairs);
+  run<1, 8>("noshfl", d, pairs);
+  run<2, 8>("flat", d, pairs);
+  run<0, 4>("u4", d, pairs);
+  run<0, 16>("u16", d, pairs);
+  run_half<true, 2>("half", d, pairs);
+  run_half<true, 3>("half", d, pairs);
+  run_half<true, 4>("half", d, pairs);
+  run_half<false, 3>("halfnosh", d, pairs);
+  const cudaError_t e = cudaDeviceSynchronize();
+  printf("%s\n", cudaGetErrorString(e));
+  return 0;
+}
