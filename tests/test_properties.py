@@ -104,3 +104,62 @@ def test_validate_and_out_range_match_reference(ref, case):
         with pytest.raises(P.Error) as e:
             ours()
         assert e.value.code.value == rc - 1
+
+
+@st.composite
+def traces(draw):
+    n = draw(st.integers(1, 6))
+    ids = [f"dev{i}" for i in range(n)]
+    times = st.floats(0.001, 1e5, allow_nan=False)
+    packages, off = [], 0
+    for seq in range(draw(st.integers(1, 24))):
+        d = draw(st.integers(0, n - 1))
+        size = draw(st.integers(1, 5000))
+        t0 = draw(times)
+        t1 = t0 + draw(times)
+        packages.append({"seq": seq, "device_index": d, "device_id": ids[d], "offset_wg": off, "size_wg": size,
+                         "t_enqueue_ms": t0, "t_start_ms": t0, "t_end_ms": t1})
+        off += size
+    used = sorted({p["device_index"] for p in packages})
+    per_dev = {ids[d]: draw(times) for d in used}
+    raw = {"schema": 1, "clock_mode": "wall", "seed": 0, "init_ms": 0.0, "init_in_total": True,
+           "scheduler": "dynamic(n=1)", "t_total_ms": max(per_dev.values()) * draw(st.floats(1.0, 1.5)),
+           "per_device_time_ms": per_dev, "packages": packages,
+           "program": {"global_work_size": off, "local_work_size": 1, "total_work_groups": off, "kernel": "synthetic",
+                       "out_pattern": {"out_indices": 1, "work_items": 1}},
+           "devices": [{"id": i, "name": i, "computing_power": 1.0, "launch_overhead_ms": 0.0,
+                        "bandwidth_bytes_per_ms": 1.0, "min_package_work_groups": 1,
+                        "backend": {"kind": "simulated"}} for i in ids]}
+    solo = [draw(times) for _ in range(draw(st.integers(1, n)))]
+    ref_ms = draw(st.one_of(st.none(), times))
+    return raw, solo, ref_ms
+
+
+@SETTINGS
+@given(traces())
+def test_metrics_report_matches_reference(ref, case):
+    # make_report (metrics.hpp:23-117) on random traces: balance, speedup,
+    # s_max, efficiency, overhead and work shares equal the reference's
+    import ctypes
+    import json
+    raw, solo, ref_ms = case
+    lib = ref.lib
+    lib.ref_report_json.restype = ctypes.c_int64
+    lib.ref_report_json.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.c_uint32,
+                                    ctypes.c_double, ctypes.c_char_p, ctypes.c_uint64]
+    arr = (ctypes.c_double * len(solo))(*solo)
+    buf = ctypes.create_string_buffer(1 << 16)
+    n = lib.ref_report_json(json.dumps(raw).encode(), arr, len(solo), -1.0 if ref_ms is None else ref_ms, buf,
+                            1 << 16)
+    if n < 0:
+        with pytest.raises(P.Error):
+            P.make_report(P.ExecutionTrace(raw), solo, ref_ms)
+        return
+    exp = json.loads(buf.value.decode())
+    got = P.make_report(P.ExecutionTrace(raw), solo, ref_ms)
+    assert got.balance == exp["balance"]
+    assert got.speedup == exp["speedup"]
+    assert got.s_max == exp["s_max"]
+    assert got.efficiency == exp["efficiency"]
+    assert got.overhead_pct == exp.get("overhead_pct")
+    assert got.work_share == exp["work_share"]
