@@ -628,17 +628,26 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
 
     # --- native single-kernel baseline (overhead denominator) ---
     barrier()
-    native_k, native_e2e = [], []
+    native_k, native_host, native_e2e = [], [], []
     if wl.steps_per_run == 1:
+        n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         for _ in range(args.warmup + args.steps):
             flush_buf.zero_()  # same L2 state as the timed engine steps
             torch.cuda.synchronize()
+            # kernel-only time, and the native program's host call bracketed
+            # exactly like an engine step (launch + completion wait included)
+            n0.record(stream)
             native_k.append(eng.native_run(None, None)[0])
+            n1.record(stream)
+            n1.synchronize()
+            native_host.append(n0.elapsed_time(n1))
         for _ in range(max(1, args.steps)):
             native_e2e.append(eng.native_run(in_arrays, out_arrays)[1])
         native_k = native_k[args.warmup:]
+        native_host = native_host[args.warmup:]
     barrier()
     k_native = sorted(native_k)[len(native_k) // 2] if native_k else None
+    h_native = sorted(native_host)[len(native_host) // 2] if native_host else None
     t_native_e2e = sorted(native_e2e)[len(native_e2e) // 2] if native_e2e else None
 
     # --- roofline: vector peaks measured on this device ---
@@ -702,6 +711,10 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
                    "efficiency": k_native / (n * ms_dev) if k_native else None,
                    # runtime overhead of co-execution vs that native run (work-normalised: N * T_N vs T_1)
                    "overhead_pct_device": (n * ms_dev - k_native) / k_native * 100.0 if k_native else None,
+                   # the same against the native program's host-bracketed call (its launch and wait
+                   # latency counted like the engine's)
+                   "native_host_ms": h_native,
+                   "overhead_pct_vs_native_host": (n * ms_dev - h_native) / h_native * 100.0 if h_native else None,
                    "overhead_pct_e2e": (ms_e2e - t_native_e2e) / t_native_e2e * 100.0
                    if t_native_e2e and n == 1 else None,
                    "kernel_ms_per_step": kernel_ms / args.steps, "outputs_sane": bool(sane),
