@@ -736,6 +736,13 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
             # with no control flow (ecl_probe_mandel_mix): the attainable roof
             line["roofline"]["mix_ceiling_tflops"] = mix.value * n
             line["roofline"]["frac_of_mix_ceiling"] = achieved / (mix.value * n)
+    if wl.name == "ray":
+        # the same bound for the bit-exact tracer: a sphere test's 17 counted
+        # flops (workloads.RAY_FLOPS_PER_SPHERE_TEST) are 16 unfused FP32 lane
+        # operations (r^2 precomputed, no FMA contraction allowed), so even a
+        # saturated FP32 pipe reaches at most 17/32 of the FFMA peak
+        line["roofline"]["nonfma_ceiling_frac"] = 17.0 / 32.0
+        line["roofline"]["frac_of_nonfma_ceiling"] = (achieved / peak) / (17.0 / 32.0)
     if cpu is not None:
         line["cpu_baseline"] = cpu
     return line

@@ -78,15 +78,42 @@ __device__ __forceinline__ float root_of(float b, float disc) {
   t = add(-b, sq);
   return t > 1e-3f ? t : -1.0f;
 }
-__device__ __forceinline__ float2 ray_sphere2(V3 o, V3 d, float2 X, float2 Y, float2 Z, float2 RR) {
+// The packed part of the pair test: b and the discriminant of both spheres.
+__device__ __forceinline__ void pair_disc(V3 o, V3 d, float4 r0, float4 r1, float2& b, float2& disc) {
+  const float2 X = make_float2(r0.x, r0.y), Y = make_float2(r0.z, r0.w);
+  const float2 Z = make_float2(r1.x, r1.y), RR = make_float2(r1.z, r1.w);
   const float2 ox = __fadd2_rn(make_float2(o.x, o.x), neg2(X));
   const float2 oy = __fadd2_rn(make_float2(o.y, o.y), neg2(Y));
   const float2 oz = __fadd2_rn(make_float2(o.z, o.z), neg2(Z));
-  const float2 b = __fadd2_rn(__fadd2_rn(pmul(ox, make_float2(d.x, d.x)), pmul(oy, make_float2(d.y, d.y))),
-                              pmul(oz, make_float2(d.z, d.z)));
+  b = __fadd2_rn(__fadd2_rn(pmul(ox, make_float2(d.x, d.x)), pmul(oy, make_float2(d.y, d.y))),
+                 pmul(oz, make_float2(d.z, d.z)));
   const float2 cc = __fadd2_rn(__fadd2_rn(__fadd2_rn(pmul(ox, ox), pmul(oy, oy)), pmul(oz, oz)), neg2(RR));
-  const float2 disc = __fadd2_rn(pmul(b, b), neg2(cc));
-  return make_float2(root_of(b.x, disc.x), root_of(b.y, disc.y));
+  disc = __fadd2_rn(pmul(b, b), neg2(cc));
+}
+// Both spheres missed outright (disc < 0 for both: root_of would return -1
+// twice).  Most pair tests end here.
+__device__ __forceinline__ bool pair_misses(float2 disc) { return fmaxf(disc.x, disc.y) < 0.0f; }
+
+// Candidate scan: the packed discriminants of 32 sphere pairs from `first`
+// (pairs [first, first + n), n <= 32), branch-free, as a bit mask of the
+// pairs where at least one sphere has disc >= 0.  Full 32-pair chunks run
+// unrolled without guards.  The rare candidates are then resolved in
+// increasing pair order, which keeps the oracle's first-lowest-index choice
+// among equal distances.
+template <bool Full>
+__device__ __forceinline__ uint32_t scan_pairs(V3 o, V3 d, const float4 (*rec)[2], uint32_t first, uint32_t n) {
+  uint32_t mask = 0;
+#pragma unroll
+  for (uint32_t q = 0; q < 32; ++q) {
+    if (!Full && q >= n) break;
+    float2 b, disc;
+    pair_disc(o, d, rec[first + q][0], rec[first + q][1], b, disc);
+    mask |= pair_misses(disc) ? 0u : (1u << q);
+  }
+  return mask;
+}
+__device__ __forceinline__ uint32_t scan_chunk(V3 o, V3 d, const float4 (*rec)[2], uint32_t first, uint32_t n) {
+  return n >= 32 ? scan_pairs<true>(o, d, rec, first, 32) : scan_pairs<false>(o, d, rec, first, n);
 }
 
 struct Lane {
@@ -137,8 +164,8 @@ __global__ void __launch_bounds__(kThreads, MB)
     rec[4 + h] = c.z;
     rec[6 + h] = mul(c.w, c.w);
   }
-  // sphere pairs [0, pairs_end) go through ray_sphere2, an odd last one alone
-  const uint32_t pairs_end = ns & ~1u;
+  // sphere pairs [0, pairs_end) go through pair_disc, an odd last one alone
+  const uint32_t pairs_end = ns & ~1u, npairs = ns / 2;
 
   const float4* cam4 = scene + 2 * ns;
   const float4 cam = cam4[0];
@@ -206,17 +233,20 @@ __global__ void __launch_bounds__(kThreads, MB)
       // ---- one bounce (oracle: trace_pixel loop body) ----
       float tmin = 1e30f;
       int hit = -1;
-      for (uint32_t s = 0; s < pairs_end; s += 2) {
-        const float4 r0 = pair_rec[s / 2][0], r1 = pair_rec[s / 2][1];
-        const float2 t = ray_sphere2(L.o, L.d, make_float2(r0.x, r0.y), make_float2(r0.z, r0.w),
-                                     make_float2(r1.x, r1.y), make_float2(r1.z, r1.w));
-        if (t.x > 0.0f && t.x < tmin) {
-          tmin = t.x;
-          hit = static_cast<int>(s);
-        }
-        if (t.y > 0.0f && t.y < tmin) {
-          tmin = t.y;
-          hit = static_cast<int>(s + 1);
+      for (uint32_t c0 = 0; c0 < npairs; c0 += 32) {
+        for (uint32_t m = scan_chunk(L.o, L.d, pair_rec, c0, npairs - c0); m; m &= m - 1) {
+          const uint32_t pq = c0 + static_cast<uint32_t>(__ffs(m)) - 1, s = 2 * pq;
+          float2 b, disc;
+          pair_disc(L.o, L.d, pair_rec[pq][0], pair_rec[pq][1], b, disc);
+          const float2 t = make_float2(root_of(b.x, disc.x), root_of(b.y, disc.y));
+          if (t.x > 0.0f && t.x < tmin) {
+            tmin = t.x;
+            hit = static_cast<int>(s);
+          }
+          if (t.y > 0.0f && t.y < tmin) {
+            tmin = t.y;
+            hit = static_cast<int>(s + 1);
+          }
         }
       }
       if (pairs_end < ns) {
@@ -288,11 +318,14 @@ __global__ void __launch_bounds__(kThreads, MB)
         const V3 po{pp.x, pp.y, pp.z}, ln{g.x, g.y, g.z};
         const float dist = g.w;
         bool shadow = false;
-        for (uint32_t s = 0; s < pairs_end && !shadow; s += 2) {
-          const float4 r0 = pair_rec[s / 2][0], r1 = pair_rec[s / 2][1];
-          const float2 t = ray_sphere2(po, ln, make_float2(r0.x, r0.y), make_float2(r0.z, r0.w),
-                                       make_float2(r1.x, r1.y), make_float2(r1.z, r1.w));
-          shadow = (t.x > 0.0f && t.x < dist) || (t.y > 0.0f && t.y < dist);
+        for (uint32_t c0 = 0; c0 < npairs && !shadow; c0 += 32) {
+          for (uint32_t m = scan_chunk(po, ln, pair_rec, c0, npairs - c0); m && !shadow; m &= m - 1) {
+            const uint32_t pq = c0 + static_cast<uint32_t>(__ffs(m)) - 1;
+            float2 b, disc;
+            pair_disc(po, ln, pair_rec[pq][0], pair_rec[pq][1], b, disc);
+            const float2 t = make_float2(root_of(b.x, disc.x), root_of(b.y, disc.y));
+            shadow = (t.x > 0.0f && t.x < dist) || (t.y > 0.0f && t.y < dist);
+          }
         }
         if (!shadow && pairs_end < ns) {
           const float t = ray_sphere(po, ln, sph[pairs_end]);
