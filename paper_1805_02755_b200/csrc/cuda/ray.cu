@@ -94,18 +94,18 @@ __device__ __forceinline__ void pair_disc(V3 o, V3 d, float4 r0, float4 r1, floa
 // twice).  Most pair tests end here.
 __device__ __forceinline__ bool pair_misses(float2 disc) { return fmaxf(disc.x, disc.y) < 0.0f; }
 
-// Candidate scan: the packed discriminants of 32 sphere pairs from `first`
-// (pairs [first, first + n), n <= 32), branch-free, as a bit mask of the
-// pairs where at least one sphere has disc >= 0.  Full 32-pair chunks run
-// unrolled without guards.  The rare candidates are then resolved in
-// increasing pair order, which keeps the oracle's first-lowest-index choice
-// among equal distances.
-template <bool Full>
-__device__ __forceinline__ uint32_t scan_pairs(V3 o, V3 d, const float4 (*rec)[2], uint32_t first, uint32_t n) {
+// Candidate scan: the packed discriminants of up to 32 sphere pairs from
+// `first`, branch-free, as a bit mask of the pairs where at least one sphere
+// has disc >= 0.  Groups of G pairs run unrolled; the loops over groups stay
+// rolled (a 32-pair unroll of both scans overflowed the instruction cache:
+// ncu "no instruction" was the top stall).  The rare candidates are then
+// resolved in increasing pair order, which keeps the oracle's
+// first-lowest-index choice among equal distances.
+template <int G>
+__device__ __forceinline__ uint32_t scan_group(V3 o, V3 d, const float4 (*rec)[2], uint32_t first) {
   uint32_t mask = 0;
 #pragma unroll
-  for (uint32_t q = 0; q < 32; ++q) {
-    if (!Full && q >= n) break;
+  for (int q = 0; q < G; ++q) {
     float2 b, disc;
     pair_disc(o, d, rec[first + q][0], rec[first + q][1], b, disc);
     mask |= pair_misses(disc) ? 0u : (1u << q);
@@ -113,7 +113,13 @@ __device__ __forceinline__ uint32_t scan_pairs(V3 o, V3 d, const float4 (*rec)[2
   return mask;
 }
 __device__ __forceinline__ uint32_t scan_chunk(V3 o, V3 d, const float4 (*rec)[2], uint32_t first, uint32_t n) {
-  return n >= 32 ? scan_pairs<true>(o, d, rec, first, 32) : scan_pairs<false>(o, d, rec, first, n);
+  constexpr int kGroup = 16;
+  uint32_t mask = 0, q = 0;
+#pragma unroll 1
+  for (; q + kGroup <= n; q += kGroup) mask |= scan_group<kGroup>(o, d, rec, first + q) << q;
+#pragma unroll 1
+  for (; q < n; ++q) mask |= scan_group<1>(o, d, rec, first + q) << q;
+  return mask;
 }
 
 struct Lane {
@@ -420,21 +426,22 @@ cudaError_t launch(const KernelSpec& spec, const LaunchEnv& env, uint64_t first,
 cudaError_t launch_ray(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
   if (count == 0) return cudaSuccess;
   // ECL_RAY_MB: 128-thread CTAs per SM the registers are sized for.  Measured
-  // (8192^2): 6 -> 20.4 ms, 8 -> 19.0, 10 -> 18.0 (48 regs, small spill),
-  // 12 -> 18.0, 16 -> 18.5: occupancy beats the spills up to ~40 warps.
+  // (8192^2, candidate scans in 16-pair groups): 8 -> 13.04 ms (64
+  // registers), 10 -> 13.12 (48, spills); before the scans 10 was best.
   static const int env_mb = [] {
     const char* v = std::getenv("ECL_RAY_MB");
     return v ? std::atoi(v) : 0;
   }();
-  // ray@1: 8 CTAs/SM (no-spill register budget), ray@2: 6
-  const int mb = spec.variant == 1 ? 8 : spec.variant == 2 ? 6 : spec.variant == 0 ? 10 : env_mb;
+  // ray@1: 10 CTAs/SM (48 registers), ray@2: 6
+  const int mb = spec.variant == 1 ? 10 : spec.variant == 2 ? 6 : spec.variant == 0 ? 8 : env_mb;
   switch (mb) {
     case 6: return launch<6>(spec, env, first, count);
     case 7: return launch<7>(spec, env, first, count);
     case 8: return launch<8>(spec, env, first, count);
     case 12: return launch<12>(spec, env, first, count);
     case 16: return launch<16>(spec, env, first, count);
-    default: return launch<10>(spec, env, first, count);
+    case 10: return launch<10>(spec, env, first, count);
+    default: return launch<8>(spec, env, first, count);
   }
 }
 
