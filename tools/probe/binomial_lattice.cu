@@ -4,6 +4,7 @@
 // that each remove one ingredient:
 //   full     — as binomial.cu (254 levels, repack to NL-1 every 32 levels)
 //   noshfl   — the neighbour is the lane's own c[0] (wrong values, no SHFL)
+//   smemx    — the neighbour exchanged through shared memory instead
 //   flat     — no repack: all 254 levels at 8 nodes per lane
 //   u4 / u16 — unroll 4 / 16 instead of 8
 //   half     — two pairs per warp, 16 nodes per lane, phases of 16 levels
@@ -12,7 +13,7 @@
 //              shuffle pair per level serves all 8), repacked down a menu of
 //              node counts (64, 56, ..., 1) through shared memory
 // Grid: one warp per option pair, 4.19M pairs (the 8M-option config).
-// Measured (B200): full 14.9 ms, noshfl 9.9, flat 19.2, u4 15.6, u16 14.7,
+// Measured (B200): full 14.9 ms, noshfl 9.9, smemx 19.7, flat 19.2, u4 15.6, u16 14.7,
 // half 17.3-18.1 (12.3 without shuffles), g4 21.2 (16.3 without shuffles,
 // 163 registers: one CTA per SM).  Removing the shuffles saves ~5 ms in every
 // layout, also in g4 where they are 8x rarer per option: the cost is not the
@@ -41,14 +42,19 @@ __device__ __forceinline__ int backward8(float2 (&c)[8], int j, int stop, float2
   return j;
 }
 
-template <int NL, bool Shfl, int U, int G = 32>
+template <int NL, bool Shfl, int U, int G = 32, bool Smem = false>
 __device__ __forceinline__ float2 phases(float2 (&c)[NL], int j, float2 r, float2 s, float2* buf, unsigned lane) {
   const int stop = NL > 1 ? G * (NL - 1) - 1 : 0;
   if (j > stop) {
 #pragma unroll U
     for (; j > stop; --j) {
       float2 right;
-      if (Shfl)
+      if (Smem) {
+        float2* x = buf + 256 - 64 + 32 * (j & 1);  // double-buffered exchange slots
+        x[lane] = c[0];
+        __syncwarp();
+        right = x[(lane + 1) & 31];
+      } else if (Shfl)
         right = make_float2(__shfl_down_sync(0xffffffffu, c[0].x, 1, G), __shfl_down_sync(0xffffffffu, c[0].y, 1, G));
       else
         right = c[0];
@@ -71,7 +77,7 @@ __device__ __forceinline__ float2 phases(float2 (&c)[NL], int j, float2 r, float
 #pragma unroll
     for (int k = 0; k < NL - 1; ++k) h[k] = buf[(NL - 1) * lane + k];
     __syncwarp();
-    return phases<NL - 1, Shfl, U, G>(h, j, r, s, buf, lane);
+    return phases<NL - 1, Shfl, U, G, Smem>(h, j, r, s, buf, lane);
   }
 }
 
@@ -88,6 +94,7 @@ __global__ void __launch_bounds__(kThreads, 4) lattice(float* out, uint64_t pair
     const float2 r = make_float2(0.999f, 0.998f), s = make_float2(0.97f, 0.96f);
     float2 v;
     if (Mode == 0) v = phases<8, true, U>(c, steps, r, s, buf, lane);
+    else if (Mode == 3) v = phases<8, false, U, 32, true>(c, steps, r, s, buf, lane);
     else if (Mode == 1) v = phases<8, false, U>(c, steps, r, s, buf, lane);
     else {
       backward8<true, U>(c, steps, 0, r);
@@ -234,6 +241,7 @@ int main() {
   run<0, 8>("full", d, pairs);
   run<1, 8>("noshfl", d, pairs);
   run<2, 8>("flat", d, pairs);
+  run<3, 8>("smemx", d, pairs);
   run<0, 4>("u4", d, pairs);
   run<0, 16>("u16", d, pairs);
   run_half<true, 2>("half", d, pairs);
