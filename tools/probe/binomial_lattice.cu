@@ -5,6 +5,8 @@
 //   full     — as binomial.cu (254 levels, repack to NL-1 every 32 levels)
 //   noshfl   — the neighbour is the lane's own c[0] (wrong values, no SHFL)
 //   smemx    — the neighbour exchanged through shared memory instead
+//   dual     — two option pairs per warp advanced in lockstep (twice the
+//              independent work between exchanges)
 //   flat     — no repack: all 254 levels at 8 nodes per lane
 //   u4 / u16 — unroll 4 / 16 instead of 8
 //   half     — two pairs per warp, 16 nodes per lane, phases of 16 levels
@@ -13,7 +15,7 @@
 //              shuffle pair per level serves all 8), repacked down a menu of
 //              node counts (64, 56, ..., 1) through shared memory
 // Grid: one warp per option pair, 4.19M pairs (the 8M-option config).
-// Measured (B200): full 14.9 ms, noshfl 9.9, smemx 19.7, flat 19.2, u4 15.6, u16 14.7,
+// Measured (B200): full 14.9 ms, noshfl 9.9, smemx 19.7, dual 14.9, flat 19.2, u4 15.6, u16 14.7,
 // half 17.3-18.1 (12.3 without shuffles), g4 21.2 (16.3 without shuffles,
 // 163 registers: one CTA per SM).  Removing the shuffles saves ~5 ms in every
 // layout, also in g4 where they are 8x rarer per option: the cost is not the
@@ -79,6 +81,85 @@ __device__ __forceinline__ float2 phases(float2 (&c)[NL], int j, float2 r, float
     __syncwarp();
     return phases<NL - 1, Shfl, U, G, Smem>(h, j, r, s, buf, lane);
   }
+}
+
+template <int NL>
+__device__ __forceinline__ float2 phases2(float2 (&c)[NL], float2 (&e)[NL], int j, float2 r, float2 s, float2* buf,
+                                          unsigned lane, float2* out_e) {
+  const int stop = NL > 1 ? 32 * (NL - 1) - 1 : 0;
+  if (j > stop) {
+#pragma unroll 4
+    for (; j > stop; --j) {
+      const float2 rc = make_float2(__shfl_down_sync(0xffffffffu, c[0].x, 1), __shfl_down_sync(0xffffffffu, c[0].y, 1));
+      const float2 re = make_float2(__shfl_down_sync(0xffffffffu, e[0].x, 1), __shfl_down_sync(0xffffffffu, e[0].y, 1));
+#pragma unroll
+      for (int k = 0; k < NL - 1; ++k) {
+        c[k] = __ffma2_rn(r, c[k + 1], c[k]);
+        e[k] = __ffma2_rn(r, e[k + 1], e[k]);
+      }
+      c[NL - 1] = __ffma2_rn(r, rc, c[NL - 1]);
+      e[NL - 1] = __ffma2_rn(r, re, e[NL - 1]);
+    }
+  }
+  if constexpr (NL == 1) {
+    *out_e = e[0];
+    return c[0];
+  } else {
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      buf[NL * lane + k] = __fmul2_rn(c[k], s);
+      buf[256 + NL * lane + k] = __fmul2_rn(e[k], s);
+    }
+    __syncwarp();
+    float2 h[NL - 1], g[NL - 1];
+#pragma unroll
+    for (int k = 0; k < NL - 1; ++k) {
+      h[k] = buf[(NL - 1) * lane + k];
+      g[k] = buf[256 + (NL - 1) * lane + k];
+    }
+    __syncwarp();
+    return phases2<NL - 1>(h, g, j, r, s, buf, lane, out_e);
+  }
+}
+
+template <int MB>
+__global__ void __launch_bounds__(kThreads, MB) lattice_dual(float* out, uint64_t pairs, int steps) {
+  __shared__ float2 buf_all[kThreads / 32][512];
+  const unsigned lane = threadIdx.x & 31u;
+  float2* buf = buf_all[threadIdx.x >> 5];
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (kThreads / 32);
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(kThreads / 32) + (threadIdx.x >> 5); 2 * w < pairs;
+       w += warps) {
+    float2 c[8], e[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      c[k] = make_float2(1.0f + 1e-3f * (lane * 8 + k) + 1e-9f * w, 2.0f - 1e-3f * k);
+      e[k] = make_float2(1.5f + 1e-3f * (lane * 8 + k) + 1e-9f * w, 2.5f - 1e-3f * k);
+    }
+    const float2 r = make_float2(0.999f, 0.998f), s = make_float2(0.97f, 0.96f);
+    float2 ve;
+    const float2 v = phases2<8>(c, e, steps, r, s, buf, lane, &ve);
+    if (lane == 0) out[w] = v.x + v.y + ve.x + ve.y;
+  }
+}
+
+template <int MB>
+void run_dual(const char* name, float* d, uint64_t pairs) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const unsigned blocks = 148 * 8 * 16;
+  float best = 1e9f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(a);
+    lattice_dual<MB><<<blocks, kThreads>>>(d, pairs, 254);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (rep && ms < best) best = ms;
+  }
+  printf("%-8s MB=%d %.3f ms  %s\n", name, MB, best, cudaGetErrorString(cudaGetLastError()));
 }
 
 template <int Mode, int U>
@@ -248,6 +329,8 @@ int main() {
   run_half<true, 3>("half", d, pairs);
   run_half<true, 4>("half", d, pairs);
   run_half<false, 3>("halfnosh", d, pairs);
+  run_dual<2>("dual", d, pairs);
+  run_dual<3>("dual", d, pairs);
   run_g4<true, 1>("g4", d, pairs);
   run_g4<false, 1>("g4nosh", d, pairs);
   const cudaError_t e = cudaDeviceSynchronize();
