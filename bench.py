@@ -128,6 +128,17 @@ class Mandelbrot(Workload):
                             f"reference kernel workloads.hpp:78-100")
 
 
+class MandelbrotPeriodic(Mandelbrot):
+    # mandelbrot@14: the same counts (checked below), with the exact early exit
+    # for orbits that became periodic in FP64 (mandelbrot.cu mandel_persistent)
+    name = "mandelbrot_periodic"
+    kernel = "mandelbrot@14"
+    workload = ("mandelbrot 16384x16384 max_iter 2048, kernel mandelbrot@14: exact early exit for FP64-periodic "
+                "orbits (identical counts; not every reference iteration is executed)")
+    roofline_note = ("effective rate: algorithmic flops of the reference's full iteration count over the step time; "
+                     "this variant skips provably redundant iterations, so frac is not a pipe utilisation")
+
+
 class MandelbrotF32(Mandelbrot):
     name = "mandelbrot_f32"
     kernel = "mandelbrot_f32"
@@ -281,7 +292,7 @@ class Ray(Workload):
         return s, n, f"{n} pixels (every {stride}th of 8192^2); restated kernel oracle.c:orc_ray"
 
 
-WORKLOADS = {c.name: c for c in (Mandelbrot, MandelbrotF32, Gaussian, NBody, Binomial, Ray)}
+WORKLOADS = {c.name: c for c in (Mandelbrot, MandelbrotPeriodic, MandelbrotF32, Gaussian, NBody, Binomial, Ray)}
 
 
 # ---------------------------------------------------------------------------
@@ -736,6 +747,8 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
             # with no control flow (ecl_probe_mandel_mix): the attainable roof
             line["roofline"]["mix_ceiling_tflops"] = mix.value * n
             line["roofline"]["frac_of_mix_ceiling"] = achieved / (mix.value * n)
+    if getattr(wl, "roofline_note", None):
+        line["roofline"]["note"] = wl.roofline_note
     if wl.name == "ray":
         # the same bound for the bit-exact tracer: a sphere test's 17 counted
         # flops (workloads.RAY_FLOPS_PER_SPHERE_TEST) are 16 unfused FP32 lane

@@ -66,8 +66,9 @@ def test_acceptance_c1_vecscale(gpu_available, oracle, sched, n_dev):
     (1024, 2048, 0xba7913ec187cbc5f, 375815484, 180918),
     (4096, 2048, 0xb928fb12dcaf9ffa, 6009619671, 2892623),
 ])
-def test_mandelbrot_golden_checksums(gpu_available, oracle, w, it, fnv, total, inside):
-    _, res = run_engine(W.mandelbrot_spec(w, w, it), P.HGuidedConfig(), n_dev=1)
+@pytest.mark.parametrize("kernel", ["mandelbrot", "mandelbrot@14"])
+def test_mandelbrot_golden_checksums(gpu_available, oracle, w, it, fnv, total, inside, kernel):
+    _, res = run_engine(W.mandelbrot_spec(w, w, it, kernel=kernel), P.HGuidedConfig(), n_dev=1)
     quad = res.outputs[0].view(np.uint32).reshape(-1, 4)
     assert (quad == quad[:, :1]).all(), "4:1 pattern: four identical counts per pixel"
     counts = np.ascontiguousarray(quad[:, 0])
@@ -76,10 +77,12 @@ def test_mandelbrot_golden_checksums(gpu_available, oracle, w, it, fnv, total, i
     assert oracle.fnv1a64(counts) == fnv
 
 
-def test_mandelbrot_config_checksum(gpu_available, oracle):
-    """16384^2 x 2048, HGuided: the BASELINE config, bit-exact."""
+@pytest.mark.parametrize("kernel", ["mandelbrot", "mandelbrot@14"])
+def test_mandelbrot_config_checksum(gpu_available, oracle, kernel):
+    """16384^2 x 2048, HGuided: the BASELINE config, bit-exact,
+    also for the periodic-orbit early exit (mandelbrot@14)."""
     w, it = 16384, 2048
-    spec = W.mandelbrot_spec(w, w, it)
+    spec = W.mandelbrot_spec(w, w, it, kernel=kernel)
     prog = P.validate_program(spec)
     with P.Engine(P.EngineConfig(devices(1), P.HGuidedConfig()), prog) as e:
         e.run_into([], None)  # device-resident
@@ -289,7 +292,7 @@ def test_specialization_must_be_a_variant_of_the_program_kernel(gpu_available):
     assert e.value.code == P.ErrorCode.ConfigError
 
 
-@pytest.mark.parametrize("kernel", [f"mandelbrot@{v}" for v in range(14)] + ["mandelbrot_f32@0", "mandelbrot_f32@1"])
+@pytest.mark.parametrize("kernel", [f"mandelbrot@{v}" for v in range(15)] + ["mandelbrot_f32@0", "mandelbrot_f32@1"])
 def test_every_mandelbrot_variant_is_bit_exact(gpu_available, oracle, kernel):
     # tuning variants selectable per device must all reproduce the reference
     w, h, it = 640, 480, 1000
