@@ -261,6 +261,14 @@ cudaError_t ring_setup(ecl_gpu* g) {
     cudaFreeHost(f);
     return e;
   }
+  // Drivers can refuse stream memory operations (module option): probe with
+  // a wait that is already satisfied and keep the landing zone if refused.
+  if (wait_value_fn()(g->copy[0], reinterpret_cast<unsigned long long>(fd), 0, 0 /* GEQ */) != 0) {
+    cudaGetLastError();
+    pinned_free(p);
+    cudaFreeHost(f);
+    return cudaSuccess;
+  }
   g->ring = static_cast<uint32_t*>(p);
   g->ring_released = static_cast<uint32_t*>(f);
   g->ring_released_dev = fd;
