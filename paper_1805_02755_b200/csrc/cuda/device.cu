@@ -136,6 +136,7 @@ struct ecl_gpu {
   void* ring_released_dev = nullptr;  // device address of ring_released
   std::vector<uint32_t> ring_uses;    // copies issued per slot
   uint32_t ring_slots = 0, ring_next = 0;
+  bool ring_tried = false;
   uint64_t ring_items = 0;
   uint64_t input_gen = 0;  // see next_input_gen()
   // Streamed inputs (ecl_gpu_set_streamed_inputs): uploads are enqueued on
@@ -239,7 +240,8 @@ cudaError_t ring_setup(ecl_gpu* g) {
     const long long n = v ? std::atoll(v) : 2048;
     return n > 0 ? static_cast<uint64_t>(n) : uint64_t{2048};
   }();
-  if (g->ring || ring_slots == 0 || !wait_value_fn()) return cudaSuccess;
+  if (g->ring || g->ring_tried || ring_slots == 0 || !wait_value_fn()) return cudaSuccess;
+  g->ring_tried = true;  // one attempt per device: a refusal keeps the landing zone
   const uint64_t items = slot_kb * 1024 / 4;
   const uint64_t auto_slots = 2ull * ecl::widen_workers() + 4;
   const uint32_t slots =
