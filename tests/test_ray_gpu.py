@@ -19,6 +19,11 @@ def devices(n):
     (320, 200, 64, 4, 3, P.HGuidedConfig()),
     (128, 96, 17, 2, 2, P.DynamicConfig(23)),
     (160, 120, 64, 0, 1, P.StaticConfig()),
+    # more than one 32-pair candidate-scan chunk: a full chunk + a 16-pair
+    # group + an odd sphere; three chunks + 4 single pairs; the maximum
+    (96, 64, 97, 3, 1, P.StaticConfig()),
+    (96, 64, 200, 2, 2, P.HGuidedConfig()),
+    (64, 48, 256, 4, 1, P.DynamicConfig(5)),
 ])
 def test_ray_bit_exact(gpu_available, oracle, w, h, ns, depth, n_dev, sched):
     scene = W.ray_scene(ns, seed=42)
