@@ -272,7 +272,10 @@ class Ray(Workload):
         return load_json("tests/golden/ray_counts.json")["8192x8192"]["flops"]
 
     def min_package(self, n):
-        return 148 * 4
+        # 4 work-groups per SM per GPU in the job: the same package count per
+        # device at every N (virtual model, tools/virtual_scaling_ray.py:
+        # HGuided 0.957 at 8 GPUs with 4736 vs 0.919 with 592)
+        return 148 * 4 * max(1, n)
 
     def host_inputs(self):
         return [self.W.ray_scene(self.SPHERES, seed=42)]
