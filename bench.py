@@ -88,6 +88,8 @@ class Workload:
 
 
 class Mandelbrot(Workload):
+    # attainable fraction of the FP64 DFMA peak and why (bench line roofline.ceiling_*)
+    ceiling = (8.0 / 12.0, "8 counted flops in 6 unfused FP64 instructions per iteration (bit-exact: no contraction)")
     name = "mandelbrot"
     W_PX, ITERS, LWS = 16384, 2048, 256
     VIEWPORT = (-2.5, -1.25, 1.0, 1.25)
@@ -145,6 +147,7 @@ class MandelbrotF32(Mandelbrot):
     dtype = "f32"
     bound = "fp32"
     SUM_COUNT = 96_141_248_575  # FP32 restatement
+    ceiling = (8.0 / 12.0, "8 counted flops in 6 unfused FP32 lane-ops per iteration (packed pairs)")
     workload = "mandelbrot_f32 16384x16384 max_iter 2048 (FP32 restatement, parity unpinned)"
 
     def flops(self):
@@ -156,6 +159,7 @@ class MandelbrotF32(Mandelbrot):
 
 
 class Gaussian(Workload):
+    ceiling = (1.0, "every counted flop pair is one FFMA lane-op")
     name = "gaussian"
     WIDTH = HEIGHT = 4096
     F = 31
@@ -190,6 +194,7 @@ class Gaussian(Workload):
 
 
 class NBody(Workload):
+    ceiling = (20.0 / 24.0, "20 counted flops per interaction in 12 FP32 lane-ops (+1 MUFU)")
     name = "nbody"
     N = 1 << 20
     steps_per_run = 10
@@ -224,6 +229,8 @@ class NBody(Workload):
 
 
 class Binomial(Workload):
+    ceiling = (1.5 * 64770.0 / 73152.0,
+               "3 counted flops per node in one FMA lane-op (scaled lattice); 64770 live of 73152 slots per pair")
     name = "binomial"
     OPTIONS = 8 * 1024 * 1024
     STEPS = 254
@@ -257,6 +264,7 @@ class Binomial(Workload):
 
 
 class Ray(Workload):
+    ceiling = (17.0 / 32.0, "17 counted flops per sphere test in 16 unfused FP32 lane-ops (bit-exact)")
     name = "ray"
     WIDTH = HEIGHT = 8192
     SPHERES, DEPTH = 64, 4
@@ -750,6 +758,11 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
             # with no control flow (ecl_probe_mandel_mix): the attainable roof
             line["roofline"]["mix_ceiling_tflops"] = mix.value * n
             line["roofline"]["frac_of_mix_ceiling"] = achieved / (mix.value * n)
+    if getattr(wl, "ceiling", None) and not getattr(wl, "roofline_note", None):
+        c, why = wl.ceiling
+        line["roofline"]["ceiling_frac"] = c
+        line["roofline"]["frac_of_ceiling"] = (achieved / peak) / c
+        line["roofline"]["ceiling_basis"] = why
     if getattr(wl, "roofline_note", None):
         line["roofline"]["note"] = wl.roofline_note
     if wl.name == "ray":
