@@ -7,6 +7,10 @@
 //   smemx    — the neighbour exchanged through shared memory instead
 //   dual     — two option pairs per warp advanced in lockstep (twice the
 //              independent work between exchanges)
+//   halo4    — like flat, but each lane also carries a 4-node halo (the
+//              neighbour's first 4 nodes, updated redundantly) and exchanges
+//              it every 4 levels: a quarter of the exchange events, the same
+//              shuffled words, +25 % FFMA2
 //   flat     — no repack: all 254 levels at 8 nodes per lane
 //   u4 / u16 — unroll 4 / 16 instead of 8
 //   half     — two pairs per warp, 16 nodes per lane, phases of 16 levels
@@ -15,7 +19,7 @@
 //              shuffle pair per level serves all 8), repacked down a menu of
 //              node counts (64, 56, ..., 1) through shared memory
 // Grid: one warp per option pair, 4.19M pairs (the 8M-option config).
-// Measured (B200): full 14.9 ms, noshfl 9.9, smemx 19.7, dual 14.9, flat 19.2, u4 15.6, u16 14.7,
+// Measured (B200): full 14.9 ms, noshfl 9.9, smemx 19.7, dual 14.9, flat 19.2, halo4 20.4 (vs flat), u4 15.6, u16 14.7,
 // half 17.3-18.1 (12.3 without shuffles), g4 21.2 (16.3 without shuffles,
 // 163 registers: one CTA per SM).  Removing the shuffles saves ~5 ms in every
 // layout, also in g4 where they are 8x rarer per option: the cost is not the
@@ -162,6 +166,24 @@ void run_dual(const char* name, float* d, uint64_t pairs) {
   printf("%-8s MB=%d %.3f ms  %s\n", name, MB, best, cudaGetErrorString(cudaGetLastError()));
 }
 
+__device__ __forceinline__ void halo4_steps(float2 (&c)[8], int j, int stop, float2 r) {
+  float2 h[4];
+  for (; j > stop;) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      h[k] = make_float2(__shfl_down_sync(0xffffffffu, c[k].x, 1), __shfl_down_sync(0xffffffffu, c[k].y, 1));
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {  // 4 levels on own + halo nodes (halo shrinks by one per level)
+#pragma unroll
+      for (int k = 0; k < 7; ++k) c[k] = __ffma2_rn(r, c[k + 1], c[k]);
+      c[7] = __ffma2_rn(r, h[0], c[7]);
+#pragma unroll
+      for (int k = 0; k < 3 - s; ++k) h[k] = __ffma2_rn(r, h[k + 1], h[k]);
+    }
+    j -= 4;
+  }
+}
+
 template <int Mode, int U>
 __global__ void __launch_bounds__(kThreads, 4) lattice(float* out, uint64_t pairs, int steps) {
   __shared__ float2 buf_all[kThreads / 32][256];
@@ -176,6 +198,10 @@ __global__ void __launch_bounds__(kThreads, 4) lattice(float* out, uint64_t pair
     float2 v;
     if (Mode == 0) v = phases<8, true, U>(c, steps, r, s, buf, lane);
     else if (Mode == 3) v = phases<8, false, U, 32, true>(c, steps, r, s, buf, lane);
+    else if (Mode == 4) {
+      halo4_steps(c, steps, 0, r);
+      v = c[0];
+    }
     else if (Mode == 1) v = phases<8, false, U>(c, steps, r, s, buf, lane);
     else {
       backward8<true, U>(c, steps, 0, r);
@@ -323,6 +349,7 @@ int main() {
   run<1, 8>("noshfl", d, pairs);
   run<2, 8>("flat", d, pairs);
   run<3, 8>("smemx", d, pairs);
+  run<4, 8>("halo4", d, pairs);
   run<0, 4>("u4", d, pairs);
   run<0, 16>("u16", d, pairs);
   run_half<true, 2>("half", d, pairs);
