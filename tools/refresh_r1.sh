@@ -1,5 +1,5 @@
 set -x
-for w in mandelbrot gaussian binomial nbody ray mandelbrot_f32; do
+for w in mandelbrot gaussian binomial nbody ray mandelbrot_f32 mandelbrot_periodic; do
   timeout 900 python bench.py --workload $w > gpurun_out/bench3_$w.json 2> gpurun_out/bench3_$w.err
   echo "$w rc=$?"
 done
