@@ -12,6 +12,7 @@
 #include <emmintrin.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <condition_variable>
 #include <cstdint>
@@ -54,7 +55,8 @@ class Pool {
     // Leave two cores for the engine's device threads and CUDA's own threads:
     // a descheduled widen worker stalls its piece for a whole time slice.
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const unsigned n = hw > 4 ? hw - 2 : hw;
+    unsigned n = hw > 4 ? hw - 2 : hw;
+    if (const char* v = std::getenv("ECL_WIDEN_THREADS"); v && std::atoi(v) > 0) n = static_cast<unsigned>(std::atoi(v));
     for (unsigned i = 0; i < n; ++i) threads_.emplace_back([this] { loop(); });
   }
   ~Pool() {
