@@ -474,6 +474,22 @@ def run_reference(args, world, rank):
     return 0
 
 
+def shared_out_dir(args):
+    """Directory for the ranks' shared output file: /dev/shm when it has room
+    for the workload's outputs (plus 10 %), else the first of $TMPDIR, /tmp
+    that has."""
+    import numpy as np
+    import paper_1805_02755_b200 as P
+    from paper_1805_02755_b200 import workloads as W
+    need = 1.1 * sum(b.size_bytes() for b in WORKLOADS[args.workload](P, W, np).spec().out_buffers)
+    for d in ("/dev/shm", os.environ.get("TMPDIR", ""), "/tmp"):
+        if d and os.path.isdir(d):
+            st = os.statvfs(d)
+            if st.f_bavail * st.f_frsize >= need:
+                return d
+    return "/dev/shm"
+
+
 class SharedHostBuffer:
     """A /dev/shm-backed host buffer every rank maps and page-locks: each
     process D2H-copies its own packages' slices into the one result."""
@@ -525,10 +541,14 @@ def run_ours(args, world, rank, local):
             td.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:  # more ranks than GPUs (a one-GPU test box): NCCL refuses shared devices
             td.init_process_group("gloo")
-        tag = [f"{os.getpid():x}{int.from_bytes(os.urandom(4), 'little'):x}" if rank == 0 else None]
+        # rank 0 names the run and picks where the shared output lives: /dev/shm
+        # unless that tmpfs is too small for the outputs (a container default
+        # of 64 MB would SIGBUS when the buffer is page-locked), then /tmp
+        tag = [f"{os.getpid():x}{int.from_bytes(os.urandom(4), 'little'):x}", shared_out_dir(args)] \
+            if rank == 0 else [None, None]
         td.broadcast_object_list(tag, src=0)
         shared = {"name": f"/ecl_bench_{tag[0]}", "rank": rank, "world": world, "local_devices": [rank],
-                  "host_buffer": f"/dev/shm/ecl_bench_out_{tag[0]}"}
+                  "host_buffer": os.path.join(tag[1], f"ecl_bench_out_{tag[0]}")}
     n = world if dist else args.gpus
     torch.cuda.set_device((local % torch.cuda.device_count()) if dist else 0)
 
