@@ -151,7 +151,9 @@ cudaError_t launch_nbody(const KernelSpec& spec, const LaunchEnv& env, uint64_t 
     const char* v = std::getenv("ECL_NBODY_SPLIT");
     return v ? std::atoi(v) : 0;
   }();
-  static const int env_pairs = [] {  // ECL_NBODY_PAIRS: target pairs per thread (2 measured 4.6 % faster than 1)
+  // ECL_NBODY_PAIRS: target pairs per thread (2 measured 4.6 % faster than 1;
+  // 3 pairs — six targets, 78 registers, 3 CTAs/SM — 435 vs 428 ms per step)
+  static const int env_pairs = [] {
     const char* v = std::getenv("ECL_NBODY_PAIRS");
     return v && std::atoi(v) == 1 ? 1 : 2;
   }();
