@@ -753,6 +753,71 @@ int ecl_gpu_launch(ecl_gpu* g, const ecl_kernel* k, uint64_t first_item, uint64_
   return ecl_gpu_submit(g, seq, first_item / lws, item_count / lws, nullptr, done, user);
 }
 
+// Streamed inputs (ecl_gpu_set_streamed_inputs): enqueues on the H2D stream
+// the prefix of every still-pending input that items [first, first+count)
+// read, and makes `st` wait for the latest upload.
+static int stream_inputs_for(ecl_gpu* g, const ecl::KernelSpec& s, uint64_t first, uint64_t count, cudaStream_t st) {
+  bool moved = false;
+  for (uint32_t i = 0; i < g->pending_in.size(); ++i) {
+    if (!g->pending_in[i]) continue;
+    const uint64_t need = ecl::input_bytes_needed(s, i, first, count), up = g->up_bytes[i];
+    if (need > up) {
+      ECL_CK(cudaMemcpyAsync(static_cast<char*>(g->in[i]) + up, g->pending_in[i] + up, need - up,
+                             cudaMemcpyHostToDevice, g->h2d));
+      g->up_bytes[i] = need;
+      moved = true;
+    }
+    if (g->up_bytes[i] >= g->in_bytes[i]) g->pending_in[i] = nullptr;
+  }
+  if (moved) {
+    ECL_CK(cudaEventRecord(g->up_ev, g->h2d));
+    g->up_live = true;
+  }
+  if (g->up_live) ECL_CK(cudaStreamWaitEvent(st, g->up_ev, 0));
+  return ECL_OK;
+}
+
+// The compact copies of one piece (items [first, first+count), one uint32
+// each) on copy stream `cp`, and the host widening of each into `dst` (the
+// piece's slice of the caller's output, `replicate` values per item).  The
+// copy may go in chunks (ECL_WIDEN_CHUNK), each widened as soon as it lands;
+// measured on the 16-core Xeon host: 2^20-item chunks = whole pieces (54.5
+// vs 54.9 ms), smaller chunks slower (API cost), so without the staging ring
+// the default is one copy per piece.  With the ring, every chunk is one slot.
+static int enqueue_compact_copies(ecl_gpu* g, Slot& slot, const ecl::KernelSpec& s, uint64_t first, uint64_t count,
+                                  uint32_t* dst, cudaStream_t cp, size_t* piece_no) {
+  const uint64_t chunk = g->ring ? g->ring_items : g->widen_chunk_items;
+  for (uint64_t c0 = 0; c0 < count; c0 += chunk) {
+    const uint64_t cn = std::min(chunk, count - c0);
+    uint32_t* land = g->compact_host ? g->compact_host + first + c0 : nullptr;
+    uint32_t* release = nullptr;
+    uint32_t release_value = 0;
+    if (g->ring) {  // next staging slot, once its previous contents are widened
+      const uint32_t r = g->ring_next;
+      g->ring_next = (r + 1) % g->ring_slots;
+      const uint32_t uses = g->ring_uses[r]++;
+      const unsigned long long flag = reinterpret_cast<unsigned long long>(g->ring_released_dev) + 4ull * r;
+      if (wait_value_fn()(cp, flag, uses, 0 /* CU_STREAM_WAIT_VALUE_GEQ */) != 0)
+        return fail(ECL_KERNEL_PANIC, "staging ring: stream wait failed");
+      land = g->ring + static_cast<uint64_t>(r) * g->ring_items;
+      release = g->ring_released + r;
+      release_value = uses + 1;
+    }
+    ECL_CK(cudaMemcpyAsync(land, g->compact_dev + first + c0, cn * sizeof(uint32_t), cudaMemcpyDeviceToHost, cp));
+    if (slot.piece_done.size() <= *piece_no) {
+      cudaEvent_t ev;
+      // blocking-sync: widen workers sleep on it instead of spinning a core
+      ECL_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventBlockingSync));
+      slot.piece_done.push_back(ev);
+    }
+    cudaEvent_t ev = slot.piece_done[(*piece_no)++];
+    ECL_CK(cudaEventRecord(ev, cp));
+    ecl::widen_async(g->ordinal, ev, land, dst + c0 * s.replicate, cn, s.replicate, &slot.widen, release,
+                     release_value);
+  }
+  return ECL_OK;
+}
+
 int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_wg, void* const* host_outputs,
                    ecl_done_fn done, void* user) {
   if (!g->spec) return fail(ECL_CONFIG_ERROR, "submit before bind");
@@ -819,24 +884,8 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
     if (widen) env.compact = g->compact_dev;
     const uint64_t n_wg = std::min(piece_wg, offset_wg + size_wg - wg);
     const uint64_t first = wg * s.lws, count = n_wg * s.lws;
-    if (streaming || g->up_live) {  // inputs this piece reads: enqueue the missing prefix, wait for it
-      bool moved = false;
-      for (uint32_t i = 0; i < g->pending_in.size(); ++i) {
-        if (!g->pending_in[i]) continue;
-        const uint64_t need = ecl::input_bytes_needed(s, i, first, count), up = g->up_bytes[i];
-        if (need > up) {
-          ECL_CK(cudaMemcpyAsync(static_cast<char*>(g->in[i]) + up, g->pending_in[i] + up, need - up,
-                                 cudaMemcpyHostToDevice, g->h2d));
-          g->up_bytes[i] = need;
-          moved = true;
-        }
-        if (g->up_bytes[i] >= g->in_bytes[i]) g->pending_in[i] = nullptr;
-      }
-      if (moved) {
-        ECL_CK(cudaEventRecord(g->up_ev, g->h2d));
-        g->up_live = true;
-      }
-      if (g->up_live) ECL_CK(cudaStreamWaitEvent(st, g->up_ev, 0));
+    if (streaming || g->up_live) {
+      if (int rc = stream_inputs_for(g, s, first, count, st)) return rc;
     }
     cudaError_t e = ecl::launch_kernel(s, env, first, count);
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
@@ -852,40 +901,9 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
     // widen_per_8 of every 8 pieces go compact + host widening, the rest are
     // copied whole: balances PCIe bytes against host-DRAM traffic.
     if (widen && (g->piece_counter++ % 8) < g->widen_per_8) {
-      // The compact copy may go in chunks (ECL_WIDEN_CHUNK), each widened as
-      // soon as it lands.  Measured on the 16-core Xeon host: 2^20-item
-      // chunks = whole pieces (54.5 vs 54.9 ms), smaller chunks slower (API
-      // cost), so the default is one copy per piece.
-      const uint64_t chunk = g->ring ? g->ring_items : g->widen_chunk_items;
-      for (uint64_t c0 = 0; c0 < count; c0 += chunk) {
-        const uint64_t cn = std::min(chunk, count - c0);
-        uint32_t* land = g->compact_host ? g->compact_host + first + c0 : nullptr;
-        uint32_t* release = nullptr;
-        uint32_t release_value = 0;
-        if (g->ring) {  // next staging slot, once its previous contents are widened
-          const uint32_t r = g->ring_next;
-          g->ring_next = (r + 1) % g->ring_slots;
-          const uint32_t uses = g->ring_uses[r]++;
-          const unsigned long long flag = reinterpret_cast<unsigned long long>(g->ring_released_dev) + 4ull * r;
-          if (wait_value_fn()(cp, flag, uses, 0 /* CU_STREAM_WAIT_VALUE_GEQ */) != 0)
-            return fail(ECL_KERNEL_PANIC, "staging ring: stream wait failed");
-          land = g->ring + static_cast<uint64_t>(r) * g->ring_items;
-          release = g->ring_released + r;
-          release_value = uses + 1;
-        }
-        ECL_CK(cudaMemcpyAsync(land, g->compact_dev + first + c0, cn * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                               cp));
-        if (slot.piece_done.size() <= piece_no) {
-          cudaEvent_t ev;
-          // blocking-sync: widen workers sleep on it instead of spinning a core
-          ECL_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventBlockingSync));
-          slot.piece_done.push_back(ev);
-        }
-        cudaEvent_t ev = slot.piece_done[piece_no++];
-        ECL_CK(cudaEventRecord(ev, cp));
-        ecl::widen_async(g->ordinal, ev, land, static_cast<uint32_t*>(host_outputs[0]) + p_off + c0 * s.replicate,
-                         cn, s.replicate, &slot.widen, release, release_value);
-      }
+      if (int rc = enqueue_compact_copies(g, slot, s, first, count, static_cast<uint32_t*>(host_outputs[0]) + p_off,
+                                          cp, &piece_no))
+        return rc;
       continue;
     }
     for (size_t b = 0; b < g->out.size(); ++b) {
