@@ -331,3 +331,22 @@ def test_staging_ring_wraps_and_matches_oracle(gpu_available, oracle, tmp_path, 
                        timeout=300)
     assert r.returncode == 0, r.stderr
     assert np.array_equal(np.load(f), expand_4to1(oracle.mandelbrot(512, 256, 300)))
+
+
+@pytest.mark.parametrize("kernel", ["mandelbrot", "mandelbrot@14"])
+def test_mandelbrot_random_viewports(gpu_available, oracle, kernel):
+    # seeded random windows: zooms into the cardioid, the period-2 bulb, the
+    # boundary and the exterior, odd sizes and iteration limits (1..3000),
+    # against the oracle's FP64 restatement (SURVEY §8c op order)
+    rng = np.random.default_rng(2024)
+    for _ in range(12):
+        w, h = int(rng.integers(16, 220)), int(rng.integers(8, 160))
+        it = int(rng.choice([1, 2, 31, 32, 33, 100, 777, 2048, 3000]))
+        centers = [(-0.1, 0.0), (-1.0, 0.0), (-0.75, 0.1), (0.3, 0.5), (-1.8, 0.0), (0.26, 0.0)]
+        cx, cy = centers[int(rng.integers(len(centers)))]
+        span = float(10.0 ** rng.uniform(-6, 0.5))
+        vp = (cx - span, cy - span * h / w, cx + span, cy + span * h / w)
+        spec = W.mandelbrot_spec(w, h, it, viewport=vp, lws=1, kernel=kernel)
+        _, res = run_engine(spec, P.HGuidedConfig(), n_dev=2)
+        exp = oracle.mandelbrot(w, h, it, viewport=vp)
+        assert np.array_equal(res.outputs[0].view(np.uint32), expand_4to1(exp)), (w, h, it, vp)
