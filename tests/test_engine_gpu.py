@@ -350,3 +350,18 @@ def test_mandelbrot_random_viewports(gpu_available, oracle, kernel):
         _, res = run_engine(spec, P.HGuidedConfig(), n_dev=2)
         exp = oracle.mandelbrot(w, h, it, viewport=vp)
         assert np.array_equal(res.outputs[0].view(np.uint32), expand_4to1(exp)), (w, h, it, vp)
+
+
+@pytest.mark.parametrize("center", [(0.25, 0.0), (-0.75, 0.0), (-1.25, 0.0)])
+def test_periodic_exit_near_parabolic_points(gpu_available, oracle, center):
+    # orbits near the cusp (c = 1/4) and the bulb junctions converge
+    # slowly and may become periodic only after tens of thousands of
+    # iterations or never: the early exit must still give the reference
+    # counts at a 50000-iteration limit
+    cx, cy = center
+    w = h = 64
+    span = 1e-3
+    vp = (cx - span, cy - span, cx + span, cy + span)
+    spec = W.mandelbrot_spec(w, h, 50000, viewport=vp, lws=64, kernel="mandelbrot@14")
+    _, res = run_engine(spec, P.DynamicConfig(5), n_dev=1)
+    assert np.array_equal(res.outputs[0].view(np.uint32), expand_4to1(oracle.mandelbrot(w, h, 50000, viewport=vp)))
