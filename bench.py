@@ -164,7 +164,9 @@ class Gaussian(Workload):
     WIDTH = HEIGHT = 4096
     F = 31
     workload = "gaussian 4096x4096 float image, 31x31 filter (sigma 5), clamp-to-edge, static, single device"
-    copy_split = 1 << 20  # 16 row bands: H2D of band k+1 and D2H of band k-1 overlap band k
+    # 32 row bands: H2D of band k+1 and D2H of band k-1 overlap band k (e2e measured:
+    # 2^19 items 1.66-1.74 ms, 2^20 1.81-1.89, 2^21 1.96, 2^18 1.93, 2^17 2.30)
+    copy_split = 1 << 19
 
     def spec(self):
         return self.W.gaussian_spec(self.WIDTH, self.HEIGHT, self.F)
