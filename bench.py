@@ -271,6 +271,9 @@ class Ray(Workload):
     WIDTH = HEIGHT = 8192
     SPHERES, DEPTH = 64, 4
     workload = "ray 8192x8192, 64 spheres + plane, 3 lights, shadows, reflections depth 4, hguided"
+    # smaller sub-launches shorten the last copy's tail (e2e measured: 2^20 items
+    # 19.7-19.8 ms, 2^21 19.9-20.2, 2^22 19.9-20.0, 2^23 20.3-20.4)
+    copy_split = 1 << 20
 
     def spec(self):
         return self.W.ray_spec(self.WIDTH, self.HEIGHT, self.SPHERES, self.DEPTH)
