@@ -563,6 +563,25 @@ class Engine:
             ptrs.append(p)
         return ptrs
 
+    def _check_outputs(self, outputs: Sequence) -> List[int]:
+        """Every output must be a writable, C-contiguous buffer of exactly the
+        descriptor's size: the native side writes spec-sized slices."""
+        outs = self._prog.spec().out_buffers
+        if len(outputs) != len(outs):
+            raise Error(ErrorCode.ConfigError, f"expected {len(outs)} output buffers, got {len(outputs)}")
+        ptrs = []
+        for b, a in zip(outs, outputs):
+            if a is None:
+                ptrs.append(None)
+                continue
+            if isinstance(a, bytes) or (isinstance(a, np.ndarray) and not a.flags["WRITEABLE"]):
+                raise Error(ErrorCode.ConfigError, f"output '{b.name}' must be a writable buffer")
+            p, n = _as_buffer(a)
+            if n != b.size_bytes():
+                raise Error(ErrorCode.ConfigError, f"output '{b.name}' must be {b.size_bytes()} bytes, got {n}")
+            ptrs.append(p)
+        return ptrs
+
     def allocate_outputs(self) -> List[np.ndarray]:
         return [np.zeros(b.size_bytes(), dtype=np.uint8) for b in self._prog.spec().out_buffers]
 
@@ -575,15 +594,7 @@ class Engine:
         if outputs is None:
             rc = N.lib.ecl_engine_run(self._h, in_arr, len(in_ptrs), None, 0)
         else:
-            outs = self._prog.spec().out_buffers
-            if len(outputs) != len(outs):
-                raise Error(ErrorCode.ConfigError, f"expected {len(outs)} output buffers")
-            out_ptrs = []
-            for b, a in zip(outs, outputs):
-                p, n = _as_buffer(a)
-                if n != b.size_bytes():
-                    raise Error(ErrorCode.ConfigError, f"output '{b.name}' must be {b.size_bytes()} bytes")
-                out_ptrs.append(p)
+            out_ptrs = self._check_outputs(outputs)
             rc = N.lib.ecl_engine_run(self._h, in_arr, len(in_ptrs), N.pointer_array(out_ptrs), len(out_ptrs))
         if rc != 0:
             self._fail(rc)
@@ -594,7 +605,7 @@ class Engine:
         """Iterative program: `steps` passes; between passes each (input i,
         output o) pair is exchanged across devices and swapped in place."""
         in_ptrs = self._check_inputs(inputs)
-        out_ptrs = [_as_buffer(a)[0] for a in outputs] if outputs is not None else []
+        out_ptrs = self._check_outputs(outputs) if outputs is not None else []
         si = (ctypes.c_uint32 * max(1, len(swaps)))(*[a for a, _ in swaps])
         so = (ctypes.c_uint32 * max(1, len(swaps)))(*[b for _, b in swaps])
         rc = N.lib.ecl_engine_run_steps(self._h, N.pointer_array(in_ptrs), len(in_ptrs),
@@ -605,10 +616,14 @@ class Engine:
         return self.last_trace() if want_trace else None
 
     def run(self, inputs: Sequence = ()) -> RunResult:
-        """Reference semantics: engine-allocated outputs (engine.hpp:219-256)."""
-        outputs = self.allocate_outputs()
+        """Reference semantics: engine-allocated outputs (engine.hpp:219-256).
+        A virtual-clock engine has no outputs to return (kernels never run on
+        the CPU here): it raises ConfigError and run_virtual() gives the trace."""
         if self._cfg.clock_mode == ClockMode.Virtual:
-            return RunResult(outputs, self.run_virtual(None))
+            raise Error(ErrorCode.ConfigError,
+                        "virtual clock mode produces a trace only: call run_virtual(); outputs need a wall-clock "
+                        "engine on cuda devices")
+        outputs = self.allocate_outputs()
         trace = self.run_into(inputs, outputs)
         return RunResult(outputs, trace)
 
@@ -623,7 +638,7 @@ class Engine:
         return self.last_trace()
 
     def gather(self, outputs: Sequence[np.ndarray]) -> None:
-        ptrs = [_as_buffer(a)[0] for a in outputs]
+        ptrs = self._check_outputs(outputs)
         rc = N.lib.ecl_engine_gather(self._h, N.pointer_array(ptrs), len(ptrs))
         if rc != 0:
             self._fail(rc)
@@ -631,7 +646,7 @@ class Engine:
     def native_run(self, inputs: Sequence = (), outputs: Optional[Sequence[np.ndarray]] = None):
         """One launch over the whole grid: returns (kernel_ms, total_ms)."""
         in_ptrs = self._check_inputs(inputs)
-        out_ptrs = [_as_buffer(a)[0] for a in outputs] if outputs is not None else []
+        out_ptrs = self._check_outputs(outputs) if outputs is not None else []
         k, t = ctypes.c_double(0), ctypes.c_double(0)
         rc = N.lib.ecl_engine_native_run(self._h, N.pointer_array(in_ptrs), len(in_ptrs),
                                          N.pointer_array(out_ptrs) if out_ptrs else None, len(out_ptrs),

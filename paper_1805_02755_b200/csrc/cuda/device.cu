@@ -138,7 +138,11 @@ struct ecl_gpu {
   uint32_t ring_slots = 0, ring_next = 0;
   bool ring_tried = false;
   uint64_t ring_items = 0;
-  uint64_t input_gen = 0;  // see next_input_gen()
+  // Host mirrors of small inputs a launcher passes in its parameters
+  // (ecl::host_mirrored_input: Gaussian's filter); empty for other inputs.
+  std::vector<std::vector<char>> in_host;
+  std::vector<const void*> in_host_ptr;  // LaunchEnv::in_host (nullptr: not mirrored)
+  std::vector<bool> in_host_valid;       // false: the device copy changed on the device (swap_io)
   // Streamed inputs (ecl_gpu_set_streamed_inputs): uploads are enqueued on
   // `h2d` piece by piece, each piece's kernel waiting for the prefix it reads.
   bool streamed = false;
@@ -192,14 +196,6 @@ cudaError_t pinned_free(void* p) {
   const cudaError_t e = cudaHostUnregister(p);
   munmap(p, len);
   return e;
-}
-
-// Process-unique ids of input contents: a kernel that derives per-device
-// state from its inputs (Gaussian's constant-bank filter) redoes it only when
-// the id or the buffer changes.
-uint64_t next_input_gen() {
-  static std::atomic<uint64_t> gen{0};
-  return ++gen;
 }
 
 // cuStreamWaitValue32 through the runtime's driver entry point (no libcuda
@@ -301,7 +297,7 @@ ecl::LaunchEnv env_of(const ecl_gpu* g, int lane) {
   env.ctrl = g->ctrl + lane * kCtrlWordsPerLane;
   env.scratch = g->scratch;
   env.device = g->ordinal;
-  env.input_gen = g->input_gen;
+  env.in_host = g->in_host_ptr.data();
   return env;
 }
 
@@ -317,6 +313,26 @@ int join_lanes(ecl_gpu* g) {
   for (int l = 1; l < g->lanes; ++l) {
     ECL_CK(cudaEventRecord(g->piece[l], g->lane[l]));
     ECL_CK(cudaStreamWaitEvent(g->lane[0], g->piece[l], 0));
+  }
+  return ECL_OK;
+}
+
+// Host mirrors (in_host): refreshed from the caller's bytes on every upload
+// path; a mirror whose device copy changed on the device (swap_io) is read
+// back before the next launch.
+void mirror_write(ecl_gpu* g, size_t i, uint64_t offset, const void* src, uint64_t bytes) {
+  if (i >= g->in_host.size() || g->in_host[i].empty()) return;
+  std::memcpy(g->in_host[i].data() + offset, src, bytes);
+}
+
+int sync_all(ecl_gpu* g);
+
+int ensure_mirrors(ecl_gpu* g) {
+  for (size_t i = 0; i < g->in_host.size(); ++i) {
+    if (g->in_host[i].empty() || g->in_host_valid[i]) continue;
+    if (int rc = sync_all(g)) return rc;
+    ECL_CK(cudaMemcpy(g->in_host[i].data(), g->in[i], g->in_host[i].size(), cudaMemcpyDeviceToHost));
+    g->in_host_valid[i] = true;
   }
   return ECL_OK;
 }
@@ -545,6 +561,14 @@ int ecl_gpu_bind(ecl_gpu* g, const ecl_kernel* k) {
     g->out_bytes = want_out;
   }
   g->spec = &k->spec;
+  g->in_host.assign(g->in.size(), {});
+  g->in_host_ptr.assign(g->in.size(), nullptr);
+  g->in_host_valid.assign(g->in.size(), false);
+  for (uint32_t i = 0; i < g->in.size(); ++i) {
+    if (!ecl::host_mirrored_input(k->spec, i)) continue;
+    g->in_host[i].assign(g->in_bytes[i], 0);
+    g->in_host_ptr[i] = g->in_host[i].data();
+  }
   const uint64_t scratch = ecl::scratch_bytes(k->spec);
   if (scratch > g->scratch_cap) {
     if (g->scratch) cudaFree(g->scratch);
@@ -582,7 +606,7 @@ int ecl_gpu_swap_io(ecl_gpu* g, uint32_t i, uint32_t o) {
   if (int rc = set_device(g)) return rc;
   if (int rc = sync_all(g)) return rc;
   std::swap(g->in[i], g->out[o]);
-  g->input_gen = next_input_gen();
+  if (i < g->in_host_valid.size()) g->in_host_valid[i] = false;  // produced on the device
   return ECL_OK;
 }
 
@@ -606,14 +630,16 @@ int ecl_gpu_upload_inputs(ecl_gpu* g, const void* const* host_inputs) {
     for (size_t i = 0; i < g->in.size(); ++i) {
       if (!host_inputs || !host_inputs[i]) continue;
       g->pending_in[i] = static_cast<const char*>(host_inputs[i]);
-      g->input_gen = next_input_gen();
+      mirror_write(g, i, 0, host_inputs[i], g->in_bytes[i]);
+      if (i < g->in_host_valid.size()) g->in_host_valid[i] = true;
     }
     return ECL_OK;
   }
   for (size_t i = 0; i < g->in.size(); ++i) {
     if (!host_inputs || !host_inputs[i]) continue;
     ECL_CK(cudaMemcpyAsync(g->in[i], host_inputs[i], g->in_bytes[i], cudaMemcpyHostToDevice, g->lane[0]));
-    g->input_gen = next_input_gen();
+    mirror_write(g, i, 0, host_inputs[i], g->in_bytes[i]);
+    if (i < g->in_host_valid.size()) g->in_host_valid[i] = true;
   }
   return fan_out_lane0(g);
 }
@@ -637,7 +663,11 @@ int ecl_replicate_inputs(ecl_gpu* const* gpus, uint32_t n, uint32_t root) {
       for (size_t b = 0; b < dst->in.size(); ++b)
         ECL_CK(cudaMemcpyPeerAsync(dst->in[b], dst->ordinal, src->in[b], src->ordinal, dst->in_bytes[b],
                                    dst->lane[0]));
-      dst->input_gen = next_input_gen();
+      if (int rc = ensure_mirrors(src)) return rc;
+      dst->in_host = src->in_host;
+      dst->in_host_valid = src->in_host_valid;
+      for (size_t b = 0; b < dst->in_host.size(); ++b)
+        dst->in_host_ptr[b] = dst->in_host[b].empty() ? nullptr : dst->in_host[b].data();
       if (int rc = fan_out_lane0(dst)) return rc;
     }
   }
@@ -733,6 +763,14 @@ int ecl_gpu_upload(ecl_gpu* g, void* dst, const void* src, size_t bytes) {
   if (int rc = set_device(g)) return rc;
   if (int rc = join_lanes(g)) return rc;
   ECL_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g->lane[0]));
+  // A raw upload into a mirrored input keeps the mirror in step.
+  for (size_t i = 0; i < g->in_host.size(); ++i) {
+    if (g->in_host[i].empty()) continue;
+    const uintptr_t b0 = reinterpret_cast<uintptr_t>(g->in[i]), b1 = b0 + g->in_bytes[i];
+    const uintptr_t d0 = reinterpret_cast<uintptr_t>(dst), d1 = d0 + bytes;
+    const uintptr_t lo = std::max(b0, d0), hi = std::min(b1, d1);
+    if (lo < hi) mirror_write(g, i, lo - b0, static_cast<const char*>(src) + (lo - d0), hi - lo);
+  }
   return fan_out_lane0(g);
 }
 
@@ -827,6 +865,7 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
   uint64_t o_off = 0, o_cnt = 0;
   if (int rc = out_range(s, offset_wg, size_wg, &o_off, &o_cnt)) return rc;
   if (int rc = set_device(g)) return rc;
+  if (int rc = ensure_mirrors(g)) return rc;
   if (find_slot(g, seq)) return fail(ECL_SCHEDULER_ERROR, "package seq submitted twice");
   Slot& slot = g->slots[g->next_slot];
   g->next_slot = (g->next_slot + 1) % (kSlots - 1);  // the last slot is reserved for native_run
@@ -1045,6 +1084,7 @@ int ecl_gpu_download_tally(ecl_gpu* g, uint32_t* host) {
 int ecl_gpu_native_run(ecl_gpu* g, float* kernel_ms) {
   if (!g->spec) return fail(ECL_CONFIG_ERROR, "native run before bind");
   if (int rc = set_device(g)) return rc;
+  if (int rc = ensure_mirrors(g)) return rc;
   if (int rc = join_lanes(g)) return rc;
   // Inputs whole before the one launch (streamed uploads finish first; the
   // kernel timing below starts after them).

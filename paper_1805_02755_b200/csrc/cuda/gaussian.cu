@@ -13,10 +13,13 @@
 //  * thread (tx, ty) owns outputs (ty, 8tx..8tx+7); lanes are laid out so
 //    the 8 lanes of an LDS.128 phase read 8 different rows -> the 100-float
 //    pitch spreads them over all 32 banks (conflict-free);
-//  * the filter lives in __constant__ memory (copied from the device input
-//    on the launch stream), so every FFMA takes its weight from a uniform
-//    register: per filter row i a thread loads 10 float4 of the input row
-//    and issues 8*F FFMAs (i outer, j inner, the oracle's order);
+//  * the filter travels as a __grid_constant__ kernel parameter (constant
+//    bank 0), packed on the host from the device layer's host mirror of the
+//    filter input, so every FFMA takes its weight from a uniform register
+//    (LDCU) and each launch carries its own filter: no per-device constant
+//    state, nothing shared between lanes or between engines on one GPU.
+//    Per filter row i a thread loads 10 float4 of the input row and issues
+//    8*F FFMAs (i outer, j inner, the oracle's order);
 //  * results leave as two float4 stores per thread.
 // Packages are arbitrary work-item ranges: tiles cover the rows the range
 // touches and only pixels inside [first, first+count) are written.
@@ -29,20 +32,20 @@ namespace {
 
 constexpr int kTileW = 64, kTileH = 32, kThreads = 256, kPitch = 100;
 constexpr int kMaxF = 31;
-__constant__ float c_filter[63 * 63];
-// Tiled path: the filter twice with an even row pitch F+1, so tap pairs are
-// 8-byte aligned: c_fa[i*(F+1) + j] = w[i][j], c_fb[i*(F+1) + j] = w[i][j+1].
-__constant__ __align__(16) float c_fa[kMaxF * (kMaxF + 1)], c_fb[kMaxF * (kMaxF + 1)];
-__device__ __align__(16) float g_fpack[2 * kMaxF * (kMaxF + 1)];
 
-__global__ void pack_filter(const float* __restrict__ filt, int F) {
-  const int P = F + 1;
-  for (int k = threadIdx.x; k < F * P; k += blockDim.x) {
-    const int i = k / P, j = k - i * P;
-    g_fpack[k] = j < F ? filt[i * F + j] : 0.0f;
-    g_fpack[F * P + k] = j + 1 < F ? filt[i * F + j + 1] : 0.0f;
-  }
-}
+// Tiled path: the filter twice with an even row pitch F+1, so tap pairs are
+// 8-byte aligned: a[i*(F+1) + j] = w[i][j], b[i*(F+1) + j] = w[i][j+1]
+// (zero past the row).  7.9 KB at F = 31, inside the 32 KB parameter limit.
+template <int F>
+struct TapPairs {
+  __align__(16) float a[F * (F + 1)];
+  __align__(16) float b[F * (F + 1)];
+};
+
+// Generic path: the F x F filter as given (F <= 63: 15.9 KB).
+struct FilterParam {
+  float w[63 * 63];
+};
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
@@ -83,7 +86,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 template <int F>
 __global__ void __launch_bounds__(kThreads)
     gaussian_tiled(const float* __restrict__ img, float* __restrict__ out, int W, int H, uint64_t first, uint64_t count,
-                   int row0) {
+                   int row0, const __grid_constant__ TapPairs<F> taps) {
   constexpr int R = F / 2;
   constexpr int TH = kTileH + F - 1;  // staged rows
   constexpr int NV = 8 + F - 1;       // input values per thread row
@@ -128,8 +131,8 @@ __global__ void __launch_bounds__(kThreads)
   // (j, j+1) of a row into (acc[b].x, acc[b].y) from the input pair
   // (v[a], v[a+1]), a = SHIFT + b + j, which is a register pair of the float4
   // loads when a is even — so outputs with even SHIFT + b pair taps from
-  // j = 0 (weights c_fa, leftover tap F-1) and the others from j = 1
-  // (weights c_fb, leftover tap 0).  Half the FP32 issue slots of scalar
+  // j = 0 (weights taps.a, leftover tap F-1) and the others from j = 1
+  // (weights taps.b, leftover tap 0).  Half the FP32 issue slots of scalar
   // FFMAs (the kernel was issue-bound); the two partial sums per output
   // change the accumulation order only (≤ 3.2e-6 relative vs the oracle's
   // sequential order on this filter, budget 1e-5).
@@ -150,8 +153,8 @@ __global__ void __launch_bounds__(kThreads)
       ev[2 * m] = make_float2(q.x, q.y);
       ev[2 * m + 1] = make_float2(q.z, q.w);
     }
-    const float2* wa = reinterpret_cast<const float2*>(c_fa + i * P);  // (w[2m], w[2m+1])
-    const float2* wb = reinterpret_cast<const float2*>(c_fb + i * P);  // (w[2m+1], w[2m+2])
+    const float2* wa = reinterpret_cast<const float2*>(taps.a + i * P);  // (w[2m], w[2m+1])
+    const float2* wb = reinterpret_cast<const float2*>(taps.b + i * P);  // (w[2m+1], w[2m+2])
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
       const int a0 = SHIFT + b;
@@ -159,9 +162,9 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int m = 0; m < NP; ++m) acc[b] = __ffma2_rn(wa[m], ev[a0 / 2 + m], acc[b]);
         const int a = a0 + F - 1;  // leftover tap F-1
-        acc[b].x = fmaf(c_fa[i * P + F - 1], (a & 1) ? ev[a >> 1].y : ev[a >> 1].x, acc[b].x);
+        acc[b].x = fmaf(taps.a[i * P + F - 1], (a & 1) ? ev[a >> 1].y : ev[a >> 1].x, acc[b].x);
       } else {
-        acc[b].x = fmaf(c_fa[i * P], ev[a0 >> 1].y, acc[b].x);  // leftover tap 0 (a0 odd)
+        acc[b].x = fmaf(taps.a[i * P], ev[a0 >> 1].y, acc[b].x);  // leftover tap 0 (a0 odd)
 #pragma unroll
         for (int m = 0; m < NP; ++m) acc[b] = __ffma2_rn(wb[m], ev[(a0 + 1) / 2 + m], acc[b]);
       }
@@ -186,10 +189,10 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// Any odd F up to 63: one thread per output, filter from constant memory.
+// Any odd F up to 63: one thread per output, filter from the parameter bank.
 __global__ void __launch_bounds__(kThreads)
     gaussian_generic(const float* __restrict__ img, float* __restrict__ out, int W, int H, int F, uint64_t first,
-                     uint64_t count) {
+                     uint64_t count, const __grid_constant__ FilterParam filt) {
   const int R = F / 2;
   for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < count;
        k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -198,76 +201,57 @@ __global__ void __launch_bounds__(kThreads)
     float acc = 0.0f;
     for (int i = 0; i < F; ++i) {
       const float* src = img + static_cast<int64_t>(clampi(y + i - R, 0, H - 1)) * W;
-      for (int j = 0; j < F; ++j) acc = fmaf(c_filter[i * F + j], src[clampi(x + j - R, 0, W - 1)], acc);
+      for (int j = 0; j < F; ++j) acc = fmaf(filt.w[i * F + j], src[clampi(x + j - R, 0, W - 1)], acc);
     }
     out[idx] = acc;
   }
 }
 
 template <int F>
-cudaError_t launch_tiled(const GaussianParams& g, const LaunchEnv& env, uint64_t first, uint64_t count) {
+cudaError_t launch_tiled(const GaussianParams& g, const LaunchEnv& env, const float* w, uint64_t first,
+                         uint64_t count) {
+  constexpr int P = F + 1;
+  TapPairs<F> taps;
+  for (int i = 0; i < F; ++i)
+    for (int j = 0; j < P; ++j) {
+      taps.a[i * P + j] = j < F ? w[i * F + j] : 0.0f;
+      taps.b[i * P + j] = j + 1 < F ? w[i * F + j + 1] : 0.0f;
+    }
   const int row0 = static_cast<int>(first / g.width);
   const int row1 = static_cast<int>((first + count - 1) / g.width);
   const dim3 grid((g.width + kTileW - 1) / kTileW, (row1 - row0 + kTileH) / kTileH);
   gaussian_tiled<F><<<grid, kThreads, 0, env.stream>>>(static_cast<const float*>(env.in[0]),
                                                        static_cast<float*>(env.out[0]), static_cast<int>(g.width),
-                                                       static_cast<int>(g.height), first, count, row0);
+                                                       static_cast<int>(g.height), first, count, row0, taps);
   return cudaGetLastError();
 }
 
 }  // namespace
 
+// The filter (input 1) is host-mirrored by the device layer
+// (host_mirrored_input): each launch packs it into its own parameters.
+bool gaussian_mirrors_input(uint32_t input) { return input == 1; }
+
 cudaError_t launch_gaussian(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
   if (count == 0) return cudaSuccess;
   const GaussianParams& g = spec.gauss;
-  // The filter (input 1) goes to constant memory on the launch stream, so the
-  // kernels that follow on this stream see this program's filter.
-  const bool tiled = g.filter == 3 || g.filter == 5 || g.filter == 7 || g.filter == 9 || g.filter == 15 ||
-                     g.filter == 31;
-  cudaError_t e;
-  // The two padded tap-pair layouts live in this device's constant bank; they
-  // are rebuilt only when the filter buffer or its contents changed (input
-  // generation), not per launch.  Launches on one device are enqueued by one
-  // host thread, and uploads join both lanes first, so no kernel reads the
-  // bank while it is rewritten with different values.
-  static const void* packed_src[64] = {};
-  static uint64_t packed_gen[64] = {};
-  static int packed_f[64] = {};
-  const int dev = env.device & 63;
-  const bool stale = packed_src[dev] != env.in[1] || packed_gen[dev] != env.input_gen ||
-                     packed_f[dev] != static_cast<int>(g.filter) || env.input_gen == 0;
-  if (tiled && stale) {
-    packed_src[dev] = env.in[1];
-    packed_gen[dev] = env.input_gen;
-    packed_f[dev] = static_cast<int>(g.filter);
-    const int F = static_cast<int>(g.filter);
-    pack_filter<<<1, 256, 0, env.stream>>>(static_cast<const float*>(env.in[1]), F);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    void* packed = nullptr;
-    if ((e = cudaGetSymbolAddress(&packed, g_fpack)) != cudaSuccess) return e;
-    const size_t bytes = sizeof(float) * F * (F + 1);
-    if ((e = cudaMemcpyToSymbolAsync(c_fa, packed, bytes, 0, cudaMemcpyDeviceToDevice, env.stream)) != cudaSuccess)
-      return e;
-    if ((e = cudaMemcpyToSymbolAsync(c_fb, static_cast<char*>(packed) + bytes, bytes, 0, cudaMemcpyDeviceToDevice,
-                                     env.stream)) != cudaSuccess)
-      return e;
-  } else if (!tiled && (e = cudaMemcpyToSymbolAsync(c_filter, env.in[1], sizeof(float) * g.filter * g.filter, 0,
-                                                     cudaMemcpyDeviceToDevice, env.stream)) != cudaSuccess) {
-    return e;
-  }
+  const float* w = env.in_host ? static_cast<const float*>(env.in_host[1]) : nullptr;
+  if (!w) return cudaErrorInvalidValue;  // the device layer keeps the filter mirrored (host_mirrored_input)
   switch (g.filter) {
-    case 3: return launch_tiled<3>(g, env, first, count);
-    case 5: return launch_tiled<5>(g, env, first, count);
-    case 7: return launch_tiled<7>(g, env, first, count);
-    case 9: return launch_tiled<9>(g, env, first, count);
-    case 15: return launch_tiled<15>(g, env, first, count);
-    case 31: return launch_tiled<31>(g, env, first, count);
+    case 3: return launch_tiled<3>(g, env, w, first, count);
+    case 5: return launch_tiled<5>(g, env, w, first, count);
+    case 7: return launch_tiled<7>(g, env, w, first, count);
+    case 9: return launch_tiled<9>(g, env, w, first, count);
+    case 15: return launch_tiled<15>(g, env, w, first, count);
+    case 31: return launch_tiled<31>(g, env, w, first, count);
     default: break;
   }
+  FilterParam filt;
+  std::copy(w, w + g.filter * g.filter, filt.w);
   const uint64_t blocks = std::min<uint64_t>((count + kThreads - 1) / kThreads, static_cast<uint64_t>(env.sms) * 16);
   gaussian_generic<<<static_cast<unsigned>(blocks), kThreads, 0, env.stream>>>(
       static_cast<const float*>(env.in[0]), static_cast<float*>(env.out[0]), static_cast<int>(g.width),
-      static_cast<int>(g.height), static_cast<int>(g.filter), first, count);
+      static_cast<int>(g.height), static_cast<int>(g.filter), first, count, filt);
   return cudaGetLastError();
 }
 

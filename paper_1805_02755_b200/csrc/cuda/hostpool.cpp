@@ -125,9 +125,12 @@ class Pool {
         widen(j.src, j.dst, j.count, j.rep);
       }
       if (j.release) __atomic_store_n(j.release, j.release_value, __ATOMIC_RELEASE);
-      if (j.ticket->pending.fetch_sub(1) == 1) {
+      {
+        // Decrement under the ticket's lock: widen_wait returns only after
+        // taking the same lock, so the ticket (owned by a device slot that
+        // ecl_gpu_close frees) outlives this worker's last touch of it.
         std::lock_guard lock(j.ticket->m);
-        j.ticket->cv.notify_all();
+        if (j.ticket->pending.fetch_sub(1) == 1) j.ticket->cv.notify_all();
       }
     }
   }
@@ -154,8 +157,7 @@ void widen_async(int device, cudaEvent_t ready, const uint32_t* src, uint32_t* d
 unsigned widen_workers() { return pool().size(); }
 
 bool widen_wait(WidenTicket* ticket) {
-  if (ticket->pending.load() == 0) return !ticket->failed.load();  // idle ticket: no lock
-  std::unique_lock lock(ticket->m);
+  std::unique_lock lock(ticket->m);  // always: see the worker's decrement
   ticket->cv.wait(lock, [&] { return ticket->pending.load() == 0; });
   return !ticket->failed.load();
 }

@@ -80,7 +80,9 @@ struct LaunchEnv {
   void* scratch = nullptr;     // per-device, per-binding kernel scratch (scratch_bytes())
   uint32_t* compact = nullptr;  // replicate > 1 and host copies pending: one value per item
   int device = 0;               // CUDA ordinal
-  uint64_t input_gen = 0;       // process-unique id of the current input contents (changes on upload)
+  // Host mirrors of the inputs host_mirrored_input() names (nullptr for the
+  // others): small inputs a launcher passes by value in its parameters.
+  const void* const* in_host = nullptr;
 };
 
 // Device scratch a kernel needs per binding (e.g. Mandelbrot coordinate tables),
@@ -95,6 +97,13 @@ cudaError_t prepare_mandelbrot(const KernelSpec& spec, const LaunchEnv& env);
 // (Gaussian rows + halo, Binomial options, vecscale elements); other
 // kernels read whole buffers.
 uint64_t input_bytes_needed(const KernelSpec& spec, uint32_t input, uint64_t first, uint64_t count);
+
+// Inputs the device layer keeps a host copy of (LaunchEnv::in_host), kept in
+// step with every way the device copy changes (upload, replication, raw
+// upload, swap): Gaussian's filter, which each launch carries in its
+// parameters instead of a per-device constant bank.
+bool host_mirrored_input(const KernelSpec& spec, uint32_t input);
+bool gaussian_mirrors_input(uint32_t input);
 
 // Parses and validates (kernel_for + check_buffer_shapes semantics).
 // Returns ECL_OK or a negative status with *err filled.

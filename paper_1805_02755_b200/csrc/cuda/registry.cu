@@ -260,6 +260,10 @@ uint64_t input_bytes_needed(const KernelSpec& spec, uint32_t input, uint64_t fir
   }
 }
 
+bool host_mirrored_input(const KernelSpec& spec, uint32_t input) {
+  return spec.kind == KernelKind::Gaussian && gaussian_mirrors_input(input);
+}
+
 cudaError_t launch_kernel(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
   switch (spec.kind) {
     case KernelKind::VecScale: return launch_vecscale(spec, env, first, count);

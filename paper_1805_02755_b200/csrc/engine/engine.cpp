@@ -8,8 +8,9 @@
 // to queue_depth packages in flight on its GPU: package k+1 is submitted
 // before package k ends, so the per-package dispatch (scheduler call +
 // kernel launch + event records) hides under the running kernel.
-// Completion is event driven: the device layer's host callback marks the
-// package done and wakes the owning thread.
+// Completion: the owning device thread blocks on the package's kernel-end
+// events (ecl_gpu_wait_compute -> cudaEventSynchronize); the engine passes no
+// host callback, and the package's D2H copies keep draining behind it.
 //
 // Virtual mode.  The discrete-event replay of drive_virtual
 // (engine.hpp:306-338) with the same cost model (simulate_package_ms,
@@ -755,12 +756,16 @@ RunResult Engine::run(std::span<const std::vector<std::byte>> inputs) {
       throw Error(ErrorCode::InputSizeMismatch, "input '" + s.in_buffers[i].name + "' is " +
                                                     std::to_string(inputs[i].size()) + " bytes, descriptor says " +
                                                     std::to_string(s.in_buffers[i].size_bytes()));
+  // The reference's drive_virtual executes every package inline on the host
+  // (engine.hpp:306-338); this engine never evaluates a kernel on the CPU, so
+  // a virtual engine yields the trace alone and run() refuses rather than
+  // return outputs that were never computed.
+  if (!impl_->wall())
+    throw Error(ErrorCode::ConfigError,
+                "virtual clock mode produces a trace only: call run_virtual(); outputs need a wall-clock engine on "
+                "cuda devices");
   RunResult r;
   for (const BufferDesc& b : s.out_buffers) r.outputs.emplace_back(b.size_bytes());
-  if (!impl_->wall()) {
-    r.trace = run_virtual({});
-    return r;
-  }
   std::vector<const void*> in;
   for (const auto& v : inputs) in.push_back(v.data());
   std::vector<void*> out;

@@ -187,14 +187,6 @@ def test_indivisible_package_fails_mid_run(gpu_available):
     assert ei.value.code == P.ErrorCode.BadKernelArgs
 
 
-def test_indivisible_package_engine_failure(gpu_available):
-    # a legal 4:1 mandelbrot program cannot produce indivisible packages, so
-    # check the device-layer guard through binomial's 1:lws pattern instead
-    spec = W.binomial_spec(4 * 64, steps=254)
-    prog = P.validate_program(spec)
-    assert prog.total_work_groups() == 64
-
-
 def test_engine_rejects_bad_configs(gpu_available):
     prog = P.validate_program(W.synthetic_spec(100, 10))
     with pytest.raises(P.Error):
