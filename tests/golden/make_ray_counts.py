@@ -1,9 +1,11 @@
 #!/usr/bin/env python3
-"""Algorithmic operation counts of the Ray config (8192^2, 64 spheres,
-depth 4, seed 42) from the CPU oracle (oracle.c:orc_ray instruments sphere
-tests, plane tests and shading evaluations).  bench.py reads the committed
-numbers as the Ray roofline's algorithmic work ("instrumented
-flop count from the CPU oracle"); the GPU never runs the oracle.
+"""Algorithmic operation counts and image checksums of the Ray config
+(8192^2, 64 spheres, depth 4, seed 42) from the CPU oracle (oracle.c:orc_ray
+instruments sphere tests, plane tests and shading evaluations).  bench.py
+reads the committed numbers as the Ray roofline's algorithmic work (SURVEY
+§8d: "instrumented flop count from the CPU oracle"); the config-size parity
+test (tests/test_config_parity_gpu.py) compares the device image's FNV-1a
+with `fnv1a64` bit for bit.  The GPU never runs the oracle.
 
 Usage: python tests/golden/make_ray_counts.py
 """
@@ -28,7 +30,8 @@ def main():
                            "flops": W.ray_flops(st, pt, sh),
                            "bounce_histogram": [int(x) for x in
                                                 __import__("numpy").bincount(img[:, 3].astype(int), minlength=5)],
-                           "rgb_sum": [float(x) for x in img[:, :3].astype("float64").sum(axis=0)]}
+                           "rgb_sum": [float(x) for x in img[:, :3].astype("float64").sum(axis=0)],
+                           "fnv1a64": hex(o.fnv1a64(img))}
     with open(os.path.join(HERE, "ray_counts.json"), "w") as f:
         json.dump(out, f, indent=1)
     print(json.dumps(out, indent=1))

@@ -1,0 +1,282 @@
+"""Parity at the BASELINE.json configs for the four kernels the reference
+does not implement, the analogue of the
+reference's full-output acceptance check (acceptance.cpp:112-168).  Mandelbrot
+at 16384^2 x 2048 is pinned in test_engine_gpu.py.
+
+* Ray 8192^2: bit-exact — FNV-1a of the whole 1 GiB image against the oracle's
+  (tests/golden/ray_counts.json, made by tests/golden/make_ray_counts.py).
+* Binomial 8M x 254: every 16th option plus every option within 256 of each
+  package boundary of the run, 1e-5 relative.
+* NBody 1M: one step, 8192 targets in 32 windows spread over the range and
+  on package boundaries, positions (as displacements) and velocities 1e-4;
+  10 steps at 32K bodies through the per-step exchange.
+* Gaussian 4096^2 x 31^2: the full image, 1e-5 relative.
+
+The oracle (oracle/oracle.c) is this repo's restatement and parity for these
+kernels is unpinned by the reference (SPEC.md:323 removed them), so each has
+an independent cross-check as well: Binomial against the Black-Scholes limit
+of the CRR lattice, NBody against momentum conservation, Gaussian against an
+f64 separable convolution computed here with numpy.
+"""
+import numpy as np
+import pytest
+
+import paper_1805_02755_b200 as P
+from paper_1805_02755_b200 import workloads as W
+from tests._oracle import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def devices(n, depth=2):
+    ng = P.gpu_count()
+    return [P.cuda_device(f"gpu{i}", ordinal=i % ng, queue_depth=depth) for i in range(n)]
+
+
+def rel_err(got, exp):
+    got = np.asarray(got, np.float64)
+    exp = np.asarray(exp, np.float64)
+    return np.abs(got - exp) / np.maximum(np.abs(exp), 1e-30)
+
+
+def golden_ray():
+    import json
+    import os
+    with open(os.path.join(ROOT, "tests", "golden", "ray_counts.json")) as f:
+        return json.load(f)
+
+
+# ---- Ray 8192^2 ----------------------------------------------------------------
+
+def test_ray_config_bit_exact(gpu_available, oracle):
+    w = h = 8192
+    g = golden_ray()["8192x8192"]
+    scene = W.ray_scene(64, seed=42)
+    prog = P.validate_program(W.ray_spec(w, h, 64, 4))
+    out = np.empty((w * h, 4), np.float32)
+    with P.Engine(P.EngineConfig(devices(2), P.HGuidedConfig()), prog) as e:
+        t = e.run_into([scene], [out])
+    assert P.tiles_exactly(t.packages, prog.total_work_groups())
+    assert hex(oracle.fnv1a64(out)) == g["fnv1a64"]
+    hist = np.bincount(out[:, 3].astype(int), minlength=len(g["bounce_histogram"]))
+    assert hist.tolist() == g["bounce_histogram"]
+    assert out[:, :3].astype(np.float64).sum(axis=0).tolist() == g["rgb_sum"]
+
+
+# ---- Binomial 8M x 254 ---------------------------------------------------------
+
+def black_scholes_call(rand):
+    """Closed-form European call for the option parameters Binomial derives
+    from `rand` (oracle.c:orc_binomial)."""
+    from scipy.special import ndtr
+    r = np.asarray(rand, np.float64)
+    S = 5 * (1 - r) + 30 * r
+    K = 1 * (1 - r) + 100 * r
+    T = 0.25 * (1 - r) + 10 * r
+    R, V = 0.02, 0.30
+    d1 = (np.log(S / K) + (R + 0.5 * V * V) * T) / (V * np.sqrt(T))
+    d2 = d1 - V * np.sqrt(T)
+    return S * ndtr(d1) - K * np.exp(-R * T) * ndtr(d2), S * V * np.sqrt(T)
+
+
+def test_binomial_config(gpu_available, oracle):
+    options, steps = 8 * 1024 * 1024, 254
+    rand = W.binomial_inputs(options, seed=42)[0]
+    prog = P.validate_program(W.binomial_spec(options, steps))
+    out = np.empty(options, np.float32)
+    with P.Engine(P.EngineConfig(devices(2), P.HGuidedConfig()), prog) as e:
+        t = e.run_into([rand], [out])
+    assert P.tiles_exactly(t.packages, prog.total_work_groups())
+    assert np.isfinite(out).all()
+
+    # every 16th option: options are independent, so the oracle prices the
+    # strided sample directly
+    idx = np.arange(0, options, 16)
+    # plus every option within 256 of each package boundary (4 options per work-group)
+    for p in t.packages:
+        for b in (4 * p.offset_wg, 4 * p.end_wg()):
+            idx = np.concatenate([idx, np.arange(max(0, b - 256), min(options, b + 256))])
+    idx = np.unique(idx)
+    exp = oracle.binomial(np.ascontiguousarray(rand[idx]), steps)
+    err = np.abs(out[idx].astype(np.float64) - exp) - (1e-5 * np.abs(exp) + 1e-6)
+    assert err.max() <= 0.0, f"{int((err > 0).sum())} options beyond 1e-5 (worst option {idx[err.argmax()]})"
+
+    # Independent of the oracle: the CRR lattice converges to Black-Scholes
+    # with an O(1/steps) error; over this option range the f64 lattice stays
+    # within 0.141 * S*sigma*sqrt(T)/steps (measured on 200k options), so the
+    # device prices must lie within 0.25 * S*sigma*sqrt(T)/steps of it.
+    bs, scale = black_scholes_call(rand[idx])
+    gap = np.abs(out[idx].astype(np.float64) - bs) / (scale / steps)
+    assert gap.max() <= 0.25, f"max |price - BS| = {gap.max():.3f} x S*sigma*sqrt(T)/steps"
+
+
+@pytest.mark.parametrize("steps", [31, 100, 254])
+def test_binomial_converges_to_black_scholes(gpu_available, steps):
+    options = 4 * 4096
+    rand = W.binomial_inputs(options, seed=5)[0]
+    prog = P.validate_program(W.binomial_spec(options, steps))
+    with P.Engine(P.EngineConfig(devices(1), P.DynamicConfig(9)), prog) as e:
+        got = e.run([rand]).outputs[0].view(np.float32).astype(np.float64)
+    bs, scale = black_scholes_call(rand)
+    assert (np.abs(got - bs) / (scale / steps)).max() <= 0.25
+
+
+# ---- NBody 1M ------------------------------------------------------------------
+
+def nbody_windows(n, packages, per=256, spread=32):
+    """Contiguous target windows: `spread` evenly over the range plus one on
+    each side of package boundaries, `per` bodies each."""
+    starts = {int(k * (n - per) / max(1, spread - 1)) for k in range(spread)}
+    for p in packages[: 2 * 8]:
+        b = p.offset_wg * 64
+        starts.add(min(max(0, b - per // 2), n - per))
+    return sorted(starts)
+
+
+def test_nbody_config_one_step(gpu_available, oracle):
+    n, dt, eps2 = 1 << 20, 0.005, 500.0
+    pos, vel = W.nbody_inputs(n, seed=42)
+    prog = P.validate_program(W.nbody_spec(n, dt, eps2))
+    npos = np.empty((n, 4), np.float32)
+    nvel = np.empty((n, 4), np.float32)
+    with P.Engine(P.EngineConfig(devices(2), P.DynamicConfig(8)), prog) as e:
+        t = e.run_into([pos, vel], [npos, nvel])
+    assert P.tiles_exactly(t.packages, prog.total_work_groups())
+    assert np.isfinite(npos).all() and np.isfinite(nvel).all()
+    assert np.array_equal(npos[:, 3], pos[:, 3]) and np.array_equal(nvel[:, 3], vel[:, 3])
+
+    checked = 0
+    for s in nbody_windows(n, t.packages):
+        ep, ev = oracle.nbody_step(pos, vel, dt, eps2, first=s, count=256)
+        sl = slice(s, s + 256)
+        # velocities start at 0: nvel = a*dt; per body, the error of the
+        # acceleration vector relative to its own magnitude
+        a_exp = ev[sl, :3].astype(np.float64)
+        a_got = nvel[sl, :3].astype(np.float64)
+        mag = np.linalg.norm(a_exp, axis=1)
+        verr = np.linalg.norm(a_got - a_exp, axis=1) / mag
+        assert verr.max() <= 1e-4, (s, float(verr.max()))
+        # positions through the displacement (p' - p = a dt^2/2), which is
+        # what the step computes; the f32 store of p' adds at most one ulp
+        d_exp = ep[sl, :3].astype(np.float64) - pos[sl, :3]
+        d_got = npos[sl, :3].astype(np.float64) - pos[sl, :3]
+        ulp = np.spacing(np.abs(ep[sl, :3])).astype(np.float64)
+        bound = 1e-4 * np.linalg.norm(d_exp, axis=1)[:, None] + 2 * ulp
+        assert (np.abs(d_got - d_exp) <= bound).all(), s
+        checked += 256
+    assert checked >= 8192
+
+    # Independent of the oracle: pairwise forces cancel, so the total momentum
+    # after a step from rest stays ~0 against the sum of |m v|
+    m = pos[:, 3].astype(np.float64)[:, None]
+    p_tot = np.linalg.norm((m * nvel[:, :3].astype(np.float64)).sum(axis=0))
+    p_abs = (m[:, 0] * np.linalg.norm(nvel[:, :3].astype(np.float64), axis=1)).sum()
+    assert p_tot <= 1e-4 * p_abs, p_tot / p_abs
+
+
+def test_nbody_ten_steps_with_exchange(gpu_available, oracle):
+    n, steps = 32768, 10
+    pos, vel = W.nbody_inputs(n, seed=7)
+    prog = P.validate_program(W.nbody_spec(n))
+    out = [np.zeros((n, 4), np.float32), np.zeros((n, 4), np.float32)]
+    with P.Engine(P.EngineConfig(devices(3), P.DynamicConfig(12)), prog) as e:
+        t = e.run_steps([pos, vel], out, steps, [(0, 0), (1, 1)])
+    assert len(t.packages) == 12 * steps
+    ep, ev = pos, vel
+    for _ in range(steps):
+        ep, ev = oracle.nbody_step(ep, ev, 0.005, 500.0)
+    # after 10 steps positions have moved far from the start: compare them
+    # relative to the distance travelled, velocities per body
+    travel = np.linalg.norm(ep[:, :3].astype(np.float64) - pos[:, :3], axis=1)
+    perr = np.linalg.norm(out[0][:, :3].astype(np.float64) - ep[:, :3], axis=1)
+    assert (perr <= 2e-4 * travel + 4 * np.spacing(np.float32(64.0))).all(), float((perr / travel).max())
+    vmag = np.linalg.norm(ev[:, :3].astype(np.float64), axis=1)
+    verr = np.linalg.norm(out[1][:, :3].astype(np.float64) - ev[:, :3], axis=1)
+    assert (verr <= 2e-4 * vmag).all(), float((verr / vmag).max())
+    m = pos[:, 3].astype(np.float64)[:, None]
+    p_tot = np.linalg.norm((m * out[1][:, :3].astype(np.float64)).sum(axis=0))
+    assert p_tot <= 1e-4 * (m[:, 0] * vmag).sum()
+
+
+# ---- Gaussian 4096^2 -----------------------------------------------------------
+
+def separable_f64(img, w, h, f, sigma):
+    """f64 blur with the 1-D factors of the (separable) Gaussian filter,
+    clamp-to-edge: an independent restatement of the 2-D definition."""
+    r = f // 2
+    d = np.arange(f) - r
+    g = np.exp(-(d * d) / (2.0 * sigma * sigma))
+    g /= g.sum()
+    x = img.reshape(h, w).astype(np.float64)
+    xp = np.pad(x, ((0, 0), (r, r)), mode="edge")
+    rows = sum(g[j] * xp[:, j:j + w] for j in range(f))
+    rp = np.pad(rows, ((r, r), (0, 0)), mode="edge")
+    return sum(g[i] * rp[i:i + h, :] for i in range(f)).ravel()
+
+
+def test_gaussian_config_full_image(gpu_available, oracle):
+    w = h = 4096
+    f = 31
+    img, filt = W.gaussian_inputs(w, h, f, seed=42)
+    prog = P.validate_program(W.gaussian_spec(w, h, f))
+    out = np.empty(w * h, np.float32)
+    with P.Engine(P.EngineConfig(devices(1), P.StaticConfig()), prog) as e:
+        e.run_into([img, filt], [out])
+    exp = oracle.gaussian(img, filt, w, h, f)
+    err = rel_err(out, exp)
+    assert err.max() <= 1e-5, f"max rel err {err.max():.2e} at pixel {err.argmax()}"
+    ind = rel_err(out, separable_f64(img, w, h, f, 5.0))
+    assert ind.max() <= 1e-5, f"vs f64 separable: {ind.max():.2e}"
+
+
+def test_gaussian_config_co_executed(gpu_available, oracle):
+    """The same image split by HGuided over 3 devices: bands start mid-row and
+    every seam reads its neighbours' halo rows from the device's replica."""
+    w = h = 4096
+    f = 31
+    img, filt = W.gaussian_inputs(w, h, f, seed=3)
+    prog = P.validate_program(W.gaussian_spec(w, h, f))
+    out = np.empty(w * h, np.float32)
+    with P.Engine(P.EngineConfig(devices(3), P.HGuidedConfig()), prog) as e:
+        t = e.run_into([img, filt], [out])
+    assert len(t.packages) > 3
+    rows = set()
+    for p in t.packages:
+        r0 = p.offset_wg * 128 // w
+        rows.update(range(max(0, r0 - 64), min(h, r0 + 64)))
+    rows = np.array(sorted(rows))
+    idx = (rows[:, None] * w + np.arange(w)[None, :]).ravel()
+    exp = oracle.gaussian(img, filt, w, h, f)
+    assert rel_err(out[idx], exp[idx]).max() <= 1e-5
+    assert rel_err(out, separable_f64(img, w, h, f, 5.0)).max() <= 1e-5
+
+
+def test_gaussian_engines_on_one_gpu_concurrently(gpu_available, oracle):
+    """Two engines with different filters running at the same time on one
+    GPU (two host threads): each launch carries its own filter, so neither
+    sees the other's."""
+    import threading
+    w, h = 1024, 512
+    img, f_wide = W.gaussian_inputs(w, h, 31, seed=8)
+    f_sharp = W.gaussian_filter(31, 1.5).ravel()
+    errs = []
+
+    def worker(filt):
+        try:
+            prog = P.validate_program(W.gaussian_spec(w, h, 31))
+            exp = oracle.gaussian(img, filt, w, h, 31)
+            with P.Engine(P.EngineConfig(devices(2), P.DynamicConfig(16)), prog) as e:
+                for _ in range(6):
+                    out = np.empty(w * h, np.float32)
+                    e.run_into([img, filt], [out])
+                    if rel_err(out, exp).max() > 1e-5:
+                        errs.append("mixed filters")
+        except Exception as ex:  # noqa: BLE001
+            errs.append(repr(ex))
+
+    th = [threading.Thread(target=worker, args=(f,)) for f in (f_wide, f_sharp)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs, errs
