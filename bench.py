@@ -16,10 +16,12 @@ One step = one Engine run over the whole index space (NBody: 10 timesteps).
           the vector peak measured on this device (ecl_probe_vector_peaks;
           MEASURED_PEAKS.json has HBM and bf16 only).
   cpu_baseline   the reference engine itself (oracle/_ref: wall mode, H
-          NativePool devices x 1 worker, Dynamic{max(64,16H)}) on a bounded
-          sample; for the kernels the reference lacks it drives this repo's
-          C restatement as an injected KernelFn.
---impl reference times that CPU reference as the reference arm.
+          NativePool devices x 1 worker, the same scheduler) on the full
+          config (NBody: a bounded sample); for the kernels the reference
+          lacks it drives this repo's C restatement as an injected KernelFn.
+--impl reference times that CPU reference as the reference arm, on the same
+config; it loads only oracle/_ref (inputs from oracle/oracle.c, the same
+bytes as workloads.py's generators), never the product package.
 """
 from __future__ import annotations
 
@@ -59,8 +61,45 @@ def load_json(rel):
 # ---------------------------------------------------------------------------
 # workloads (BASELINE.json configs)
 
+def describe_doc(doc):
+    """Scheduler description (the engine's describe(), schedulers.hpp:18-30) of
+    a schema-1 scheduler dict, without loading the product library."""
+    t = doc["type"]
+    if t == "static":
+        return "static(props=power)"
+    if t == "dynamic":
+        return f"dynamic(packages={doc['num_packages']})"
+    s = f"hguided(k={doc.get('k', 2.0):g}"
+    if doc.get("adaptive"):
+        s += f";adaptive={doc.get('ema_alpha', 0.5):g}"
+    return s + ")"
+
+
+class OracleInputs:
+    """The synthetic inputs of workloads.py (gaussian_inputs, nbody_inputs,
+    binomial_inputs, ray_scene) made by oracle/oracle.c instead — the same
+    bytes (tests/test_bench_cpu.py checks) — so the reference arm builds its
+    inputs without loading the product package."""
+
+    def __init__(self, orc, np):
+        self.o, self.np = orc, np
+
+    def gaussian_inputs(self, w, h, f=31, seed=42):
+        return [self.o.fill_f64(seed, w * h).astype(self.np.float32), self.o.gaussian_filter(f, 5.0)]
+
+    def nbody_inputs(self, n, seed=42):
+        return list(self.o.nbody_init(seed, n))
+
+    def binomial_inputs(self, n, seed=42):
+        return [self.o.binomial_init(seed, n)]
+
+    def ray_scene(self, spheres=64, seed=42):
+        return self.o.ray_scene(seed, spheres)
+
+
 class Workload:
     name = ""
+    LWS_CFG = 1
     workload = ""
     dtype = "f32"
     bound = "fp32"
@@ -74,17 +113,29 @@ class Workload:
     def scheduler(self, n):
         return self.P.HGuidedConfig()
 
+    def sched_doc(self, n):
+        """The scheduler as a schema-1 dict (both arms; config.hpp:41-62)."""
+        return {"type": "hguided", "k": 2.0}
+
     def min_package(self, n):
         return 1
 
     def host_inputs(self):
         return []
 
-    def cpu_sample(self, ref, inputs, threads):
+    def cpu_run(self, ref, inputs, threads, full=True):
+        """Reference engine on this workload: (seconds, work-items, what ran)."""
         raise NotImplementedError
 
     def check(self, outputs):
         return True
+
+    def config(self, n, sched_doc=None):
+        """The `config` object both arms print (identical for the same N)."""
+        return {"workload": self.workload, "scheduler": describe_doc(sched_doc or self.sched_doc(n)),
+                "lws": self.LWS_CFG, "work_items_per_step": self.units(),
+                "l2": "GPU arm: L2 flushed before every timed step on every GPU (512 MiB write each, outside "
+                      "the step's CUDA events)"}
 
 
 class Mandelbrot(Workload):
@@ -92,6 +143,7 @@ class Mandelbrot(Workload):
     ceiling = (8.0 / 12.0, "8 counted flops in 6 unfused FP64 instructions per iteration (bit-exact: no contraction)")
     name = "mandelbrot"
     W_PX, ITERS, LWS = 16384, 2048, 256
+    LWS_CFG = LWS
     VIEWPORT = (-2.5, -1.25, 1.0, 1.25)
     SUM_COUNT, INSIDE = 96_141_151_663, 46_275_993  # SURVEY §8c golden facts
     dtype = "f64"
@@ -119,15 +171,19 @@ class Mandelbrot(Workload):
         return (int(counts.sum(dtype=self.np.uint64)) == self.SUM_COUNT and
                 int((counts >= self.ITERS).sum()) == self.INSIDE)
 
-    def cpu_sample(self, ref, inputs, threads):
-        sw = 4096
+    def cpu_run(self, ref, inputs, threads, full=True):
+        # the reference's own Mandelbrot kernel (workloads.hpp:78-100) in its
+        # own engine, same program and scheduler as the B200 arm; warm-up
+        # passes take a 4096^2 sub-grid of the same viewport
+        sw = self.W_PX if full else 4096
         prog = {"kernel": "mandelbrot", "global_work_size": sw * sw, "local_work_size": self.LWS,
                 "out_pattern": {"out_indices": 4, "work_items": 1},
                 "out_buffers": [{"name": "counts", "element_size_bytes": 4, "element_count": sw * sw * 4}],
                 "args": [sw, sw, self.ITERS] + list(self.VIEWPORT)}
-        s, _ = ref.wall_run(prog, threads, 1, max(64, 16 * threads))
-        return s, sw * sw, (f"{sw}x{sw} sub-grid of the same viewport, max_iter {self.ITERS} (1/16 of the pixels); "
-                            f"reference kernel workloads.hpp:78-100")
+        s, _ = ref.wall_run_sched(prog, self.sched_doc(1), threads, 1)
+        what = (f"full {sw}x{sw} x {self.ITERS} config" if full else
+                f"{sw}x{sw} sub-grid of the same viewport (warm-up)")
+        return s, sw * sw, f"{what}; reference kernel workloads.hpp:78-100 in the reference Engine::run"
 
 
 class MandelbrotPeriodic(Mandelbrot):
@@ -163,6 +219,7 @@ class Gaussian(Workload):
     name = "gaussian"
     WIDTH = HEIGHT = 4096
     F = 31
+    LWS_CFG = 128
     workload = "gaussian 4096x4096 float image, 31x31 filter (sigma 5), clamp-to-edge, static, single device"
     # 32 row bands: H2D of band k+1 and D2H of band k-1 overlap band k (e2e measured:
     # 2^19 items 1.66-1.74 ms, 2^20 1.81-1.89, 2^21 1.96, 2^18 1.93, 2^17 2.30)
@@ -173,6 +230,9 @@ class Gaussian(Workload):
 
     def scheduler(self, n):
         return self.P.StaticConfig()
+
+    def sched_doc(self, n):
+        return {"type": "static"}
 
     def units(self):
         return self.WIDTH * self.HEIGHT
@@ -188,10 +248,11 @@ class Gaussian(Workload):
         # a normalized positive filter over U[0,1) keeps pixels in [0,1) with mean ~0.5
         return bool(self.np.isfinite(out).all() and out.min() >= 0 and out.max() < 1 and abs(out.mean() - 0.5) < 0.01)
 
-    def cpu_sample(self, ref, inputs, threads):
+    def cpu_run(self, ref, inputs, threads, full=True):
         n = self.units()
         out = self.np.zeros(n, self.np.float32)
-        s = ref.wall_run_restated("gaussian", inputs, out, n, 1, [self.WIDTH, self.HEIGHT, self.F], threads)
+        s = ref.wall_run_restated("gaussian", inputs, out, n, 1, [self.WIDTH, self.HEIGHT, self.F], threads,
+                                  self.sched_doc(1))
         return s, n, "full 4096x4096 image; restated kernel oracle.c:orc_gaussian injected as KernelFn"
 
 
@@ -199,6 +260,7 @@ class NBody(Workload):
     ceiling = (20.0 / 24.0, "20 counted flops per interaction in 12 FP32 lane-ops (+1 MUFU)")
     name = "nbody"
     N = 1 << 20
+    LWS_CFG = 64
     steps_per_run = 10
     swaps = ((0, 0), (1, 1))
     workload = "nbody 1048576 bodies x 10 timesteps, dt 0.005, eps2 500, dynamic, NVLink owner-slice exchange"
@@ -208,6 +270,9 @@ class NBody(Workload):
 
     def scheduler(self, n):
         return self.P.DynamicConfig(max(8, 4 * n))
+
+    def sched_doc(self, n):
+        return {"type": "dynamic", "num_packages": max(8, 4 * n)}
 
     def units(self):
         return self.N * self.steps_per_run
@@ -222,11 +287,13 @@ class NBody(Workload):
         pos = outputs[0].view(self.np.float32).reshape(-1, 4)
         return bool(self.np.isfinite(pos).all() and (pos[:, 3] >= 1).all())
 
-    def cpu_sample(self, ref, inputs, threads):
-        targets = 8192
+    def cpu_run(self, ref, inputs, threads, full=True):
+        # the full config is 1.1e13 interactions (~40 min on 16 cores): always a sample
+        targets = 8192 if full else 1024
         out = self.np.zeros((self.N, 4), self.np.float32)
         s = ref.wall_run_restated("nbody", inputs, out, targets, self.N // targets, [self.N, 0.005, 500.0], threads)
-        return s, targets, (f"{targets} target bodies (stride {self.N // targets}) x all {self.N} sources x 1 step; "
+        return s, targets, (f"{targets} target bodies (stride {self.N // targets}) x all {self.N} sources x 1 step "
+                            "(sampled: the full 10-step config takes ~40 min on the host); "
                             "restated kernel oracle.c:orc_nbody_step")
 
 
@@ -236,6 +303,7 @@ class Binomial(Workload):
     name = "binomial"
     OPTIONS = 8 * 1024 * 1024
     STEPS = 254
+    LWS_CFG = STEPS + 1
     workload = "binomial 8388608 options x 254 steps (2097152 float4 work-groups of 255), hguided"
 
     def spec(self):
@@ -257,12 +325,13 @@ class Binomial(Workload):
         call = outputs[0].view(self.np.float32)
         return bool(self.np.isfinite(call).all() and (call >= 0).all() and (call <= 30.0001).all())
 
-    def cpu_sample(self, ref, inputs, threads):
-        stride = 64
+    def cpu_run(self, ref, inputs, threads, full=True):
+        stride = 1 if full else 64
         n = self.OPTIONS // stride
         out = self.np.zeros(self.OPTIONS, self.np.float32)
-        s = ref.wall_run_restated("binomial", inputs, out, n, stride, [self.STEPS], threads)
-        return s, n, f"{n} options (every {stride}th) x {self.STEPS} steps; restated kernel oracle.c:orc_binomial"
+        s = ref.wall_run_restated("binomial", inputs, out, n, stride, [self.STEPS], threads, self.sched_doc(1))
+        what = "all 8388608 options" if full else f"{n} options (every {stride}th, warm-up)"
+        return s, n, f"{what} x {self.STEPS} steps; restated kernel oracle.c:orc_binomial"
 
 
 class Ray(Workload):
@@ -270,6 +339,7 @@ class Ray(Workload):
     name = "ray"
     WIDTH = HEIGHT = 8192
     SPHERES, DEPTH = 64, 4
+    LWS_CFG = 128
     workload = "ray 8192x8192, 64 spheres + plane, 3 lights, shadows, reflections depth 4, hguided"
     # smaller sub-launches shorten the last copy's tail (e2e measured: 2^20 items
     # 19.7-19.8 ms, 2^21 19.9-20.2, 2^22 19.9-20.0, 2^23 20.3-20.4)
@@ -299,13 +369,14 @@ class Ray(Workload):
         hist = self.np.bincount(img[:, 3].astype(int), minlength=len(g["bounce_histogram"]))
         return [int(x) for x in hist] == g["bounce_histogram"]
 
-    def cpu_sample(self, ref, inputs, threads):
-        stride = 16
+    def cpu_run(self, ref, inputs, threads, full=True):
+        stride = 1 if full else 16
         n = self.units() // stride
         out = self.np.zeros((self.units(), 4), self.np.float32)
         s = ref.wall_run_restated("ray", inputs, out, n, stride,
-                                  [self.WIDTH, self.HEIGHT, self.SPHERES, self.DEPTH], threads)
-        return s, n, f"{n} pixels (every {stride}th of 8192^2); restated kernel oracle.c:orc_ray"
+                                  [self.WIDTH, self.HEIGHT, self.SPHERES, self.DEPTH], threads, self.sched_doc(1))
+        what = "all 8192^2 pixels" if full else f"{n} pixels (every {stride}th, warm-up)"
+        return s, n, f"{what}; restated kernel oracle.c:orc_ray"
 
 
 WORKLOADS = {c.name: c for c in (Mandelbrot, MandelbrotPeriodic, MandelbrotF32, Gaussian, NBody, Binomial, Ray)}
@@ -397,13 +468,66 @@ class ClockSampler:
                 "samples": len(self.samples), "source": "nvml", "power_w_max": max(power) if power else None}
 
 
-def merge_clocks(*cs):
+def merge_clocks(*cs, per_gpu=None):
+    """One clocks object over several samplers (several GPUs and/or timed
+    regions): the lowest median SM clock, every reason seen; with per_gpu
+    (the ordinals of cs, in order) also each GPU's own summary."""
     cs = [c for c in cs if c]
     sm = [c["sm_mhz"] for c in cs if c.get("sm_mhz")]
-    return {"sm_mhz": min(sm) if sm else None, "sm_max_mhz": max((c["sm_max_mhz"] or 0) for c in cs) or None,
-            "reasons": sorted(set().union(*[set(c["reasons"]) for c in cs])),
-            "samples": sum(c["samples"] for c in cs),
-            "power_w_max": max((c.get("power_w_max") or 0) for c in cs) or None}
+    out = {"sm_mhz": min(sm) if sm else None, "sm_max_mhz": max((c["sm_max_mhz"] or 0) for c in cs) or None,
+           "reasons": sorted(set().union(*[set(c["reasons"]) for c in cs])),
+           "samples": sum(c["samples"] for c in cs),
+           "power_w_max": max((c.get("power_w_max") or 0) for c in cs) or None}
+    if per_gpu is not None:
+        out["per_gpu"] = {str(d): {k: c.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons", "samples")}
+                          for d, c in zip(per_gpu, cs)}
+    else:
+        merged = {}
+        for c in cs:
+            merged.update(c.get("per_gpu", {}))
+        if merged:
+            out["per_gpu"] = merged
+    return out
+
+
+def busy_per_device(trace):
+    """Device busy time of one run: the union of its packages' kernel
+    intervals per device (packages overlap on the two lanes, so a plain sum
+    double-counts)."""
+    iv = {}
+    for p in trace.packages:
+        iv.setdefault(p.device_id, []).append((p.t_start_ms, p.t_end_ms))
+    out = {}
+    for dev, xs in iv.items():
+        xs.sort()
+        total, cur0, cur1 = 0.0, None, None
+        for a, b in xs:
+            if cur1 is None or a > cur1:
+                if cur1 is not None:
+                    total += cur1 - cur0
+                cur0, cur1 = a, b
+            else:
+                cur1 = max(cur1, b)
+        if cur1 is not None:
+            total += cur1 - cur0
+        out[dev] = total
+    return out
+
+
+def pcie_d2h_gbps(torch, ordinal, nbytes=256 << 20):
+    """Device-to-pinned-host copy rate of one GPU (CUDA events)."""
+    src = torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", ordinal))
+    dst = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    with torch.cuda.device(ordinal):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(3):
+            dst.copy_(src, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        return 3 * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9
 
 
 # ---------------------------------------------------------------------------
@@ -441,37 +565,43 @@ def init_dist():
     return env_int("WORLD_SIZE", 1), env_int("RANK", 0), env_int("LOCAL_RANK", 0)
 
 
-def reference_measure(wl, steps, threads):
-    """Times the reference engine on the workload's bounded sample."""
+def reference_runner(np):
+    """(reference library, synthetic-input maker): oracle/_ref and oracle.c only."""
     from tests import _oracle
     ref = _oracle.Reference.load()
     if ref is None:
         raise RuntimeError("oracle/_ref is not built (make -C oracle where /root/reference exists)")
-    inputs = wl.host_inputs()
-    times, units, sample = [], 0, ""
-    for _ in range(steps):
-        s, units, sample = wl.cpu_sample(ref, inputs, threads)
-        times.append(s)
-    return times, units, sample
+    return ref, OracleInputs(_oracle.Oracle(), np)
 
 
 def run_reference(args, world, rank):
+    """The reference arm: the reference's own engine (oracle/_ref, wall mode,
+    H NativePool devices x 1 worker) on the same workload, program and
+    scheduler as the B200 arm, on this box's host cores.  Warm-up passes run
+    a smaller sample; every timed pass runs the full config (NBody: a
+    bounded sample, the full config is ~40 min).  Loads no product code."""
     if rank != 0:
         return 0
     import numpy as np
-    import paper_1805_02755_b200 as P
-    from paper_1805_02755_b200 import workloads as W
-    wl = WORKLOADS[args.workload](P, W, np)
+    ref, synth = reference_runner(np)
+    wl = WORKLOADS[args.workload](None, synth, np)
     h = cpu_threads()
-    times, units, sample = reference_measure(wl, args.warmup + args.steps, h)
-    timed = times[args.warmup:] or times
-    sec = sum(timed) / len(timed)
+    inputs = wl.host_inputs()
+    for _ in range(args.warmup):
+        wl.cpu_run(ref, inputs, h, full=False)
+    secs, units, sample = [], 0, ""
+    for _ in range(args.steps):
+        s, units, sample = wl.cpu_run(ref, inputs, h, full=True)
+        secs.append(s)
+    sec = sum(secs) / len(secs)
     value = units / sec
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "work-items/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic",
-            "config": {"workload": wl.workload + " (sampled)", "sample": sample,
-                       "scheduler": f"dynamic(packages={max(64, 16 * h)})"},
+            "config": wl.config(args.gpus),
+            "reference": {"engine": f"reference coexec::Engine (oracle/_ref), wall mode, {h} NativePool devices "
+                                    "x 1 worker", "sample": sample,
+                          "warmup": "warm-up passes on a smaller sample of the same workload"},
             "cpu_baseline": {"value": value, "unit": "work-items/s", "cores": h, "kind": "reference",
                              "sample": sample},
             "e2e": {"value": value, "unit": "work-items/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -625,17 +755,23 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
         else:
             eng.run_into(inputs, outputs, want_trace=False)
 
-    # L2 flush between timed steps: a 512 MiB write (4x the 126 MB L2) on this
-    # rank's GPU before every step, outside the step's events.
-    flush_buf = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=torch.device("cuda", torch.cuda.current_device()))
+    # L2 flush between timed steps: a 512 MiB write (4x the 126 MB L2) on
+    # every GPU this process drives, before every step, outside the step's events.
+    my_gpus = [rank % ngpu] if shared else sorted({i % ngpu for i in range(n)})
+    flush_bufs = [torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=torch.device("cuda", d)) for d in my_gpus]
+
+    def flush_l2():
+        for b in flush_bufs:
+            b.zero_()
+        for d in my_gpus:
+            torch.cuda.synchronize(d)
 
     def timed(fn, steps):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         total = 0.0
         for _ in range(steps):
-            flush_buf.zero_()
-            torch.cuda.synchronize()
+            flush_l2()
             barrier()
             e0.record(stream)
             fn()
@@ -650,14 +786,16 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
     run(in_arrays, None)
     for _ in range(max(0, args.warmup - 1)):
         run(None, None)
-    my_gpu = (rank % ngpu) if shared else 0
+    my_gpu = my_gpus[0]
     eng.kernel_timing(reset=True)
-    sampler = ClockSampler(my_gpu).start()
+    samplers = [ClockSampler(d).start() for d in my_gpus]
     ms_dev = max_over_ranks(timed(lambda: run(None, None), args.steps))
-    clocks = sampler.stop()
+    clocks = merge_clocks(*[c.stop() for c in samplers], per_gpu=my_gpus)
+    clocks["region"] = "device-resident"
     kernel_ms, launches = eng.kernel_timing(reset=True)
     last = eng.last_trace()
     bal = P.balance(last) if n > 1 else 1.0
+    busy = busy_per_device(last)
 
     # --- end to end through the C-ABI with page-locked host buffers ---
     for _ in range(args.warmup):
@@ -665,9 +803,9 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
     if rank == 0:
         for a in out_arrays:
             a[:] = 0
-    sampler2 = ClockSampler(my_gpu).start()
+    samplers2 = [ClockSampler(d).start() for d in my_gpus]
     ms_e2e = max_over_ranks(timed(lambda: run(in_arrays, out_arrays), args.steps))
-    clocks2 = sampler2.stop()
+    clocks2 = merge_clocks(*[c.stop() for c in samplers2], per_gpu=my_gpus)
     eng.kernel_timing(reset=True)
     sane = wl.check(out_arrays) if rank == 0 else True
     e2e_trace = eng.last_trace()
@@ -679,8 +817,7 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
     if wl.steps_per_run == 1:
         n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         for _ in range(args.warmup + args.steps):
-            flush_buf.zero_()  # same L2 state as the timed engine steps
-            torch.cuda.synchronize()
+            flush_l2()  # same L2 state as the timed engine steps
             # kernel-only time, and the native program's host call bracketed
             # exactly like an engine step (launch + completion wait included)
             n0.record(stream)
@@ -715,32 +852,70 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
         pb.free()
 
     cpu = None
-    if n == 1 and not args.no_cpu_baseline:
+    if n == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
             h = cpu_threads()
-            times, units_s, sample = reference_measure(wl, 1, h)
-            cpu = {"value": units_s / times[0], "unit": "work-items/s", "cores": h, "kind": "reference",
+            ref, _ = reference_runner(np)
+            secs, units_s, sample = wl.cpu_run(ref, host_in, h, full=True)
+            cpu = {"value": units_s / secs, "unit": "work-items/s", "cores": h, "kind": "reference",
                    "sample": sample + f"; reference engine wall mode, {h} NativePool devices x 1 worker, "
-                                      f"Dynamic{{{max(64, 16 * h)}}}"}
+                                      f"{describe_doc(wl.sched_doc(1))}"}
         except Exception as exc:  # noqa: BLE001 — report it, keep the GPU line
             cpu = {"value": None, "unit": "work-items/s", "cores": cpu_threads(), "kind": "reference",
                    "sample": f"unavailable: {exc}"}
 
     traffic, traffic_basis = ncu_traffic(wl.name)
     units = wl.units()
+    cfg = wl.config(n, sched.to_json())
+    # NVLink peer access between the GPUs this process drives (replication
+    # and exchange copies use it when enabled)
+    p2p = None
+    if len(my_gpus) > 1:
+        pairs = {}
+        for a in my_gpus:
+            for b in my_gpus:
+                if a != b:
+                    can, en = ctypes.c_int(0), ctypes.c_int(0)
+                    N.lib.ecl_peer_access(a, b, ctypes.byref(can), ctypes.byref(en))
+                    pairs[f"{a}->{b}"] = {"can_access": bool(can.value), "enabled": bool(en.value)}
+        p2p = {"pairs": pairs, "all_enabled": all(v["enabled"] for v in pairs.values())}
+    # End-to-end floor at this N: every output byte lands in ONE host's
+    # memory.  Replicated outputs (Mandelbrot 4:1) are widened by the host
+    # pool (measured here, the same for every N: the host is shared); other
+    # outputs are PCIe-bound, N links in parallel (measured on one GPU).
+    floor = None
+    if rank == 0:
+        try:
+            gbps = pcie_d2h_gbps(torch, my_gpu)
+            pcie_ms = d2h / (len(my_gpus) * gbps * 1e9) * 1e3 if not shared else d2h / (n * gbps * 1e9) * 1e3
+            floor = {"pcie_d2h_gbps_per_gpu": gbps, "pcie_ms": pcie_ms}
+            spec0 = prog.spec()
+            if wl.name.startswith("mandelbrot"):
+                wms = ctypes.c_double(0.0)
+                N.lib.ecl_probe_host_widen(spec0.global_work_size, 4, ctypes.byref(wms))
+                floor["host_widen_ms"] = wms.value
+                floor["e2e_floor_ms"] = max(pcie_ms / 4.0, wms.value)
+                floor["basis"] = ("compact counts cross PCIe (1/4 of the output bytes) and the host widens them "
+                                  "4:1 into the caller's buffer: max(PCIe at N links, host widening), and the "
+                                  "host widening is shared by all N GPUs, so end-to-end scaling flattens at it")
+            else:
+                floor["e2e_floor_ms"] = pcie_ms
+                floor["basis"] = "output bytes over N PCIe links at the measured per-GPU D2H rate"
+        except Exception as exc:  # noqa: BLE001
+            floor = {"error": str(exc)}
     line = {
         "metric": METRIC, "value": units / (ms_dev * 1e-3), "unit": "work-items/s", "n_gpus": n,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic",
-        "config": {"workload": wl.workload, "scheduler": P.describe(sched), "lws": prog.local_work_size(),
-                   "work_items_per_step": units, "min_package_work_groups": min_wg, "queue_depth": args.queue_depth,
-                   "widen_per_8": args.widen, "copy_split_items": copy_split,
+        "config": cfg,
+        "engine": {"scheduler": P.describe(sched), "min_package_work_groups": min_wg,
+                   "queue_depth": args.queue_depth, "widen_per_8": args.widen, "copy_split_items": copy_split,
                    "parallelism": f"coexec{n}" + ("-processes" if shared else ""),
                    "coordination": ("one process per GPU, shared-memory decision log" if shared else
                                     "one process, one host thread per GPU"),
-                   "l2": "L2 flushed before every timed step (512 MiB write, outside the step's CUDA events)"},
+                   "gpus_driven": my_gpus, "p2p": p2p},
         "e2e": {"value": units / (ms_e2e * 1e-3), "unit": "work-items/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
+                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e, "floor": floor},
         "roofline": {"bound": wl.bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_basis": traffic_basis,
                      "algorithmic_flops_per_step": wl.flops(),
@@ -764,7 +939,10 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
                    "overhead_pct_vs_native_host": (n * ms_dev - h_native) / h_native * 100.0 if h_native else None,
                    "overhead_pct_e2e": (ms_e2e - t_native_e2e) / t_native_e2e * 100.0
                    if t_native_e2e and n == 1 else None,
-                   "kernel_ms_per_step": kernel_ms / args.steps, "outputs_sane": bool(sane),
+                   # device busy time of the last resident step: union of its packages' kernel intervals
+                   "device_busy_ms": max(busy.values()) if busy else None,
+                   "device_busy_ms_per_device": busy,
+                   "outputs_sane": bool(sane),
                    "e2e_last_kernel_end_ms": e2e_last_kernel_end},
         "gpu_launches": launches,
         "clocks": merge_clocks(clocks, clocks2),

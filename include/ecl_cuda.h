@@ -14,7 +14,10 @@
  * One ecl_gpu = one B200: two compute streams ("lanes", consecutive packages
  * alternate), one copy stream per lane, a notify stream, a ring of timing
  * events, this device's replica of every read-only input and its own output
- * partition.  Each ecl_gpu is driven by exactly one host thread.
+ * partition.  Each ecl_gpu is driven by exactly one host thread.  Completion
+ * is observed through events (ecl_gpu_wait_compute / ecl_gpu_wait /
+ * ecl_gpu_poll); the per-package host callback of ecl_gpu_submit is optional
+ * (the engine passes none and blocks on the kernel-end events).
  *
  * Status codes: ECL_OK (0) or the negated coexec::ErrorCode + 1 (error.hpp:11-39
  * order), so a caller maps them 1:1 onto coexec::Error; device faults map to
@@ -124,6 +127,12 @@ int ecl_replicate_inputs(ecl_gpu* const* gpus, uint32_t n, uint32_t root);
  * compute stream. */
 int ecl_broadcast_output_slice(ecl_gpu* const* gpus, uint32_t n, uint32_t src, uint32_t index,
                                uint64_t elem_offset, uint64_t elem_count);
+/* Peer access from ordinal dst to ordinal src: *can_access from
+ * cudaDeviceCanAccessPeer, *enabled = 1 once the device layer enabled it for
+ * replication / exchange (NVLink P2P in use); same ordinal counts as enabled.
+ * ECL_FORCE_PEER_COPY=1 routes same-ordinal exchange copies through
+ * cudaMemcpyPeerAsync too (tests the peer call path on one GPU). */
+int ecl_peer_access(int dst, int src, int* can_access, int* enabled);
 /* D2H of a slice of one output (used to gather device-resident results). */
 int ecl_gpu_download_slice(ecl_gpu* gpu, uint32_t index, uint64_t elem_offset, uint64_t elem_count,
                            void* host_dst);
@@ -216,6 +225,11 @@ int ecl_probe_vector_peaks(int ordinal, double* fp64_fma_tflops, double* fp64_ad
 int ecl_probe_mandel_mix(int ordinal, double* tflops);
 /* The same for the packed FP32 variant (FFMA2/FADD2, two pixels per lane). */
 int ecl_probe_mandel_mix_f32(int ordinal, double* tflops);
+
+/* Host widening rate (hostpool): *ms to widen `items` uint32 `replicate`-fold
+ * between host buffers on the widen pool's thread count — the host-DRAM floor
+ * of end-to-end runs with replicated outputs (Mandelbrot). */
+int ecl_probe_host_widen(uint64_t items, uint32_t replicate, double* ms);
 
 const char* ecl_last_error(void);
 

@@ -19,6 +19,7 @@
  *      — "parity unpinned" by the reference.
  */
 #include <math.h>
+#include <stdlib.h>
 #include <stdint.h>
 #include <string.h>
 
@@ -299,6 +300,36 @@ void orc_binomial(const float* rand4, float* out4, uint32_t steps, uint64_t firs
 void orc_binomial_init(uint64_t seed, uint64_t n_opt, float* rand4) {
   uint64_t st = seed;
   for (uint64_t i = 0; i < n_opt; ++i) rand4[i] = (float)((double)(splitmix_next(&st) >> 11) * 0x1.0p-53);
+}
+
+/* Ray synthetic scene (layout below): the same arithmetic as
+ * paper_1805_02755_b200/workloads.py:ray_scene — doubles from splitmix64(seed),
+ * eight draws per sphere, cast to float at the end — so bench.py's reference
+ * arm builds the scene without the product package.  buf: (2*ns+8) float4. */
+void orc_ray_scene(uint64_t seed, uint32_t ns, float* buf) {
+  uint64_t st = seed;
+  double* u = (double*)malloc(sizeof(double) * 8 * (size_t)ns);
+  for (uint64_t i = 0; i < 8ull * ns; ++i) u[i] = (double)(splitmix_next(&st) >> 11) * 0x1.0p-53;
+  for (uint64_t i = 0; i < 4ull * (2 * ns + 8); ++i) buf[i] = 0.0f;
+  for (uint32_t k = 0; k < ns; ++k) {
+    const double* v = u + 8 * (size_t)k;
+    const double r = 0.3 + 1.2 * v[2];
+    float* sp = buf + 4 * (size_t)k;
+    float* mt = buf + 4 * ((size_t)ns + k);
+    sp[0] = (float)(-8.0 + 16.0 * v[0]);
+    sp[1] = (float)(r + 2.0 * v[3]);
+    sp[2] = (float)(2.0 + 16.0 * v[1]);
+    sp[3] = (float)r;
+    for (int c = 0; c < 3; ++c) mt[c] = (float)(0.2 + 0.8 * v[4 + c]);
+    mt[3] = (float)((k % 3) == 0 ? 0.6 + 0.3 * v[7] : 0.15 * v[7]);
+  }
+  free(u);
+  static const float tail[7][4] = {{0.0f, 2.5f, -12.0f, 0.6f}, {-10.0f, 12.0f, -6.0f, 0.7f},
+                                   {8.0f, 15.0f, 0.0f, 0.5f},   {0.0f, 20.0f, 10.0f, 0.4f},
+                                   {0.9f, 0.9f, 0.9f, 0.3f},    {0.08f, 0.5f, 0.0f, 0.0f},
+                                   {0.25f, 0.35f, 0.55f, 0.0f}};
+  for (int t = 0; t < 7; ++t)
+    for (int c = 0; c < 4; ++c) buf[4 * (2 * (size_t)ns + t) + c] = tail[t][c];
 }
 
 int orc_num_threads(void) {

@@ -160,6 +160,38 @@ double ref_wall_run(const char* program_json, uint32_t devices, uint32_t workers
   }
 }
 
+// The same with any scheduler (config.hpp:41 scheduler_from_json), so the
+// reference arm runs the very configuration the B200 arm runs (HGuided k=2
+// for Mandelbrot).  `devices` NativePool devices x `workers` threads each.
+double ref_wall_run_sched(const char* program_json, const char* scheduler_json, uint32_t devices, uint32_t workers,
+                          uint64_t seed, uint64_t* fnv) {
+  try {
+    const auto prog = validate_program(program_from_json(json::parse(program_json)));
+    EngineConfig cfg;
+    for (uint32_t d = 0; d < devices; ++d) {
+      DeviceProfile dev;
+      dev.id = "cpu" + std::to_string(d);
+      dev.name = dev.id;
+      dev.backend = {BackendKind::NativePool, workers};
+      cfg.devices.push_back(dev);
+    }
+    apply_default_min_package(cfg.devices);
+    cfg.scheduler = scheduler_from_json(json::parse(scheduler_json));
+    cfg.clock_mode = ClockMode::Wall;
+    cfg.seed = seed;
+    const auto inputs = fill_default_inputs(prog, seed);
+    Engine engine(cfg, prog);
+    const auto t0 = std::chrono::steady_clock::now();
+    const auto result = engine.run(inputs);
+    const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (fnv) *fnv = fnv1a(result.outputs);
+    return s;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return -1.0;
+  }
+}
+
 // make_report over a trace JSON; reference_ms < 0 means "no overhead".
 int64_t ref_report_json(const char* trace_json, const double* solo, uint32_t nsolo, double reference_ms,
                         char* out, uint64_t cap) {
@@ -177,12 +209,13 @@ int64_t ref_report_json(const char* trace_json, const double* solo, uint32_t nso
 
 // CPU baseline for the kernels the reference does not have (SURVEY §8d,
 // BASELINE.md §3): the reference engine itself in wall mode (devices x 1
-// worker, Dynamic{max(64,16*devices)}) drives this repo's C restatement,
-// injected as a KernelFn through Engine::run(inputs, kernel, cost)
-// (engine.hpp:223).  Work-item i of the sampled program is item i*stride of
-// the real workload.  Returns wall seconds of Engine::run, -1 on error.
+// worker, the given scheduler; NULL = Dynamic{max(64,16*devices)}) drives
+// this repo's C restatement, injected as a KernelFn through
+// Engine::run(inputs, kernel, cost) (engine.hpp:223).  Work-item i of the
+// program is item i*stride of the real workload (stride 1 = the whole
+// workload).  Returns wall seconds of Engine::run, -1 on error.
 double ref_wall_run_restated(const char* kind, const void* in0, const void* in1, void* out, uint64_t sample,
-                             uint64_t stride, const double* p, uint32_t devices) {
+                             uint64_t stride, const double* p, uint32_t devices, const char* scheduler_json) {
   try {
     const std::string k = kind;
     KernelFn fn;
@@ -226,7 +259,10 @@ double ref_wall_run_restated(const char* kind, const void* in0, const void* in1,
       dev.backend = {BackendKind::NativePool, 1};
       cfg.devices.push_back(dev);
     }
-    cfg.scheduler = DynamicConfig{std::max<uint64_t>(64, 16ull * devices)};
+    if (scheduler_json)
+      cfg.scheduler = scheduler_from_json(json::parse(scheduler_json));
+    else
+      cfg.scheduler = DynamicConfig{std::max<uint64_t>(64, 16ull * devices)};
     cfg.clock_mode = ClockMode::Wall;
     Engine engine(cfg, prog);
     const CostFn cost = [](std::uint64_t) { return 1.0; };

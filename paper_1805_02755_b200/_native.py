@@ -82,6 +82,8 @@ _sig("ecl_host_unregister", c_int, c_void_p)
 _sig("ecl_host_alloc", c_int, ctypes.c_size_t, ctypes.POINTER(c_void_p))
 _sig("ecl_host_free", c_int, c_void_p)
 _sig("ecl_last_error", c_char_p)
+_sig("ecl_peer_access", c_int, c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int))
+_sig("ecl_probe_host_widen", c_int, c_u64, c_u32, ctypes.POINTER(c_dbl))
 _sig("ecl_probe_vector_peaks", c_int, c_int, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl))
 
 ERROR_NAMES = [

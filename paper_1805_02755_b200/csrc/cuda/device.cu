@@ -386,13 +386,34 @@ void free_buffers(ecl_gpu* g) {
   g->out_bytes.clear();
 }
 
+// Peer access state per (dst, src) ordinal pair: 0 unknown, 1 enabled (dst
+// reads/writes src's memory over NVLink), 2 not possible (copies then stage
+// through the host).
+std::mutex g_peer_m;
+int g_peer[64][64] = {};
+
 void enable_peer(int dst, int src) {
   if (dst == src) return;
+  std::lock_guard lock(g_peer_m);
+  if (g_peer[dst & 63][src & 63] != 0) return;
   cudaSetDevice(dst);
   int can = 0;
   cudaDeviceCanAccessPeer(&can, dst, src);
-  if (can) cudaDeviceEnablePeerAccess(src, 0);  // AlreadyEnabled is fine
+  cudaError_t e = cudaErrorPeerAccessUnsupported;
+  if (can) e = cudaDeviceEnablePeerAccess(src, 0);
+  g_peer[dst & 63][src & 63] = (e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled) ? 1 : 2;
   cudaGetLastError();
+}
+
+// ECL_FORCE_PEER_COPY=1: owner-slice copies between logical devices on ONE
+// ordinal also go through cudaMemcpyPeerAsync (the multi-GPU call path),
+// so a one-GPU box exercises it.
+bool force_peer_copy() {
+  static const bool on = [] {
+    const char* v = std::getenv("ECL_FORCE_PEER_COPY");
+    return v && std::string(v) == "1";
+  }();
+  return on;
 }
 
 }  // namespace
@@ -690,7 +711,7 @@ int ecl_broadcast_output_slice(ecl_gpu* const* gpus, uint32_t n, uint32_t src_i,
     if (d == src_i || dst->out.size() <= index) continue;
     char* to = static_cast<char*>(dst->out[index]) + elem_offset * esz;
     const char* from = static_cast<const char*>(src->out[index]) + elem_offset * esz;
-    if (dst->ordinal == src->ordinal)
+    if (dst->ordinal == src->ordinal && !force_peer_copy())
       ECL_CK(cudaMemcpyAsync(to, from, elem_count * esz, cudaMemcpyDeviceToDevice, src->lane[0]));
     else
       ECL_CK(cudaMemcpyPeerAsync(to, dst->ordinal, from, src->ordinal, elem_count * esz, src->lane[0]));
@@ -715,6 +736,24 @@ int ecl_gpu_download_slice(ecl_gpu* g, uint32_t index, uint64_t elem_offset, uin
                          cudaMemcpyDeviceToHost, g->copy[0]));
   ECL_CK(cudaStreamSynchronize(g->copy[0]));
   return ECL_OK;
+}
+
+int ecl_peer_access(int dst, int src, int* can_access, int* enabled) {
+  *can_access = 0;
+  *enabled = 0;
+  if (dst == src) {
+    *can_access = *enabled = 1;
+    return ECL_OK;
+  }
+  ECL_CK(cudaDeviceCanAccessPeer(can_access, dst, src));
+  std::lock_guard lock(g_peer_m);
+  *enabled = g_peer[dst & 63][src & 63] == 1;
+  return ECL_OK;
+}
+
+int ecl_probe_host_widen(uint64_t items, uint32_t replicate, double* ms) {
+  *ms = ecl::widen_probe_ms(items, replicate);
+  return *ms >= 0.0 ? ECL_OK : fail(ECL_CONFIG_ERROR, "widen probe: allocation failed");
 }
 
 int ecl_host_register(void* ptr, size_t bytes) {

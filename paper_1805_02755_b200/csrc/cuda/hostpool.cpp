@@ -12,6 +12,7 @@
 #include <emmintrin.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <atomic>
 #include <condition_variable>
@@ -155,6 +156,32 @@ void widen_async(int device, cudaEvent_t ready, const uint32_t* src, uint32_t* d
 }
 
 unsigned widen_workers() { return pool().size(); }
+
+double widen_probe_ms(uint64_t items, uint32_t rep) {
+  // The pool's own arithmetic and thread count on fresh huge-page buffers,
+  // without the CUDA event gating: what host DRAM sustains for widening.
+  const unsigned n = std::max(1u, pool().size());
+  std::vector<uint32_t> src(items);
+  for (uint64_t i = 0; i < items; ++i) src[i] = static_cast<uint32_t>(i);
+  void* raw = nullptr;
+  if (posix_memalign(&raw, 1 << 21, items * rep * sizeof(uint32_t)) != 0) return -1.0;
+  auto* dst = static_cast<uint32_t*>(raw);
+  auto pass = [&] {
+    std::vector<std::thread> ts;
+    const uint64_t per = (items + n - 1) / n;
+    for (unsigned t = 0; t < n; ++t) {
+      const uint64_t a = std::min<uint64_t>(items, t * per), b = std::min<uint64_t>(items, a + per);
+      ts.emplace_back([&, a, b] { widen(src.data() + a, dst + a * rep, b - a, rep); });
+    }
+    for (auto& t : ts) t.join();
+  };
+  pass();  // first touch of the destination pages
+  const auto t0 = std::chrono::steady_clock::now();
+  pass();
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  free(raw);
+  return ms;
+}
 
 bool widen_wait(WidenTicket* ticket) {
   std::unique_lock lock(ticket->m);  // always: see the worker's decrement

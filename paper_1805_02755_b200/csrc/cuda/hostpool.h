@@ -29,6 +29,11 @@ void widen_async(int device, cudaEvent_t ready, const uint32_t* src, uint32_t* d
 // Number of widen worker threads.
 unsigned widen_workers();
 
+// Milliseconds the pool's threads take to widen `items` values `rep`-fold
+// between host buffers (second pass, pages already touched): the host-DRAM
+// floor of an end-to-end run whose outputs are widened.
+double widen_probe_ms(uint64_t items, uint32_t rep);
+
 // Blocks until every job of the ticket finished; false if a copy failed.
 bool widen_wait(WidenTicket* ticket);
 

@@ -45,6 +45,7 @@ class Oracle:
         lib.orc_nbody_init.argtypes = [U64, U64, VP, VP]
         lib.orc_binomial.argtypes = [VP, VP, U32, U64, U64]
         lib.orc_binomial_init.argtypes = [U64, U64, VP]
+        lib.orc_ray_scene.argtypes = [U64, U32, VP]
         lib.orc_num_threads.restype = ctypes.c_int
         lib.orc_ray.argtypes = [VP, U32, U32, U32, U32, VP, U64, U64, VP]
 
@@ -117,6 +118,16 @@ class Oracle:
         self.lib.orc_binomial(rand.ctypes.data, out.ctypes.data, steps, first, count)
         return out
 
+    def binomial_init(self, seed, n):
+        out = np.zeros(n, np.float32)
+        self.lib.orc_binomial_init(seed, n, out.ctypes.data)
+        return out
+
+    def ray_scene(self, seed, spheres):
+        out = np.zeros((2 * spheres + 8, 4), np.float32)
+        self.lib.orc_ray_scene(seed, spheres, out.ctypes.data)
+        return out
+
     def threads(self) -> int:
         return self.lib.orc_num_threads()
 
@@ -142,15 +153,17 @@ class Reference:
         lib.ref_wall_run.restype = D
         lib.ref_wall_run.argtypes = [ctypes.c_char_p, U32, U32, U64, U64, ctypes.POINTER(U64)]
 
-    def wall_run_restated(self, kind, inputs, out, sample, stride, params, devices):
-        """Reference engine (wall mode) driving oracle.c's restated kernel."""
+    def wall_run_restated(self, kind, inputs, out, sample, stride, params, devices, scheduler=None):
+        """Reference engine (wall mode) driving oracle.c's restated kernel;
+        scheduler: a schema-1 scheduler dict (None = Dynamic{max(64,16H)})."""
         f = self.lib.ref_wall_run_restated
         f.restype = D
-        f.argtypes = [ctypes.c_char_p, VP, VP, VP, U64, U64, ctypes.POINTER(D), U32]
+        f.argtypes = [ctypes.c_char_p, VP, VP, VP, U64, U64, ctypes.POINTER(D), U32, ctypes.c_char_p]
         ins = [np.ascontiguousarray(a) for a in inputs] + [None, None]
         p = (D * len(params))(*params)
         s = f(kind.encode(), ins[0].ctypes.data if ins[0] is not None else None,
-              ins[1].ctypes.data if ins[1] is not None else None, out.ctypes.data, sample, stride, p, devices)
+              ins[1].ctypes.data if ins[1] is not None else None, out.ctypes.data, sample, stride, p, devices,
+              json.dumps(scheduler).encode() if scheduler else None)
         if s < 0:
             raise RuntimeError(self.lib.ref_last_error().decode())
         return s
@@ -176,6 +189,17 @@ class Reference:
         buf = ctypes.create_string_buffer(n + 1)
         self.lib.ref_run_json(json.dumps(config).encode(), buf, n + 1, ctypes.byref(fnv))
         return json.loads(buf.value.decode()), fnv.value
+
+    def wall_run_sched(self, program: dict, scheduler: dict, devices: int, workers: int, seed: int = 0):
+        """Reference Engine::run in wall mode with any scheduler (schema-1 dict)."""
+        f = self.lib.ref_wall_run_sched
+        f.restype = D
+        f.argtypes = [ctypes.c_char_p, ctypes.c_char_p, U32, U32, U64, ctypes.POINTER(U64)]
+        fnv = U64(0)
+        s = f(json.dumps(program).encode(), json.dumps(scheduler).encode(), devices, workers, seed, ctypes.byref(fnv))
+        if s < 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return s, fnv.value
 
     def wall_run(self, program: dict, devices: int, workers: int, packages: int, seed: int = 0):
         fnv = U64(0)

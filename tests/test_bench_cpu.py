@@ -51,3 +51,54 @@ def test_shared_output_dir_falls_back_when_dev_shm_is_small(monkeypatch, shm_fre
     monkeypatch.setattr(os.path, "isdir", lambda d: d in ("/dev/shm", "/tmp"))
     monkeypatch.delenv("TMPDIR", raising=False)
     assert bench.shared_out_dir(argparse.Namespace(workload="mandelbrot")) == expect
+
+
+def test_reference_inputs_are_the_product_inputs_byte_for_byte(oracle):
+    """The reference arm makes its inputs with oracle.c (OracleInputs); they
+    must be the very bytes workloads.py gives the B200 arm."""
+    synth = bench.OracleInputs(oracle, np)
+    for name, cls in bench.WORKLOADS.items():
+        ours = cls(P, W, np).host_inputs()
+        theirs = cls(None, synth, np).host_inputs()
+        assert len(ours) == len(theirs), name
+        for a, b in zip(ours, theirs):
+            assert np.ascontiguousarray(a).tobytes() == np.ascontiguousarray(b).tobytes(), name
+
+
+@pytest.mark.parametrize("name", sorted(bench.WORKLOADS))
+@pytest.mark.parametrize("n", [1, 2, 8])
+def test_both_arms_print_the_same_config(oracle, name, n):
+    cls = bench.WORKLOADS[name]
+    ours = cls(P, W, np)
+    sched = ours.scheduler(n)
+    theirs = cls(None, bench.OracleInputs(oracle, np), np)
+    assert ours.config(n, sched.to_json()) == theirs.config(n)
+    assert bench.describe_doc(sched.to_json()) == P.describe(sched)
+
+
+def test_describe_doc_matches_the_engine():
+    for cfg in (P.StaticConfig(), P.DynamicConfig(12), P.HGuidedConfig(k=3.0), P.HGuidedConfig(adaptive=True)):
+        assert bench.describe_doc(cfg.to_json()) == P.describe(cfg)
+
+
+def test_reference_arm_loads_no_product_code(tmp_path):
+    """--impl reference runs the reference (oracle/_ref) only: the product
+    package is never imported and none of its libraries is mapped."""
+    import json
+    import subprocess
+    import sys
+    from tests._oracle import REF_SO
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref not built")
+    code = ("import sys, json, bench\n"
+            "rc = bench.main(['--impl', 'reference', '--workload', 'gaussian', '--steps', '1', '--warmup', '0'])\n"
+            "maps = open('/proc/self/maps').read()\n"
+            "print(json.dumps({'rc': rc, 'imported': [m for m in sys.modules if m.startswith('paper_1805')],\n"
+            "                  'libs': [l for l in ('libcoexec.so', 'libecl_cuda.so') if l in maps]}))\n")
+    r = subprocess.run([sys.executable, "-c", code], cwd=bench.ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    line, probe = lines[0], lines[-1]
+    assert probe == {"rc": 0, "imported": [], "libs": []}
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["config"]["work_items_per_step"] == 4096 * 4096
