@@ -59,13 +59,8 @@ enum ecl_status {
   ECL_PENDING = 1 /* ecl_gpu_poll: package still running */
 };
 
-/* A kernel argument: coexec::ArgValue = variant<int64_t, double> (core.hpp:75). */
-typedef struct {
-  int32_t is_double;
-  int32_t reserved;
-  int64_t i;
-  double d;
-} ecl_arg;
+/* ecl_arg (coexec::ArgValue, core.hpp:75) and the plugin launch ABI. */
+#include "ecl_plugin.h"
 
 /* Buffer geometry: coexec::BufferDesc without the name (core.hpp:55-64). */
 typedef struct {
@@ -99,6 +94,23 @@ int ecl_kernel_create(const char* kernel_id, uint64_t global_work_size, uint64_t
                       const ecl_buffer_geom* outputs, uint32_t n_outputs, uint64_t out_indices,
                       uint64_t out_work_items, ecl_kernel** out);
 void ecl_kernel_destroy(ecl_kernel* kernel);
+
+/* ---- device kernel plugins (replaces Engine::run(inputs, KernelFn, CostFn),
+ * engine.hpp:223, and kernel_for, workloads.hpp:203) ---------------------
+ * Registers a user kernel compiled for sm_100a (cubin / fatbin, or
+ * NUL-terminated PTX; image_bytes is informational) under `kernel_id`; its
+ * `entry` follows include/ecl_plugin.h.  From then on ecl_kernel_create
+ * resolves the id (also as a program's kernel and as a per-device kernel)
+ * like a built-in.  Any buffer geometry and out pattern is accepted (the
+ * kernel owns its shapes); local_work_size must be <= 1024, at most
+ * ECL_PLUGIN_MAX_BUFFERS inputs/outputs and ECL_PLUGIN_MAX_ARGS args.
+ * Fails with ECL_CONFIG_ERROR for a built-in or already registered id, and
+ * ECL_UNKNOWN_KERNEL when the image has no such entry (or does not load). */
+int ecl_kernel_register(const char* kernel_id, const void* image, size_t image_bytes, const char* entry);
+/* Removes the id; kernels already created from it stay valid. */
+int ecl_kernel_unregister(const char* kernel_id);
+/* 1 when `kernel_id` names a registered plugin, else 0. */
+int ecl_kernel_is_plugin(const char* kernel_id);
 
 /* ---- buffers --------------------------------------------------------- */
 /* Allocates this device's replica of every input and its output partition

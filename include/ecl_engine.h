@@ -39,6 +39,12 @@ void ecl_engine_destroy(ecl_engine* engine);
  * buffers (ecl_host_register) get per-package async D2H. */
 int ecl_engine_run(ecl_engine* engine, const void* const* inputs, uint32_t n_inputs, void* const* outputs,
                    uint32_t n_outputs);
+/* ecl_engine_run with the device kernel `kernel_id` (a built-in id or one
+ * registered with ecl_kernel_register) in place of the program's kernel for
+ * this run: the reference's Engine::run(inputs, kernel, cost)
+ * (engine.hpp:223) for a caller-supplied kernel. */
+int ecl_engine_run_kernel(ecl_engine* engine, const char* kernel_id, const void* const* inputs, uint32_t n_inputs,
+                          void* const* outputs, uint32_t n_outputs);
 /* Iterative run (e.g. NBody timesteps): `steps` passes; between passes the
  * pairs (swap_in[k], swap_out[k]) are exchanged across devices (each owner
  * GPU's package slices over NVLink) and swapped in place; outputs are

@@ -82,6 +82,10 @@ _sig("ecl_host_unregister", c_int, c_void_p)
 _sig("ecl_host_alloc", c_int, ctypes.c_size_t, ctypes.POINTER(c_void_p))
 _sig("ecl_host_free", c_int, c_void_p)
 _sig("ecl_last_error", c_char_p)
+_sig("ecl_kernel_register", c_int, c_char_p, c_void_p, ctypes.c_size_t, c_char_p)
+_sig("ecl_kernel_unregister", c_int, c_char_p)
+_sig("ecl_kernel_is_plugin", c_int, c_char_p)
+_sig("ecl_engine_run_kernel", c_int, c_void_p, c_char_p, PVOID, c_u32, PVOID, c_u32)
 _sig("ecl_peer_access", c_int, c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int))
 _sig("ecl_probe_host_widen", c_int, c_u64, c_u32, ctypes.POINTER(c_dbl))
 _sig("ecl_probe_vector_peaks", c_int, c_int, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl))

@@ -586,16 +586,20 @@ class Engine:
         return [np.zeros(b.size_bytes(), dtype=np.uint8) for b in self._prog.spec().out_buffers]
 
     def run_into(self, inputs: Sequence, outputs: Optional[Sequence[np.ndarray]],
-                 want_trace: bool = True) -> Optional[ExecutionTrace]:
+                 want_trace: bool = True, kernel: Optional[str] = None) -> Optional[ExecutionTrace]:
         """Caller-owned buffers; outputs=None keeps the results device-resident.
-        want_trace=False skips serializing the trace (last_trace() has it)."""
+        want_trace=False skips serializing the trace (last_trace() has it).
+        kernel: run this device kernel id (built-in or register_kernel'ed)
+        instead of the program's, for this run only."""
         in_ptrs = self._check_inputs(inputs)
         in_arr = N.pointer_array(in_ptrs)
-        if outputs is None:
-            rc = N.lib.ecl_engine_run(self._h, in_arr, len(in_ptrs), None, 0)
+        out_ptrs = self._check_outputs(outputs) if outputs is not None else []
+        out_arr = N.pointer_array(out_ptrs) if outputs is not None else None
+        if kernel is None:
+            rc = N.lib.ecl_engine_run(self._h, in_arr, len(in_ptrs), out_arr, len(out_ptrs))
         else:
-            out_ptrs = self._check_outputs(outputs)
-            rc = N.lib.ecl_engine_run(self._h, in_arr, len(in_ptrs), N.pointer_array(out_ptrs), len(out_ptrs))
+            rc = N.lib.ecl_engine_run_kernel(self._h, kernel.encode(), in_arr, len(in_ptrs), out_arr,
+                                             len(out_ptrs))
         if rc != 0:
             self._fail(rc)
         return self.last_trace() if want_trace else None
@@ -615,8 +619,12 @@ class Engine:
             self._fail(rc)
         return self.last_trace() if want_trace else None
 
-    def run(self, inputs: Sequence = ()) -> RunResult:
+    def run(self, inputs: Sequence = (), kernel: Optional[str] = None, cost=None) -> RunResult:
         """Reference semantics: engine-allocated outputs (engine.hpp:219-256).
+        run(inputs, kernel, cost) is the reference's plugin overload
+        (engine.hpp:223): `kernel` is a device kernel id (built-in or
+        register_kernel'ed) run instead of the program's; `cost` (a per-item
+        function) is the virtual clock's model and unused by a wall run.
         A virtual-clock engine has no outputs to return (kernels never run on
         the CPU here): it raises ConfigError and run_virtual() gives the trace."""
         if self._cfg.clock_mode == ClockMode.Virtual:
@@ -624,10 +632,15 @@ class Engine:
                         "virtual clock mode produces a trace only: call run_virtual(); outputs need a wall-clock "
                         "engine on cuda devices")
         outputs = self.allocate_outputs()
-        trace = self.run_into(inputs, outputs)
+        trace = self.run_into(inputs, outputs, kernel=kernel)
         return RunResult(outputs, trace)
 
-    def run_virtual(self, item_costs: Optional[np.ndarray]) -> ExecutionTrace:
+    def run_virtual(self, item_costs) -> ExecutionTrace:
+        """item_costs: one cost per work-item, a per-item cost function (the
+        reference's CostFn), or None for vecscale/synthetic's analytic costs."""
+        if callable(item_costs):
+            gws = self._prog.global_work_size()
+            item_costs = np.array([item_costs(i) for i in range(gws)], dtype=np.float64)
         if item_costs is None:
             rc = N.lib.ecl_engine_run_virtual(self._h, None, 0)
         else:
@@ -705,6 +718,32 @@ class PinnedBuffer:
 
     def __del__(self):
         self.free()
+
+
+def register_kernel(kernel_id: str, image, entry: str) -> str:
+    """Registers a device kernel compiled for sm_100a (include/ecl_plugin.h
+    ABI) under `kernel_id`: `image` is the cubin / fatbin / PTX bytes or a
+    path to such a file.  Returns the id (usable as a program's kernel, a
+    per-device kernel, or Engine.run(kernel=...))."""
+    if isinstance(image, str) or hasattr(image, "__fspath__"):
+        with open(image, "rb") as f:
+            image = f.read()
+    data = bytes(image) + b"\0"  # PTX is read up to its NUL
+    buf = ctypes.create_string_buffer(data, len(data))
+    rc = N.lib.ecl_kernel_register(kernel_id.encode(), buf, len(data) - 1, entry.encode())
+    if rc != 0:
+        raise Error(ErrorCode[N.code_name(rc)], N.device_last_error())
+    return kernel_id
+
+
+def unregister_kernel(kernel_id: str) -> None:
+    rc = N.lib.ecl_kernel_unregister(kernel_id.encode())
+    if rc != 0:
+        raise Error(ErrorCode[N.code_name(rc)], N.device_last_error())
+
+
+def is_registered_kernel(kernel_id: str) -> bool:
+    return N.lib.ecl_kernel_is_plugin(kernel_id.encode()) == 1
 
 
 def gpu_count() -> int:

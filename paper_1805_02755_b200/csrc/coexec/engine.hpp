@@ -19,7 +19,9 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <memory>
+#include <string>
 #include <span>
 #include <utility>
 #include <vector>
@@ -55,6 +57,22 @@ struct NativeResult {
   double total_ms = 0.0;   // host wall time: first H2D -> last D2H
 };
 
+/// A device kernel by id — the B200 form of the reference's KernelFn
+/// (workloads.hpp:44): a built-in ("vecscale", "mandelbrot@3", ...) or a
+/// kernel registered with register_device_kernel (include/ecl_plugin.h ABI).
+struct DeviceKernel {
+  std::string id;
+};
+
+/// Per-work-item cost for the virtual clock (reference CostFn, workloads.hpp:47).
+using CostFn = std::function<double(std::uint64_t index)>;
+
+/// Registers a device kernel image (cubin / fatbin / NUL-terminated PTX for
+/// sm_100a) whose `entry` follows include/ecl_plugin.h; throws Error.
+DeviceKernel register_device_kernel(const std::string& id, std::span<const std::byte> image, const std::string& entry);
+/// The same from a file (a .cubin / .fatbin / .ptx written by nvcc).
+DeviceKernel register_device_kernel_file(const std::string& id, const std::string& path, const std::string& entry);
+
 struct KernelTiming {
   double kernel_ms = 0.0;  // summed CUDA-event time of every package launch
   std::uint64_t launches = 0;
@@ -70,6 +88,16 @@ class Engine {
   /// Reference semantics (engine.hpp:219-256): engine-allocated outputs.
   RunResult run(std::span<const std::vector<std::byte>> inputs);
 
+  /// The reference's run(inputs, kernel, cost) (engine.hpp:223): this run
+  /// executes `kernel` (same program geometry) on every device instead of the
+  /// program's kernel; `cost` is the virtual clock's model, which a wall run
+  /// does not use (as in drive_wall).  Virtual engines throw ConfigError
+  /// (trace only: run_virtual(cost)).
+  RunResult run(std::span<const std::vector<std::byte>> inputs, const DeviceKernel& kernel, const CostFn& cost);
+  /// run_into with a kernel override (caller-owned buffers).
+  ExecutionTrace run_into(std::span<const void* const> inputs, std::span<void* const> outputs,
+                          const DeviceKernel& kernel);
+
   /// Caller-owned buffers; inputs[i] must hold in_buffers[i].size_bytes()
   /// bytes.  outputs empty (or all null) = device-resident run.
   ExecutionTrace run_into(std::span<const void* const> inputs, std::span<void* const> outputs);
@@ -83,6 +111,8 @@ class Engine {
   /// Virtual clock (simulated devices): per-item costs, one per work-item;
   /// empty = the analytic cost of vecscale/synthetic kernels.
   ExecutionTrace run_virtual(std::span<const double> item_costs);
+  /// The same with a cost function evaluated per work-item.
+  ExecutionTrace run_virtual(const CostFn& cost);
 
   /// Copies the last device-resident run's slices to host buffers.
   void gather(std::span<void* const> outputs);

@@ -560,6 +560,21 @@ int ecl_kernel_create(const char* kernel_id, uint64_t gws, uint64_t lws, const e
 
 void ecl_kernel_destroy(ecl_kernel* k) { delete k; }
 
+int ecl_kernel_register(const char* kernel_id, const void* image, size_t image_bytes, const char* entry) {
+  (void)image_bytes;
+  std::string err;
+  const int rc = ecl::register_plugin(kernel_id ? kernel_id : "", image, entry ? entry : "", &err);
+  return rc == ECL_OK ? rc : fail(rc, err);
+}
+
+int ecl_kernel_unregister(const char* kernel_id) {
+  std::string err;
+  const int rc = ecl::unregister_plugin(kernel_id ? kernel_id : "", &err);
+  return rc == ECL_OK ? rc : fail(rc, err);
+}
+
+int ecl_kernel_is_plugin(const char* kernel_id) { return kernel_id && ecl::find_plugin(kernel_id) ? 1 : 0; }
+
 int ecl_gpu_bind(ecl_gpu* g, const ecl_kernel* k) {
   if (int rc = set_device(g)) return rc;
   if (int rc = sync_all(g)) return rc;

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -16,7 +17,10 @@
 
 namespace ecl {
 
-enum class KernelKind { VecScale, Mandelbrot, MandelbrotF32, Synthetic, Gaussian, NBody, Binomial, Ray, Fault };
+enum class KernelKind { VecScale, Mandelbrot, MandelbrotF32, Synthetic, Gaussian, NBody, Binomial, Ray, Fault, Plugin };
+
+// A user kernel registered with ecl_kernel_register (plugin.cu).
+struct PluginKernel;
 
 enum class SyntheticProfile { Constant = 0, Ramp = 1, Step = 2 };
 
@@ -68,6 +72,7 @@ struct KernelSpec {
   NBodyParams nbody;
   BinomialParams binom;
   RayParams ray;
+  std::shared_ptr<const PluginKernel> plugin;  // KernelKind::Plugin: keeps the loaded image alive
 };
 
 // Everything a launcher needs from the device context.
@@ -120,6 +125,15 @@ cudaError_t launch_gaussian(const KernelSpec& spec, const LaunchEnv& env, uint64
 cudaError_t launch_nbody(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
 cudaError_t launch_binomial(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
 cudaError_t launch_ray(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
+
+// Plugins (plugin.cu): the registered kernel named `id` (null if none), the
+// launch-shape checks, and the launcher (include/ecl_plugin.h ABI).
+std::shared_ptr<const PluginKernel> find_plugin(const std::string& id);
+int register_plugin(const std::string& id, const void* image, const std::string& entry, std::string* err);
+int unregister_plugin(const std::string& id, std::string* err);
+int check_plugin_spec(const KernelSpec& spec, std::string* err);
+cudaError_t launch_plugin(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count);
+bool is_builtin_kernel_id(const std::string& id);
 
 // Test hook (ECL_FAULT_INJECTION=1 only): the work-item `fault_item` executes
 // a trap, so the device faults mid-run (reference test_engine.cpp:236-254).

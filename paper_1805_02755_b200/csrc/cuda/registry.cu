@@ -46,7 +46,22 @@ int bad(std::string* err, const std::string& msg) {
 
 }  // namespace
 
+bool is_builtin_kernel_id(const std::string& full) {
+  const std::string id = full.substr(0, full.find('@'));
+  return id == "vecscale" || id == "mandelbrot" || id == "mandelbrot_f32" || id == "synthetic" ||
+         id.rfind("synthetic:", 0) == 0 || id == "gaussian" || id == "nbody" || id == "binomial" || id == "ray" ||
+         id == "fault";
+}
+
 int resolve_kernel(KernelSpec& s, std::string* err) {
+  // A registered device kernel (ecl_kernel_register): the program's own
+  // kernel, or a per-device binary kernel.
+  if (auto pk = find_plugin(s.id)) {
+    s.kind = KernelKind::Plugin;
+    s.plugin = std::move(pk);
+    s.variant = -1;
+    return check_plugin_spec(s, err);
+  }
   // "<kernel>@<n>": the same kernel's tuning variant n (per-device kernel
   // specialization) — identical results, different code.
   std::string id = s.id;
@@ -203,6 +218,8 @@ int resolve_kernel(KernelSpec& s, std::string* err) {
         return bad(err, "fault expects no inputs and one double output, 1:1");
       if (!arg_u64(s, 0, &s.fault_item, err)) return ECL_BAD_KERNEL_ARGS;
       return ECL_OK;
+    case KernelKind::Plugin:
+      return check_plugin_spec(s, err);
     case KernelKind::Ray: {
       // args [W, H, spheres, max_depth]; in: scene float4 buffer; out: float4 RGBA per pixel.
       uint64_t w, h, ns, depth;
@@ -275,6 +292,7 @@ cudaError_t launch_kernel(const KernelSpec& spec, const LaunchEnv& env, uint64_t
     case KernelKind::Binomial: return launch_binomial(spec, env, first, count);
     case KernelKind::Ray: return launch_ray(spec, env, first, count);
     case KernelKind::Fault: return launch_fault(spec, env, first, count);
+    case KernelKind::Plugin: return launch_plugin(spec, env, first, count);
   }
   return cudaErrorInvalidValue;
 }

@@ -114,6 +114,16 @@ int ecl_engine_run(ecl_engine* e, const void* const* inputs, uint32_t n_in, void
   });
 }
 
+int ecl_engine_run_kernel(ecl_engine* e, const char* kernel_id, const void* const* inputs, uint32_t n_in,
+                          void* const* outputs, uint32_t n_out) {
+  return guarded(e, [&] {
+    if (!kernel_id) throw coexec::Error(coexec::ErrorCode::UnknownKernel, "null kernel id");
+    std::span<const void* const> in(inputs, inputs ? n_in : 0);
+    std::span<void* const> out(outputs, outputs ? n_out : 0);
+    e->engine->run_into(in, out, coexec::DeviceKernel{kernel_id});
+  });
+}
+
 int ecl_engine_run_steps(ecl_engine* e, const void* const* inputs, uint32_t n_in, void* const* outputs,
                          uint32_t n_out, uint32_t steps, const uint32_t* swap_in, const uint32_t* swap_out,
                          uint32_t n_swaps) {

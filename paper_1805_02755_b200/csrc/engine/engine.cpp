@@ -22,6 +22,7 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
@@ -142,12 +143,37 @@ struct Engine::Impl {
 
   void make_kernel() {
     create_kernel(prog.spec().kernel, &kernel);
+    // A per-device kernel is a tuning variant of the program's kernel, or a
+    // registered binary kernel the caller vouches for.
     for (const DeviceProfile& d : cfg.devices)
-      if (!d.kernel.empty() && base_id(d.kernel) != base_id(prog.spec().kernel))
+      if (!d.kernel.empty() && base_id(d.kernel) != base_id(prog.spec().kernel) &&
+          !ecl_kernel_is_plugin(d.kernel.c_str()))
         throw Error(ErrorCode::ConfigError, "device '" + d.id + "': kernel '" + d.kernel +
-                                                "' is not a variant of the program's kernel '" +
-                                                prog.spec().kernel + "'");
+                                                "' is neither a variant of the program's kernel '" +
+                                                prog.spec().kernel + "' nor a registered device kernel");
   }
+
+  // The kernel a device runs by default: its own specialization or the program's.
+  ecl_kernel* default_kernel(std::uint32_t index) {
+    return cfg.devices[index].kernel.empty() ? kernel : kernel_for(cfg.devices[index].kernel);
+  }
+
+  // run(inputs, kernel, cost): every local device runs `id` for one run,
+  // then goes back to its default kernel.  Rebinding keeps the device
+  // buffers (same geometry), so resident inputs stay resident.
+  struct KernelOverride {
+    Impl& impl;
+    bool active = false;
+    KernelOverride(Impl& i, const std::string& id) : impl(i) {
+      ecl_kernel* k = impl.kernel_for(id);
+      active = true;
+      for (auto& d : impl.devices) check(ecl_gpu_bind(d->gpu, k), "bind '" + id + "'");
+    }
+    ~KernelOverride() {
+      if (!active) return;
+      for (auto& d : impl.devices) (void)ecl_gpu_bind(d->gpu, impl.default_kernel(d->index));
+    }
+  };
 
   void create_kernel(const std::string& id, ecl_kernel** out) {
     const ProgramSpec& s = prog.spec();
@@ -194,8 +220,7 @@ struct Engine::Impl {
       check(ecl_gpu_set_copy_split(d->gpu, be.copy_split_items), "copy split");
       check(ecl_gpu_set_widen_fraction(d->gpu, be.widen_per_8), "widen fraction");
       devices.push_back(std::move(d));
-      ecl_kernel* k = cfg.devices[i].kernel.empty() ? kernel : kernel_for(cfg.devices[i].kernel);
-      check(ecl_gpu_bind(devices.back()->gpu, k), "bind '" + cfg.devices[i].id + "'");
+      check(ecl_gpu_bind(devices.back()->gpu, default_kernel(i)), "bind '" + cfg.devices[i].id + "'");
     }
     // One device in this process: stream its inputs up piece by piece so
     // the H2D overlaps the first packages (replication needs them whole).
@@ -788,7 +813,48 @@ ExecutionTrace Engine::run_into(std::span<const void* const> inputs, std::span<v
   return impl_->run_wall(inputs, outputs);
 }
 
+RunResult Engine::run(std::span<const std::vector<std::byte>> inputs, const DeviceKernel& kernel, const CostFn& cost) {
+  (void)cost;  // the virtual clock's model; a wall run times the device kernel itself
+  if (!impl_->wall())
+    throw Error(ErrorCode::ConfigError,
+                "virtual clock mode produces a trace only: call run_virtual(cost); outputs need a wall-clock engine "
+                "on cuda devices");
+  Impl::KernelOverride use(*impl_, kernel.id);
+  return run(inputs);
+}
+
+ExecutionTrace Engine::run_into(std::span<const void* const> inputs, std::span<void* const> outputs,
+                                const DeviceKernel& kernel) {
+  if (!impl_->wall()) throw Error(ErrorCode::ConfigError, "run_into needs clock_mode wall");
+  Impl::KernelOverride use(*impl_, kernel.id);
+  return impl_->run_wall(inputs, outputs);
+}
+
 ExecutionTrace Engine::run_virtual(std::span<const double> item_costs) { return impl_->run_virtual(item_costs); }
+
+ExecutionTrace Engine::run_virtual(const CostFn& cost) {
+  std::vector<double> c(impl_->prog.global_work_size());
+  for (std::uint64_t i = 0; i < c.size(); ++i) c[i] = cost(i);
+  return impl_->run_virtual(c);
+}
+
+DeviceKernel register_device_kernel(const std::string& id, std::span<const std::byte> image, const std::string& entry) {
+  // cudaLibraryLoadData reads PTX up to its NUL: keep one after the bytes
+  std::vector<std::byte> buf(image.begin(), image.end());
+  buf.push_back(std::byte{0});
+  check(ecl_kernel_register(id.c_str(), buf.data(), image.size(), entry.c_str()), "register '" + id + "'");
+  return DeviceKernel{id};
+}
+
+DeviceKernel register_device_kernel_file(const std::string& id, const std::string& path, const std::string& entry) {
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) throw Error(ErrorCode::IoError, "cannot open device kernel image '" + path + "'");
+  std::vector<std::byte> buf;
+  std::byte tmp[65536];
+  for (std::size_t n; (n = std::fread(tmp, 1, sizeof tmp, f)) > 0;) buf.insert(buf.end(), tmp, tmp + n);
+  std::fclose(f);
+  return register_device_kernel(id, buf, entry);
+}
 
 ExecutionTrace Engine::run_steps(std::span<const void* const> inputs, std::span<void* const> outputs,
                                  std::uint32_t steps, std::span<const std::pair<std::uint32_t, std::uint32_t>> swaps) {

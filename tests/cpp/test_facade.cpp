@@ -5,7 +5,7 @@
 //   Listing 2: NBody on three devices, Static({0.08, 0.3}).
 //   Mandelbrot co-executed with HGuided, bit-exact with the reference kernel.
 //
-// Usage: test_facade [--no-gpu]   (exit 0 = all checks passed)
+// Usage: test_facade [--no-gpu | --plugin <plugins.cubin>]   (exit 0 = all checks passed)
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -140,6 +140,47 @@ static void mandelbrot_hguided(int ng) {
   CHECK(coexec::tiles_exactly(engine.trace().packages, w * h / 256), "mandelbrot: tiling");
 }
 
+// The reference's plugin overload Engine::run(inputs, kernel, cost)
+// (engine.hpp:223) with a user kernel compiled out of tree
+// (tests/plugins/plugins.cu -> _build/plugins.cubin, include/ecl_plugin.h).
+static void plugin_kernel_run(int ng, const char* cubin) {
+  const std::uint64_t n = 1 << 16;
+  coexec::ProgramSpec spec;
+  spec.global_work_size = n;
+  spec.local_work_size = 128;
+  spec.in_buffers.push_back({"x", 8, n, coexec::BufferRole::Input});
+  spec.out_buffers.push_back({"y", 8, n, coexec::BufferRole::Output});
+  spec.kernel = "vecscale";
+  spec.args = {2.5, -1.0};
+  coexec::EngineConfig cfg;
+  for (int i = 0; i < 2; ++i) {
+    coexec::DeviceProfile d;
+    d.id = "gpu" + std::to_string(i);
+    d.name = d.id;
+    d.backend.kind = coexec::BackendKind::Cuda;
+    d.backend.ordinal = i % ng;
+    cfg.devices.push_back(d);
+  }
+  cfg.scheduler = coexec::DynamicConfig{8};
+  std::vector<std::vector<std::byte>> inputs(1, std::vector<std::byte>(n * 8));
+  auto* x = reinterpret_cast<double*>(inputs[0].data());
+  for (std::uint64_t i = 0; i < n; ++i) x[i] = static_cast<double>(i) * 0.25 - 100.0;
+  try {
+    const coexec::DeviceKernel k = coexec::register_device_kernel_file("cpp_vecscale", cubin, "vecscale_plugin");
+    coexec::Engine engine(cfg, coexec::validate_program(spec));
+    const coexec::CostFn cost = [](std::uint64_t) { return 1.0; };
+    const coexec::RunResult r = engine.run(inputs, k, cost);
+    const auto* y = reinterpret_cast<const double*>(r.outputs[0].data());
+    std::uint64_t bad = 0;
+    for (std::uint64_t i = 0; i < n; ++i) bad += y[i] != 2.5 * x[i] + -1.0;
+    CHECK(bad == 0, "plugin vecscale: %llu wrong items", static_cast<unsigned long long>(bad));
+    CHECK(coexec::tiles_exactly(r.trace.packages, n / 128), "plugin vecscale: tiling");
+    ecl_kernel_unregister("cpp_vecscale");
+  } catch (const std::exception& e) {
+    CHECK(false, "plugin run threw: %s", e.what());
+  }
+}
+
 static void errors_are_collected() {
   std::vector<double> out(1024);
   ecl::EngineCL engine;
@@ -170,6 +211,7 @@ int main(int argc, char** argv) {
     listing1_binomial(ng);
     listing2_nbody(ng);
     mandelbrot_hguided(ng);
+    if (argc > 2 && std::strcmp(argv[1], "--plugin") == 0) plugin_kernel_run(ng, argv[2]);
   }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;

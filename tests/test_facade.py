@@ -32,3 +32,13 @@ def test_facade_compiles_and_reports_errors_without_running_kernels():
 @pytest.mark.gpu
 def test_facade_listings_match_oracle(gpu_available):
     run()
+
+
+@pytest.mark.gpu
+def test_cpp_engine_run_with_a_plugin_kernel(gpu_available):
+    """coexec::Engine::run(inputs, DeviceKernel, CostFn) from C++ with a cubin
+    registered by coexec::register_device_kernel_file."""
+    plug = os.path.join(ROOT, "tests", "plugins")
+    r = subprocess.run(["make", "-s", "-C", plug], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    run("--plugin", os.path.join(plug, "_build", "plugins.cubin"))
