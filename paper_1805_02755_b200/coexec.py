@@ -673,6 +673,15 @@ class Engine:
         _check(N.lib.ecl_engine_kernel_time(self._h, ctypes.byref(ms), ctypes.byref(n), 1 if reset else 0))
         return ms.value, n.value
 
+    def learned_powers(self) -> List[float]:
+        """Adaptive HGuided: work-items/ms per device measured by the last run
+        (the next run's seeds); [] before a run measured every device."""
+        cap = len(self._cfg.devices)
+        buf = (ctypes.c_double * max(1, cap))()
+        n = ctypes.c_uint32(0)
+        _check(N.lib.ecl_engine_learned_powers(self._h, buf, cap, ctypes.byref(n)))
+        return [buf[i] for i in range(min(n.value, cap))]
+
     def last_trace(self) -> ExecutionTrace:
         s = N.read_string(N.lib.ecl_engine_trace_json, self._h)
         if isinstance(s, int):

@@ -122,6 +122,9 @@ class Engine {
   NativeResult native_run(std::span<const void* const> inputs, std::span<void* const> outputs);
 
   KernelTiming kernel_timing(bool reset);
+  /// Adaptive HGuided: the per-device work-items/ms the last run measured,
+  /// which seed the next run (empty before a run measured every device).
+  std::vector<double> learned_powers() const;
   const ExecutionTrace& last_trace() const;
   double init_ms() const;
   const ValidatedProgram& program() const;

@@ -52,6 +52,9 @@ class SharedCoordinator {
   std::vector<Package> end_run(bool* peer_failed);
   void barrier();
 
+  /// The run's adaptive-HGuided powers (identical on every rank: end_run
+  /// replays the whole decision log first); empty if not learned.
+  std::vector<double> learned_powers() const { return sched_ ? sched_->learned_powers() : std::vector<double>{}; }
   const SharedConfig& config() const { return cfg_; }
   std::uint64_t remaining() const;
 

@@ -124,6 +124,13 @@ int ecl_engine_run_kernel(ecl_engine* e, const char* kernel_id, const void* cons
   });
 }
 
+int ecl_engine_learned_powers(const ecl_engine* e, double* powers, uint32_t cap, uint32_t* n) {
+  const std::vector<double> p = e->engine->learned_powers();
+  *n = static_cast<uint32_t>(p.size());
+  for (uint32_t i = 0; i < p.size() && i < cap; ++i) powers[i] = p[i];
+  return ECL_OK;
+}
+
 int ecl_engine_run_steps(ecl_engine* e, const void* const* inputs, uint32_t n_in, void* const* outputs,
                          uint32_t n_out, uint32_t steps, const uint32_t* swap_in, const uint32_t* swap_out,
                          uint32_t n_swaps) {

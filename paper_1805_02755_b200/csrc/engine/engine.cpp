@@ -97,6 +97,9 @@ struct Engine::Impl {
   std::vector<Package> last_packages;  // packages of the last wall run (for gather)
   bool last_resident = false;
   bool inputs_resident = false;  // the devices hold replicas of every input
+  // Adaptive HGuided: per-device work-items/ms learned by the previous run,
+  // the next run's seed powers (empty until a run measured every device).
+  std::vector<double> learned;
 
   // device-thread run protocol
   std::mutex run_m;
@@ -292,6 +295,12 @@ struct Engine::Impl {
     const double epoch_abs = steady_ms(epoch);
     std::deque<Package> inflight;
     bool drained = false;
+    // Throughput observations use non-overlapping busy time: packages on the
+    // two lanes overlap, so a package counts from max(its start, the latest
+    // end seen on this device); items of a package hidden entirely under an
+    // earlier one carry into the next observation.
+    double busy_end = -1e300;
+    std::uint64_t carry_items = 0;
     void* const* host_out = rs.host_out.empty() ? nullptr : rs.host_out.data();
 
     auto pull = [&]() -> bool {
@@ -347,13 +356,18 @@ struct Engine::Impl {
       }
       pkg.t_start_ms = t0 - epoch_abs;  // device times come on the absolute steady clock
       pkg.t_end_ms = t1 - epoch_abs;
+      const double busy = t1 - std::max(t0, busy_end);
+      busy_end = std::max(busy_end, t1);
+      carry_items += pkg.size_wg * prog.local_work_size();
+      const bool report = busy > 1e-6;
       if (rs.shared) {
-        rs.shared->observe(dev.index, pkg.size_wg * prog.local_work_size(), t1 - t0);
+        if (report) rs.shared->observe(dev.index, carry_items, busy);
         rs.shared->complete(pkg);
-      } else {
+      } else if (report) {
         std::lock_guard lock(rs.coordinator);
-        rs.scheduler->observe(dev.index, pkg.size_wg * prog.local_work_size(), t1 - t0);
+        rs.scheduler->observe(dev.index, carry_items, busy);
       }
+      if (report) carry_items = 0;
       std::lock_guard lock(rs.completion);
       rs.completed.push_back(std::move(pkg));
     }
@@ -447,14 +461,18 @@ struct Engine::Impl {
   std::vector<Package> co_execute(std::span<void* const> host_out, std::uint64_t first_seq, bool tally) {
     RunState rs;
     std::unique_ptr<Scheduler> scheduler;
+    // Adaptive HGuided starts from the rates the previous run measured.
+    SchedulerConfig sc = cfg.scheduler;
+    if (auto* h = std::get_if<HGuidedConfig>(&sc); h && h->adaptive && learned.size() == cfg.devices.size())
+      h->powers = learned;
     if (shared) {
       // Collective with the peer processes: the run's epoch is shared so all
       // ranks' timestamps share one (CLOCK_MONOTONIC) timeline.
-      const double ep = shared->begin_run(cfg.scheduler, prog.total_work_groups(), cfg.devices);
+      const double ep = shared->begin_run(sc, prog.total_work_groups(), cfg.devices);
       epoch = Clock::time_point(std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double, std::milli>(ep)));
       rs.shared = shared.get();
     } else {
-      scheduler = make_scheduler(cfg.scheduler, prog.total_work_groups(), cfg.devices);
+      scheduler = make_scheduler(sc, prog.total_work_groups(), cfg.devices);
       rs.scheduler = scheduler.get();
     }
     rs.next_seq = first_seq;
@@ -485,6 +503,8 @@ struct Engine::Impl {
     } else {
       all = std::move(rs.completed);
     }
+    if (auto lp = shared ? shared->learned_powers() : scheduler->learned_powers(); !lp.empty() && errors.empty())
+      learned = std::move(lp);
     std::sort(all.begin(), all.end(), [](const Package& a, const Package& b) { return a.seq < b.seq; });
     if (errors.empty()) {
       if (!tiles_exactly(all, prog.total_work_groups()))
@@ -678,6 +698,9 @@ struct Engine::Impl {
       clock = e.t;
       Package p = std::move(inflight[e.dev]);
       p.t_end_ms = e.t;
+      // measured-throughput HGuided sees the simulated busy time (a no-op
+      // for the reference's schedulers, which ignore observations)
+      scheduler->observe(e.dev, p.size_wg * lws, p.t_end_ms - p.t_start_ms);
       completed.push_back(std::move(p));
       request(e.dev);
     }
@@ -880,6 +903,7 @@ KernelTiming Engine::kernel_timing(bool reset) {
   return t;
 }
 
+std::vector<double> Engine::learned_powers() const { return impl_->learned; }
 const ExecutionTrace& Engine::last_trace() const { return impl_->last; }
 double Engine::init_ms() const { return impl_->init_ms; }
 const ValidatedProgram& Engine::program() const { return impl_->prog; }

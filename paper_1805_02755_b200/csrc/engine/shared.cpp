@@ -215,6 +215,7 @@ std::vector<Package> SharedCoordinator::end_run(bool* peer_failed) {
   barrier();  // every rank has completed its packages
   std::vector<Package> out;
   Lock lock(&region_->mu);
+  replay();  // every rank's scheduler ends in the same state (learned powers)
   *peer_failed = region_->failed != 0;
   for (std::uint64_t i = 0; i < region_->n_done; ++i) {
     const DoneRec& r = region_->done[i];

@@ -357,3 +357,28 @@ def test_periodic_exit_near_parabolic_points(gpu_available, oracle, center):
     spec = W.mandelbrot_spec(w, h, 50000, viewport=vp, lws=64, kernel="mandelbrot@14")
     _, res = run_engine(spec, P.DynamicConfig(5), n_dev=1)
     assert np.array_equal(res.outputs[0].view(np.uint32), expand_4to1(oracle.mandelbrot(w, h, 50000, viewport=vp)))
+
+
+def test_adaptive_hguided_learns_and_carries_powers(gpu_available, oracle):
+    """Measured-throughput HGuided: a run measures every device's
+    work-items/ms over non-overlapping busy time; the next run starts from
+    those rates.  Device 0 runs the periodic-orbit variant (mandelbrot@14,
+    same counts, fewer iterations) so the two logical devices differ."""
+    w, it = 2048, 2048
+    spec = W.mandelbrot_spec(w, w, it)
+    prog = P.validate_program(spec)
+    devs = devices(2)
+    devs[0].kernel = "mandelbrot@14"
+    exp = expand_4to1(oracle.mandelbrot(w, w, it))
+    with P.Engine(P.EngineConfig(devs, P.HGuidedConfig(adaptive=True)), prog) as e:
+        assert e.learned_powers() == []
+        first = e.run([])
+        lp = e.learned_powers()
+        assert len(lp) == 2 and all(p > 1e3 for p in lp), lp  # work-items/ms, not the unit seeds
+        second = e.run([])
+        lp2 = e.learned_powers()
+    print("learned powers", lp, lp2)
+    for r in (first, second):
+        assert np.array_equal(r.outputs[0].view(np.uint32), exp)
+        assert P.tiles_exactly(r.trace.packages, prog.total_work_groups())
+    assert lp2[0] > lp2[1]  # the variant that skips periodic orbits is faster

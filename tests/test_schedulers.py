@@ -268,3 +268,30 @@ def test_drains_against_live_reference(ref):
         for cfg in (P.StaticConfig(), P.DynamicConfig(n + rng.randrange(500)), P.HGuidedConfig(0.5 + rng.random() * 3)):
             exp = ref.drain(cfg.to_json(), [x.to_json() for x in d], total)
             assert drain(P.Scheduler(cfg, total, d), n) == exp
+
+
+def test_hguided_adaptive_first_report_keeps_units_consistent():
+    """Seeds are relative (computing_power = 1.0) and a report is in
+    work-items/ms (~7e6 for a B200 on Mandelbrot): until every device has
+    reported, the unmeasured devices' seeds are scaled by the measured
+    rate/seed ratio, so one early report cannot take ~all of sum(P)."""
+    n, total = 8, 1 << 20
+    s = P.Scheduler(P.HGuidedConfig(2.0, adaptive=True, ema_alpha=0.5), total, devs(*[1.0] * n))
+    before = [s.unclamped_size(total, i) for i in range(n)]
+    s.observe(0, 1_000_000, 0.14)  # ~7.1e6 items/ms
+    after = [s.unclamped_size(total, i) for i in range(n)]
+    assert after == before  # equal devices, equal shares, whatever the unit
+    s.observe(1, 1_000_000, 0.28)  # device 1 measured at half the rate
+    sizes = [s.unclamped_size(total, i) for i in range(n)]
+    assert sizes[0] == pytest.approx(2 * sizes[1], rel=1e-6)
+    # devices 2..7 are seeded at the measured mean rate/seed
+    assert all(x == sizes[2] for x in sizes[2:]) and sizes[1] < sizes[2] < sizes[0]
+
+
+def test_hguided_adaptive_seed_powers_in_rates_are_unchanged_by_scaling():
+    # seeds already in items/ms (e.g. learned by a previous run): scaling by
+    # the measured rate/seed ratio leaves them as they are
+    d = devs(4000.0, 2000.0)
+    s = P.Scheduler(P.HGuidedConfig(2.0, adaptive=True, ema_alpha=1.0), 100000, d)
+    s.observe(0, 4000, 1.0)
+    assert s.unclamped_size(100000, 1) == 100000 * 2000 // (2 * 6000 * 2)

@@ -119,3 +119,21 @@ def test_virtual_runs_are_deterministic(oracle):
     costs = oracle.mandelbrot(64, 64, 100).astype(np.float64)
     e = P.Engine(P.EngineConfig(devs, P.HGuidedConfig(), P.ClockMode.Virtual, 5), prog)
     assert e.run_virtual(costs).raw == e.run_virtual(costs).raw
+
+
+def test_virtual_adaptive_hguided_recovers_from_wrong_seeds():
+    """Seeds claim four equal devices; one is 8x faster and every package
+    costs 0.5 ms of launch overhead.  HGuided balances either way (it is
+    self-scheduling), but measured-throughput HGuided sizes packages from the
+    learned rates: fewer packages, less overhead, closer to the ideal."""
+    devs = [P.simulated_device("fast", 8.0, 0.5, 1e30)] + \
+        [P.simulated_device(f"slow{i}", 1.0, 0.5, 1e30) for i in range(3)]
+    prog = P.validate_program(W.synthetic_spec(400000, 100))
+    t = {}
+    for adaptive in (False, True):
+        cfg = P.HGuidedConfig(2.0, [1.0] * 4, adaptive=adaptive, ema_alpha=0.5)
+        t[adaptive] = P.Engine(P.EngineConfig(devs, cfg, P.ClockMode.Virtual), prog).run_virtual(None)
+        assert P.tiles_exactly(t[adaptive].packages, prog.total_work_groups())
+    assert t[True].t_total_ms < t[False].t_total_ms
+    assert len(t[True].packages) < len(t[False].packages)
+    assert t[True].t_total_ms < 1.002 * 400000 / 11.0  # ideal: 11 work-items/ms in total
