@@ -295,3 +295,19 @@ def test_hguided_adaptive_seed_powers_in_rates_are_unchanged_by_scaling():
     s = P.Scheduler(P.HGuidedConfig(2.0, adaptive=True, ema_alpha=1.0), 100000, d)
     s.observe(0, 4000, 1.0)
     assert s.unclamped_size(100000, 1) == 100000 * 2000 // (2 * 6000 * 2)
+
+
+def test_hguided_adaptive_weighs_reports_by_busy_time():
+    """The guided tail's tiny packages (busy time mostly launch latency) must
+    not outvote the large packages: forgetting is by busy time."""
+    s = P.Scheduler(P.HGuidedConfig(2.0, adaptive=True, ema_alpha=0.5), 1 << 20, devs(1.0, 1.0))
+    s.observe(0, 1_000_000, 100.0)  # 1e4 items/ms
+    s.observe(1, 1_000_000, 100.0)
+    for _ in range(20):
+        s.observe(0, 256, 0.01)  # 2.56e4 items/ms each, 0.2 ms in total
+    a, b = s.unclamped_size(1 << 20, 0), s.unclamped_size(1 << 20, 1)
+    assert abs(a / b - 1.0) < 0.01
+    # a report as long as the history halves it (alpha 0.5): the rate becomes
+    # the busy-weighted mean (50 ms at 1e4, 100 ms at 2e4) = 1.667e4
+    s.observe(0, 2_000_000, 100.0)
+    assert s.unclamped_size(1 << 20, 0) / s.unclamped_size(1 << 20, 1) == pytest.approx(5 / 3, rel=0.01)
