@@ -6,16 +6,23 @@
 // float4 (four options) per work-group, out pattern 1:lws.  A package of
 // work-groups [o, o+n) is options [4o, 4(o+n)).
 //
-// Mapping: one warp per option pair.  Lane l holds lattice nodes
-// t = 8l .. 8l+7 in registers (255 nodes for 254 steps); a backward step
-//   c[t] <- puByr * c[t+1] + pdByr * c[t]      (t < j)
-// is 8 register FMAs per lane (scaled form, below) plus one warp shuffle for the neighbour
-// node c[8l+8] held by lane l+1 — the OpenCL kernel's local-memory lattice
-// and barriers become registers and __shfl_down_sync.  The two options of a
-// warp travel packed in float2 registers through FFMA2/FADD2 (half the
-// issue slots of the scalar lattice, same per-component rounding).  Per-option
-// parameters (dt, u, d, pu/a, pd/a) are formed in FP64 so the subtraction
-// a - d does not lose the 1e-5 relative budget; the lattice itself is FP32.
+// Mapping (default kernel, binomial_hw): one warp per four options, one
+// half-warp per option pair.  The two options of a pair travel packed in
+// float2 registers through FFMA2 (half the issue slots of the scalar
+// lattice, same per-component rounding).  Nodes below the strike are exactly
+// zero and stay zero until the level where their whole subtree has been
+// reached, so a pair's live lattice is a window of W = steps - tw + 1 nodes
+// (tw = the lowest first-positive leaf of the four options) that slides down
+// one node per level, then shrinks by one node per level; at the config W is
+// ~116 of 255 nodes and fits 16 lanes x 8 nodes in registers.  A backward
+// step is 8 register FMAs per lane (scaled form, below) plus one warp
+// shuffle per packed component that serves both pairs of the warp — the
+// OpenCL kernel's local-memory lattice and barriers become registers and
+// shuffles.  Per-option parameters (dt, u, d, pu/a, pd/a) are formed in FP64
+// so the subtraction a - d does not lose the 1e-5 relative budget; the
+// lattice itself is FP32.  Every variant (binomial@1..4) computes the same
+// node values with the same FMAs, so all prices are bit-identical to the
+// scalar full lattice (binomial@1).
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -58,9 +65,9 @@ __device__ __forceinline__ float2 shfl_from(float2 v, unsigned src) {
 // holds nodes NL*l .. NL*l+NL-1): w[t] <- w[t] + r*w[t+1].  The neighbour of
 // a lane's last node is the next lane's first (one shuffle).  Returns the
 // next j.
-template <int G, int NL, typename V>
+template <int G, int NL, typename V, int U = 8>
 __device__ __forceinline__ int backward(V (&c)[NL], int j, int stop, V r) {
-#pragma unroll 8
+#pragma unroll U
   for (; j > stop; --j) {
     const V right = shfl_down1<G>(c[0]);
 #pragma unroll
@@ -78,12 +85,14 @@ __device__ __forceinline__ int backward(V (&c)[NL], int j, int stop, V r) {
 // shared-memory buffer.  Phases above ceil((steps+1)/G) run no steps and
 // neither rescale nor repack anything that matters.  Slots beyond the live
 // nodes carry don't-care values.  `lane` is the lane within its group.
-template <int G, int NL, typename V>
+// RS: the rescale period in levels (a multiple of G): the lattice is rescaled
+// by s = pd^RS at the phase boundaries that are multiples of RS.
+template <int G, int NL, typename V, int RS = G, int U = 8>
 __device__ __forceinline__ V phases(V (&c)[NL], int j, V r, V s, V* buf, unsigned lane) {
   const int stop = NL > 1 ? G * (NL - 1) - 1 : 0;
   if (j > stop) {
-    j = backward<G, NL>(c, j, stop, r);
-    if constexpr (NL > 1) {
+    j = backward<G, NL, V, U>(c, j, stop, r);
+    if constexpr (NL > 1 && (G * (NL - 1)) % RS == 0) {
 #pragma unroll
       for (int k = 0; k < NL; ++k) c[k] = rescale(c[k], s);
     }
@@ -98,7 +107,7 @@ __device__ __forceinline__ V phases(V (&c)[NL], int j, V r, V s, V* buf, unsigne
 #pragma unroll
     for (int k = 0; k < NL - 1; ++k) h[k] = buf[(NL - 1) * lane + k];
     __syncwarp();
-    return phases<G, NL - 1>(h, j, r, s, buf, lane);
+    return phases<G, NL - 1, V, RS, U>(h, j, r, s, buf, lane);
   }
 }
 
@@ -117,6 +126,7 @@ struct Option {
   double K, base, f, u2;  // leaf of node t = NL l + k: base * f^l * u2^k - K  (f = u^(2 NL))
   float r, s;             // pu/pd and pd^G (the scaled lattice's step and rescale factors)
   double tail;            // pd^(steps - G R) * exp(-R T) / q^R: undoes the remaining scale, discounts
+  int t0;                 // every leaf below node t0 is exactly zero (conservative by 2 nodes)
 };
 
 // G = lane-group width (phase length in levels), NL = nodes per lane at the leaves.
@@ -144,6 +154,10 @@ __device__ __forceinline__ Option option_params(double rv, int steps) {
   o.base = S * exp(-vsdt * static_cast<double>(steps));
   o.u2 = u * u;
   o.f = upow(o.u2, NL);
+  // leaf(t) = S u^(2t - steps) - K > 0  <=>  t > (steps + ln(K/S)/vsdt) / 2
+  const double x = 0.5 * (steps + log(o.K / S) / vsdt);
+  const double t0 = floor(x) - 1.0;
+  o.t0 = t0 <= 0.0 ? 0 : (t0 >= steps ? steps : static_cast<int>(t0));
   return o;
 }
 
@@ -189,8 +203,92 @@ __device__ __forceinline__ V lattice(V (&c)[kNodesPerLane], int steps, V r, V s3
   return phases<32, kNodesPerLane>(c, steps, r, s32, buf, lane);
 }
 
-// P = options per warp (1: scalar lattice, 2: two options packed per lane).
-template <int P, int MB>
+// ---- Zero window -----------------------------------------------------------
+// Leaves below the strike are exactly 0, and node t of level j is a
+// combination of leaves t .. t + (steps - j) only, so at level j every node
+// below b_j = max(0, tw - (steps - j)) is exactly 0 (tw <= the first
+// positive leaf of both options of the pair).  While b_j > 0 the warp keeps
+// only nodes b_j .. j: a window of constant width W = steps - tw + 1 whose
+// base moves down one node per level.  In window slots (slot s = node
+// b_j + s) a backward step reads the slot below:
+//   w'[s] = w[s-1] + (pu/pd) w[s]          (w[-1] = node b_j - 1 = 0)
+// — the same FMA on the same operands as the full lattice, so every price is
+// bit-identical to it; exact zeros are skipped, not approximated.  After tw
+// levels the base reaches node 0 with W live nodes in NL = ceil(W/32) nodes
+// per lane, which is exactly the layout phases<32, NL> continues from.  At
+// the config (rv ~ U[0,1)) tw ~ 139 of 254, W ~ 116: NL = 4 instead of 8
+// for half the levels, ~27 % fewer FFMA2s and shuffles.
+// Previous lane's value within lane groups of G.
+template <int G>
+__device__ __forceinline__ float shfl_up1(float v) {
+  return __shfl_up_sync(0xffffffffu, v, 1, G);
+}
+template <int G>
+__device__ __forceinline__ float2 shfl_up1(float2 v) {
+  return make_float2(__shfl_up_sync(0xffffffffu, v.x, 1, G), __shfl_up_sync(0xffffffffu, v.y, 1, G));
+}
+
+// Window steps from level j down to jend in lane groups of G (`lane` = lane
+// within the group), rescaling at the levels 32m - 1 as phases() does.
+// Returns jend.
+template <int G, int NL, typename V, int U = 8>
+__device__ __forceinline__ int window_steps(V (&c)[NL], int j, int jend, V r, V s, unsigned lane) {
+  while (j > jend) {
+    const int nb = (j >> 5) * 32 - 1;  // next rescale level below j (-1: none)
+    const int stop = nb > jend ? nb : jend;
+#pragma unroll U
+    for (; j > stop; --j) {
+      V left = shfl_up1<G>(c[NL - 1]);
+      if (lane == 0) left = V{};  // node b_j - 1 is zero
+#pragma unroll
+      for (int k = NL - 1; k > 0; --k) c[k] = lattice_step(c[k - 1], c[k], r);
+      c[0] = lattice_step(left, c[0], r);
+    }
+    if (j == nb) {
+#pragma unroll
+      for (int k = 0; k < NL; ++k) c[k] = rescale(c[k], s);
+    }
+  }
+  return j;
+}
+
+// Leaves (8 per lane, full layout, in buf) -> window slots tw + NL*lane + k,
+// window steps, then the shrinking phases from NL nodes per lane.
+template <int NL, typename V>
+__device__ __forceinline__ V from_window(int steps, int tw, V r, V s, V* buf, unsigned lane) {
+  V h[NL];
+#pragma unroll
+  for (int k = 0; k < NL; ++k) {
+    const int i = tw + NL * static_cast<int>(lane) + k;
+    h[k] = i < 32 * kNodesPerLane ? buf[i] : V{};
+  }
+  __syncwarp();  // phases() reuses buf
+  const int j = window_steps<32, NL>(h, steps, steps - tw, r, s, lane);
+  return phases<32, NL>(h, j, r, s, buf, lane);
+}
+
+template <typename V>
+__device__ __forceinline__ V lattice_window(V (&c)[kNodesPerLane], int steps, int tw, V r, V s, V* buf,
+                                            unsigned lane) {
+  if (tw <= 0) return lattice(c, steps, r, s, buf, lane);
+#pragma unroll
+  for (int k = 0; k < kNodesPerLane; ++k) buf[kNodesPerLane * lane + k] = c[k];
+  __syncwarp();
+  switch ((steps - tw + 32) >> 5) {  // ceil(W / 32), W = steps - tw + 1
+    case 1: return from_window<1>(steps, tw, r, s, buf, lane);
+    case 2: return from_window<2>(steps, tw, r, s, buf, lane);
+    case 3: return from_window<3>(steps, tw, r, s, buf, lane);
+    case 4: return from_window<4>(steps, tw, r, s, buf, lane);
+    case 5: return from_window<5>(steps, tw, r, s, buf, lane);
+    case 6: return from_window<6>(steps, tw, r, s, buf, lane);
+    case 7: return from_window<7>(steps, tw, r, s, buf, lane);
+    default: return from_window<8>(steps, tw, r, s, buf, lane);
+  }
+}
+
+// P = options per warp (1: scalar lattice, 2: two options packed per lane);
+// Window: skip the exact-zero nodes below the strike (lattice_window).
+template <int P, int MB, bool Window = true>
 __global__ void __launch_bounds__(kThreads, MB)
     binomial_warp(const float* __restrict__ rand, float* __restrict__ out, int steps, uint64_t first_opt,
                   uint64_t n_opt) {
@@ -236,13 +334,136 @@ __global__ void __launch_bounds__(kThreads, MB)
         s32.y = b.s;
         tail_b = b.tail;
       }
-      const float2 v = lattice(c, steps, r, s32, buf, lane);
+      const int tw = min(__shfl_sync(0xffffffffu, mine.t0, 0), __shfl_sync(0xffffffffu, mine.t0, 16));
+      const float2 v = Window ? lattice_window(c, steps, tw, r, s32, buf, lane) : lattice(c, steps, r, s32, buf, lane);
       if (lane == 0) {
         out[o] = static_cast<float>(static_cast<double>(v.x) * tail_a);
         if (has_b) out[o + 1] = static_cast<float>(static_cast<double>(v.y) * tail_b);
       }
     }
   }
+}
+
+// ---- Default kernel: half-warp lattices with the zero window -------------
+// The lattice's cost is per level, not per node: every level needs the
+// neighbour exchange (one SHFL per packed component), and the exchange, not
+// the FFMA2 count, paces the warp (skipping a quarter of the FFMA2s with the
+// zero window alone left the time unchanged; ncu: SHFLs and their selects,
+// branches and scoreboard waits stayed per level).  The zero window makes a
+// pair's live lattice W = steps - tw + 1 <= 128 nodes at the config, which
+// fits 16 lanes x 8 nodes, so each half-warp runs one option pair: one warp
+// SHFL serves two pairs and the per-level overhead halves, with the
+// registers of the 8-node warp lattice.  Phases are 16 levels (repack to
+// NL-1 nodes per lane every 16 levels, less dead work than 32) while the
+// rescale stays at the levels 32m - 1 by pd^32, so the prices are
+// bit-identical to the full scalar lattice.  Warps whose four options need
+// W > 128 (deep in the money) run their two pairs one after the other as
+// 32-lane window lattices instead.
+// One code path for every window width (W <= 128): the window steps run at
+// 8 nodes per lane whatever W is.  Width-specialised entries (NL = ceil(W/16)
+// per pair) cut FFMA2s further but multiplied the kernel's code eightfold:
+// ncu's top stall became "no instruction" (instruction-cache misses) and the
+// kernel got slower.
+template <int U>
+__device__ __forceinline__ float2 half_lattice(int steps, int tw, float2 r, float2 s, float2* buf, unsigned lh) {
+  float2 h[kNodesPerLane];
+#pragma unroll
+  for (int k = 0; k < kNodesPerLane; ++k) {
+    const int i = tw + kNodesPerLane * static_cast<int>(lh) + k;
+    h[k] = i < 32 * kNodesPerLane ? buf[i] : float2{};
+  }
+  __syncwarp();  // phases() reuses buf
+  const int j = window_steps<16, kNodesPerLane, float2, U>(h, steps, steps - tw, r, s, lh);
+  return phases<16, kNodesPerLane, float2, 32, U>(h, j, r, s, buf, lh);
+}
+
+// Deep in-the-money groups (W > 128): each pair on the whole warp, full
+// 32-lane lattice (rare).
+template <int U>
+__device__ __forceinline__ float2 warp_lattice(const float2* leaves_buf, int steps, float2 r, float2 s, float2* buf,
+                                            unsigned lane) {
+  float2 c[kNodesPerLane];
+#pragma unroll
+  for (int k = 0; k < kNodesPerLane; ++k) c[k] = leaves_buf[kNodesPerLane * lane + k];
+  __syncwarp();
+  return phases<32, kNodesPerLane, float2, 32, U>(c, steps, r, s, buf, lane);
+}
+
+// U: unroll of the level loops (code size: the kernel is instruction-fetch
+// sensitive, see half_lattice).
+template <int MB, int U>
+__global__ void __launch_bounds__(kThreads, MB)
+    binomial_hw(const float* __restrict__ rand, float* __restrict__ out, int steps, uint64_t first_opt,
+                uint64_t n_opt) {
+  // per warp: the leaves of its two pairs (full 32 x 8 layout), then each
+  // pair's window / repack buffer
+  __shared__ float2 pair_buf[kThreads / 32][2][32 * kNodesPerLane];
+  __shared__ double tail_buf[kThreads / 32][4];
+  const unsigned lane = threadIdx.x & 31u, half = lane >> 4, lh = lane & 15u;
+  float2 (*const bufs)[32 * kNodesPerLane] = pair_buf[threadIdx.x >> 5];
+  double* const tails = tail_buf[threadIdx.x >> 5];
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (kThreads / 32);
+  const uint64_t groups = (n_opt + 3) / 4;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(kThreads / 32) + (threadIdx.x >> 5); w < groups;
+       w += warps) {
+    const uint64_t o = first_opt + w * 4;
+    const uint64_t left = first_opt + n_opt - o;  // options of this group that exist (>= 1)
+    // Lanes 8q..8q+7 set up option o+q (missing options repeat option o).
+    const unsigned q = lane >> 3;
+    const Option mine = option_params<32, kNodesPerLane>(rand[o + (q < left ? q : 0)], steps);
+    const int tw = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(mine.t0)));
+    // Only the lattice's inputs stay in registers across it: the tails wait
+    // in shared memory, each pair's (pu/pd, pd^32) is re-read from its lanes.
+    if ((lane & 7u) == 0) tails[q] = mine.tail;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const Option a = shfl_option(mine, 16 * p), b = shfl_option(mine, 16 * p + 8);
+      float ca[kNodesPerLane], cb[kNodesPerLane];
+      leaves<kNodesPerLane>(a, steps, lane, ca);
+      leaves<kNodesPerLane>(b, steps, lane, cb);
+#pragma unroll
+      for (int k = 0; k < kNodesPerLane; ++k) bufs[p][kNodesPerLane * lane + k] = make_float2(ca[k], cb[k]);
+    }
+    const float mr = mine.r, ms = mine.s;
+    __syncwarp();
+    if (steps - tw + 1 <= 16 * kNodesPerLane) {
+      const unsigned src = 16 * half;
+      const float2 r = make_float2(__shfl_sync(0xffffffffu, mr, src), __shfl_sync(0xffffffffu, mr, src + 8));
+      const float2 sc = make_float2(__shfl_sync(0xffffffffu, ms, src), __shfl_sync(0xffffffffu, ms, src + 8));
+      const float2 v = half_lattice<U>(steps, tw, r, sc, bufs[half], lh);
+      if (lh == 0) {
+        const uint64_t i = 2 * half;
+        if (i < left) out[o + i] = static_cast<float>(static_cast<double>(v.x) * tails[i]);
+        if (i + 1 < left) out[o + i + 1] = static_cast<float>(static_cast<double>(v.y) * tails[i + 1]);
+      }
+    } else {
+#pragma unroll 1
+      for (int p = 0; p < 2; ++p) {
+        const float2 r = make_float2(__shfl_sync(0xffffffffu, mr, 16 * p), __shfl_sync(0xffffffffu, mr, 16 * p + 8));
+        const float2 sc = make_float2(__shfl_sync(0xffffffffu, ms, 16 * p), __shfl_sync(0xffffffffu, ms, 16 * p + 8));
+        const float2 v = warp_lattice<U>(bufs[p], steps, r, sc, bufs[p], lane);
+        if (lane == 0) {
+          const uint64_t i = 2 * p;
+          if (i < left) out[o + i] = static_cast<float>(static_cast<double>(v.x) * tails[i]);
+          if (i + 1 < left) out[o + i + 1] = static_cast<float>(static_cast<double>(v.y) * tails[i + 1]);
+        }
+      }
+    }
+    __syncwarp();  // the next group rewrites the buffers
+  }
+}
+
+template <int MB, int U>
+cudaError_t launch_hw(const KernelSpec& spec, const LaunchEnv& env, uint64_t first_opt, uint64_t n_opt) {
+  const uint64_t warps_per_block = kThreads / 32;
+  const uint64_t groups = (n_opt + 3) / 4;
+  uint64_t blocks = (groups + warps_per_block - 1) / warps_per_block;
+  const uint64_t cap = static_cast<uint64_t>(env.sms) * 8 * 16;
+  if (blocks > cap) blocks = cap;
+  binomial_hw<MB, U><<<static_cast<unsigned>(blocks), kThreads, 0, env.stream>>>(
+      static_cast<const float*>(env.in[0]), static_cast<float*>(env.out[0]), static_cast<int>(spec.binom.steps),
+      first_opt, n_opt);
+  return cudaGetLastError();
 }
 
 // Four options per warp: each half-warp carries an option pair packed in
@@ -302,14 +523,14 @@ cudaError_t launch_half(const KernelSpec& spec, const LaunchEnv& env, uint64_t f
   return cudaGetLastError();
 }
 
-template <int P, int MB>
+template <int P, int MB, bool Window = true>
 cudaError_t launch(const KernelSpec& spec, const LaunchEnv& env, uint64_t first_opt, uint64_t n_opt) {
   const uint64_t warps_per_block = kThreads / 32;
   const uint64_t groups = (n_opt + P - 1) / P;
   uint64_t blocks = (groups + warps_per_block - 1) / warps_per_block;
   const uint64_t cap = static_cast<uint64_t>(env.sms) * 8 * 16;
   if (blocks > cap) blocks = cap;
-  binomial_warp<P, MB><<<static_cast<unsigned>(blocks), kThreads, 0, env.stream>>>(
+  binomial_warp<P, MB, Window><<<static_cast<unsigned>(blocks), kThreads, 0, env.stream>>>(
       static_cast<const float*>(env.in[0]), static_cast<float*>(env.out[0]), static_cast<int>(spec.binom.steps),
       first_opt, n_opt);
   return cudaGetLastError();
@@ -322,7 +543,7 @@ cudaError_t launch_binomial(const KernelSpec& spec, const LaunchEnv& env, uint64
   if (spec.binom.steps + 1 > 32 * kNodesPerLane) return cudaErrorInvalidValue;
   // work-items -> work-groups -> scalar options (4 per float4 work-group)
   const uint64_t first_opt = first / spec.lws * 4, n_opt = count / spec.lws * 4;
-  static const int env_variant = [] {  // ECL_BINOMIAL_VARIANT=1: scalar lattice
+  static const int env_variant = [] {  // ECL_BINOMIAL_VARIANT: variant when the kernel id has no @n
     const char* v = std::getenv("ECL_BINOMIAL_VARIANT");
     return v ? std::atoi(v) : 0;
   }();
@@ -331,18 +552,38 @@ cudaError_t launch_binomial(const KernelSpec& spec, const LaunchEnv& env, uint64
     const char* v = std::getenv("ECL_BINOMIAL_MB");
     return v ? std::atoi(v) : 0;
   }();
-  if (variant == 1) return launch<1, 4>(spec, env, first_opt, n_opt);
-  if (variant == 2) {
-    switch (mb) {
-      case 2: return launch_half<2>(spec, env, first_opt, n_opt);
-      case 4: return launch_half<4>(spec, env, first_opt, n_opt);
-      default: return launch_half<3>(spec, env, first_opt, n_opt);
-    }
-  }
-  switch (mb) {  // measured: 4 (52 registers) 18.8 ms, 5 19.1 ms, 6 19.2 ms
-    case 5: return launch<2, 5>(spec, env, first_opt, n_opt);
-    case 6: return launch<2, 6>(spec, env, first_opt, n_opt);
-    default: return launch<2, 4>(spec, env, first_opt, n_opt);
+  // Variants (all bit-identical; times at the 8M x 254 config, one launch):
+  //   0  binomial_hw: half-warp pairs + zero window      12.69 ms (MB 6, unroll 4)
+  //   1  scalar full lattice, one option per warp         20.2 ms
+  //   2  half-warp pairs, 16 nodes per lane, full lattice 18.8 ms
+  //   3  packed pair per warp, full lattice (round 1)     17.5 ms
+  //   4  packed pair per warp + zero window (32 lanes)    17.6 ms: 26 % fewer
+  //      FFMA2s, same time — the per-level exchange paced it, hence variant 0
+  static const int hw_unroll = [] {  // ECL_BINOMIAL_UNROLL: level-loop unroll of the default kernel
+    const char* v = std::getenv("ECL_BINOMIAL_UNROLL");
+    return v ? std::atoi(v) : 4;
+  }();
+  switch (variant) {
+    case 1: return launch<1, 4>(spec, env, first_opt, n_opt);
+    case 2:
+      switch (mb) {
+        case 2: return launch_half<2>(spec, env, first_opt, n_opt);
+        case 4: return launch_half<4>(spec, env, first_opt, n_opt);
+        default: return launch_half<3>(spec, env, first_opt, n_opt);
+      }
+    case 3: return launch<2, 4, false>(spec, env, first_opt, n_opt);
+    case 4: return launch<2, 4>(spec, env, first_opt, n_opt);
+    default:
+      // measured (MB, unroll): (4,2) 13.57, (4,4) 12.93, (5,2) 12.97,
+      // (5,4) 12.84, (6,2) 12.69, (6,4) 12.69 ms
+      switch ((mb ? mb : 6) * 10 + hw_unroll) {
+        case 42: return launch_hw<4, 2>(spec, env, first_opt, n_opt);
+        case 44: return launch_hw<4, 4>(spec, env, first_opt, n_opt);
+        case 52: return launch_hw<5, 2>(spec, env, first_opt, n_opt);
+        case 54: return launch_hw<5, 4>(spec, env, first_opt, n_opt);
+        case 62: return launch_hw<6, 2>(spec, env, first_opt, n_opt);
+        default: return launch_hw<6, 4>(spec, env, first_opt, n_opt);
+      }
   }
 }
 

@@ -105,27 +105,37 @@ import paper_1805_02755_b200 as P
 from paper_1805_02755_b200 import workloads as W
 opts = 4 * 777
 rand = W.binomial_inputs(opts, seed=11)[0]
-prog = P.validate_program(W.binomial_spec(opts))
-with P.Engine(P.EngineConfig([P.cuda_device("gpu0", 0)], P.DynamicConfig(13)), prog) as e:
-    np.save(sys.argv[1], e.run([rand]).outputs[0].view(np.float32))
+# deep in / at / out of the money and both ends of the range: the packed
+# kernel's zero window starts anywhere from node 0 to the top
+rand[:16] = np.array([0.0, 1e-7, 1e-4, 1e-3, 0.01, 0.02, 0.05, 0.1, 0.3, 0.5, 0.7, 0.9, 0.99, 0.999,
+                      1 - 2**-24, 0.25], np.float32)
+out = []
+for steps in (254, 255, 200, 129, 100, 64, 33, 31, 7, 1):
+    prog = P.validate_program(W.binomial_spec(opts, steps))
+    with P.Engine(P.EngineConfig([P.cuda_device("gpu0", 0)], P.DynamicConfig(13)), prog) as e:
+        out.append(e.run([rand]).outputs[0].view(np.float32))
+np.save(sys.argv[1], np.concatenate(out))
 """
 
 
 def test_binomial_packed_lattice_is_bit_identical_to_scalar(gpu_available, tmp_path):
     # FFMA2/FADD2 round each component like FFMA/FADD: the packed two-options-
-    # per-warp kernel must reproduce the scalar kernel (ECL_BINOMIAL_VARIANT=1)
+    # per-warp kernel must reproduce the scalar kernel (ECL_BINOMIAL_VARIANT=1),
+    # which runs the full lattice — so this also pins the packed kernel's zero
+    # window (it skips exact zeros only) at every window width
     import os
     import subprocess
     import sys
     outs = []
-    for variant in ("1", "0"):
+    for variant in ("1", "0", "3", "4"):
         f = tmp_path / f"v{variant}.npy"
         env = dict(os.environ, ECL_BINOMIAL_VARIANT=variant)
         r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, str(f)], env=env, capture_output=True,
                            text=True, timeout=300)
         assert r.returncode == 0, r.stderr
         outs.append(np.load(f))
-    assert outs[0].view(np.uint32).tolist() == outs[1].view(np.uint32).tolist()
+    for o in outs[1:]:
+        assert outs[0].view(np.uint32).tolist() == o.view(np.uint32).tolist()
 
 
 def test_binomial_prices_are_sane(gpu_available):
