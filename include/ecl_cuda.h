@@ -212,6 +212,12 @@ int ecl_gpu_download_tally(ecl_gpu* gpu, uint32_t* host_counts);
 /* One launch over the whole grid on the compute stream; *kernel_ms is the
  * CUDA-event time of that launch.  Synchronous. */
 int ecl_gpu_native_run(ecl_gpu* gpu, float* kernel_ms);
+/* The same grid as launches of `items_per_launch` work-items (rounded down
+ * to whole work-groups) alternating over the device's compute lanes, no
+ * scheduler: the best plain-CUDA program for kernels whose single launch
+ * leaves a tail (persistent warps draining) that a second stream can fill.
+ * *kernel_ms spans the first launch's start to the last one's end. */
+int ecl_gpu_native_run_split(ecl_gpu* gpu, uint64_t items_per_launch, float* kernel_ms);
 
 /* Work-items per sub-launch when a package copies to host buffers (default
  * 2^23; 0 = one launch per package): bounds how much compute precedes the

@@ -59,6 +59,9 @@ int64_t ecl_engine_trace_json(ecl_engine* engine, char* buf, uint64_t cap);
 /* Native baseline: one launch over the whole grid on the first device. */
 int ecl_engine_native_run(ecl_engine* engine, const void* const* inputs, uint32_t n_inputs, void* const* outputs,
                           uint32_t n_outputs, double* kernel_ms, double* total_ms);
+/* Native baseline as plain sub-launches of items_per_launch work-items over
+ * the first device's two compute streams (resident outputs, no scheduler). */
+int ecl_engine_native_run_split(ecl_engine* engine, uint64_t items_per_launch, double* kernel_ms);
 /* Adaptive HGuided: the work-items/ms per device the last run measured (the
  * next run's seed powers); *n = 0 before a run measured every device. */
 int ecl_engine_learned_powers(const ecl_engine* engine, double* powers, uint32_t cap, uint32_t* n);

@@ -49,6 +49,7 @@ _sig("ecl_engine_gather", c_int, c_void_p, PVOID, c_u32)
 _sig("ecl_engine_trace_json", c_i64, c_void_p, c_char_p, c_u64)
 _sig("ecl_engine_native_run", c_int, c_void_p, PVOID, c_u32, PVOID, c_u32, ctypes.POINTER(c_dbl),
      ctypes.POINTER(c_dbl))
+_sig("ecl_engine_native_run_split", c_int, c_void_p, c_u64, ctypes.POINTER(c_dbl))
 _sig("ecl_engine_kernel_time", c_int, c_void_p, ctypes.POINTER(c_dbl), ctypes.POINTER(c_u64), c_int)
 _sig("ecl_engine_init_ms", c_dbl, c_void_p)
 _sig("ecl_engine_learned_powers", c_int, c_void_p, ctypes.POINTER(c_dbl), c_u32, ctypes.POINTER(c_u32))

@@ -668,6 +668,16 @@ class Engine:
             self._fail(rc)
         return k.value, t.value
 
+    def native_run_split(self, items_per_launch: int) -> float:
+        """The same grid as plain sub-launches of `items_per_launch`
+        work-items over the first device's two compute streams (resident
+        outputs): kernel span in ms."""
+        k = ctypes.c_double(0)
+        rc = N.lib.ecl_engine_native_run_split(self._h, int(items_per_launch), ctypes.byref(k))
+        if rc != 0:
+            self._fail(rc)
+        return k.value
+
     def kernel_timing(self, reset: bool = False) -> Tuple[float, int]:
         ms, n = ctypes.c_double(0), ctypes.c_uint64(0)
         _check(N.lib.ecl_engine_kernel_time(self._h, ctypes.byref(ms), ctypes.byref(n), 1 if reset else 0))

@@ -14,7 +14,8 @@
 //                  outputs keep results device-resident (gather() later).
 //   run_virtual()  the virtual-clock replay (engine.hpp:306-338) with
 //                  caller-supplied per-item costs; trace only.
-//   native_run()   one launch over the whole grid: the overhead denominator.
+//   native_run()   one launch over the whole grid: the overhead denominator;
+//   native_run_split()  the same grid as plain sub-launches on two streams.
 #pragma once
 
 #include <cstddef>
@@ -120,6 +121,10 @@ class Engine {
   /// One kernel launch over the whole grid on the first device, same
   /// uploads/downloads as run_into (outputs may be empty).
   NativeResult native_run(std::span<const void* const> inputs, std::span<void* const> outputs);
+  // The same kernel as launches of items_per_launch work-items alternating
+  // over the first device's compute lanes (resident outputs, no scheduler):
+  // returns the kernel span in ms.
+  double native_run_split(std::uint64_t items_per_launch);
 
   KernelTiming kernel_timing(bool reset);
   /// Adaptive HGuided: the per-device work-items/ms the last run measured,

@@ -1159,6 +1159,37 @@ int ecl_gpu_native_run(ecl_gpu* g, float* kernel_ms) {
   return fan_out_lane0(g);
 }
 
+int ecl_gpu_native_run_split(ecl_gpu* g, uint64_t items_per_launch, float* kernel_ms) {
+  if (!g->spec) return fail(ECL_CONFIG_ERROR, "native run before bind");
+  const uint64_t lws = g->spec->lws, gws = g->spec->gws;
+  uint64_t piece = items_per_launch / lws * lws;
+  if (piece == 0) piece = lws;
+  if (int rc = set_device(g)) return rc;
+  if (int rc = ensure_mirrors(g)) return rc;
+  if (int rc = join_lanes(g)) return rc;
+  if (int rc = flush_streamed(g)) return rc;
+  ECL_CK(cudaEventRecord(g->up_ev, g->h2d));
+  ECL_CK(cudaStreamWaitEvent(g->lane[0], g->up_ev, 0));
+  Slot& slot = g->slots[kSlots - 1];
+  ECL_CK(cudaEventRecord(slot.start, g->lane[0]));
+  if (int rc = fan_out_lane0(g)) return rc;  // every lane starts after the start event
+  uint64_t launches = 0;
+  for (uint64_t first = 0; first < gws; first += piece, ++launches) {
+    const uint64_t count = first + piece < gws ? piece : gws - first;
+    cudaError_t e = ecl::launch_kernel(*g->spec, env_of(g, static_cast<int>(launches % g->lanes)), first, count);
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  }
+  if (int rc = join_lanes(g)) return rc;
+  ECL_CK(cudaEventRecord(slot.end, g->lane[0]));
+  ECL_CK(cudaEventSynchronize(slot.end));
+  float ms = 0.f;
+  ECL_CK(cudaEventElapsedTime(&ms, slot.start, slot.end));
+  *kernel_ms = ms;
+  g->kernel_ms += ms;
+  g->launches += launches;
+  return fan_out_lane0(g);
+}
+
 int ecl_gpu_kernel_time(ecl_gpu* g, double* total_ms, uint64_t* launches, int reset) {
   *total_ms = g->kernel_ms;
   *launches = g->launches;

@@ -90,35 +90,82 @@ __device__ __forceinline__ void pair_disc(V3 o, V3 d, float4 r0, float4 r1, floa
   const float2 cc = __fadd2_rn(__fadd2_rn(__fadd2_rn(pmul(ox, ox), pmul(oy, oy)), pmul(oz, oz)), neg2(RR));
   disc = __fadd2_rn(pmul(b, b), neg2(cc));
 }
-// Both spheres missed outright (disc < 0 for both: root_of would return -1
-// twice).  Most pair tests end here.
-__device__ __forceinline__ bool pair_misses(float2 disc) { return fmaxf(disc.x, disc.y) < 0.0f; }
 
-// Candidate scan: the packed discriminants of up to 32 sphere pairs from
-// `first`, branch-free, as a bit mask of the pairs where at least one sphere
-// has disc >= 0.  Groups of G pairs run unrolled; the loops over groups stay
-// rolled (a 32-pair unroll of both scans overflowed the instruction cache:
-// ncu "no instruction" was the top stall).  The rare candidates are then
-// resolved in increasing pair order, which keeps the oracle's
-// first-lowest-index choice among equal distances.
-template <int G>
-__device__ __forceinline__ uint32_t scan_group(V3 o, V3 d, const float4 (*rec)[2], uint32_t first) {
-  uint32_t mask = 0;
-#pragma unroll
-  for (int q = 0; q < G; ++q) {
-    float2 b, disc;
-    pair_disc(o, d, rec[first + q][0], rec[first + q][1], b, disc);
-    mask |= pair_misses(disc) ? 0u : (1u << q);
-  }
-  return mask;
+// Candidate scan with a conservative FMA prefilter.  The exact test above
+// costs 16 unfused lane-ops per sphere; the scan instead evaluates the same
+// discriminant in a translation-free form with FMAs, per sphere pair
+//   e    = o.d - s.d                      (o.d per ray, s.d: 3 FMA)
+//   cc   = (|o|^2 + q) - 2 o.s            (q = |s|^2 - r^2 per sphere, o.s: 3 FMA)
+//   disc'= e*e - cc
+// (10 packed instructions per pair instead of 16) and rejects a sphere only
+// when disc' < -M, M = 2^-17 ((|o|_1 + max|s|)^2 + max r^2).  Error bound
+// (u = 2^-24, R >= |o| + |s|, |d| = 1): the IEEE-ordered exact path's disc
+// is within 17.1 u R^2 + 3 u r^2 of the real-number discriminant, disc'
+// within ~20 u (R^2 + r^2) — together < 40 u (R^2 + r^2) <= M / 3 — so
+// disc' < -M implies the exact disc < 0: the exact test would miss too.
+// Every sphere that survives goes through the exact test (pair_disc +
+// root_of), so the image stays bit-identical; only provable misses are
+// skipped.
+struct RayPre {
+  float2 ox, oy, oz, dx, dy, dz;  // (v, v) pairs: FFMA2 operands
+  float2 od, moo;                 // o.d and M - |o|^2
+  uint32_t all;                   // ~0u: M overflowed, every pair is a candidate
+};
+__device__ __forceinline__ RayPre ray_pre(V3 o, V3 d, float smax, float rmax2) {
+  RayPre p;
+  p.ox = make_float2(o.x, o.x);
+  p.oy = make_float2(o.y, o.y);
+  p.oz = make_float2(o.z, o.z);
+  p.dx = make_float2(d.x, d.x);
+  p.dy = make_float2(d.y, d.y);
+  p.dz = make_float2(d.z, d.z);
+  const float od = fmaf(o.z, d.z, fmaf(o.y, d.y, o.x * d.x));
+  const float oo = fmaf(o.z, o.z, fmaf(o.y, o.y, o.x * o.x));
+  const float R = fabsf(o.x) + fabsf(o.y) + fabsf(o.z) + smax;
+  const float M = 0x1p-17f * fmaf(R, R, rmax2);
+  p.od = make_float2(od, od);
+  p.moo = make_float2(M - oo, M - oo);
+  // with M finite every magnitude below is finite (no NaN); otherwise skip nothing
+  p.all = M < INFINITY ? 0u : ~0u;
+  return p;
 }
-__device__ __forceinline__ uint32_t scan_chunk(V3 o, V3 d, const float4 (*rec)[2], uint32_t first, uint32_t n) {
+// pre[i] = (x0, x1, y0, y1), (z0, z1, q0, q1) for sphere pair i.  The scan
+// evaluates t = disc' + M = e*e + ((M - |o|^2 - q) + 2 o.s) and collects the
+// sign bits: a sphere is rejected iff t < 0, a pair iff both are — one AND of
+// the two words and one funnel shift per pair, no compares.  Bit G-1-k of
+// the collected word is pair k's "both rejected".
+template <int G>
+__device__ __forceinline__ uint32_t scan_group(const RayPre& p, const float4 (*pre)[2], uint32_t first) {
+  static_assert(G >= 1 && G <= 32, "group of at most 32 pairs");
+  uint32_t miss = 0;
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    const float4 r0 = pre[first + k][0], r1 = pre[first + k][1];
+    const float2 X = make_float2(r0.x, r0.y), Y = make_float2(r0.z, r0.w);
+    const float2 Z = make_float2(r1.x, r1.y), Q = make_float2(r1.z, r1.w);
+    const float2 sd = __ffma2_rn(Z, p.dz, __ffma2_rn(Y, p.dy, __fmul2_rn(X, p.dx)));
+    const float2 os = __ffma2_rn(Z, p.oz, __ffma2_rn(Y, p.oy, __fmul2_rn(X, p.ox)));
+    const float2 e = __fadd2_rn(p.od, neg2(sd));
+    const float2 mc = __ffma2_rn(os, make_float2(2.0f, 2.0f), __fadd2_rn(p.moo, neg2(Q)));  // M - cc
+    const float2 t = __ffma2_rn(e, e, mc);
+    miss = __funnelshift_l(__float_as_uint(t.x) & __float_as_uint(t.y), miss, 1);
+  }
+  const uint32_t cand = (~miss | p.all) & (G == 32 ? ~0u : ((1u << G) - 1u));
+  return __brev(cand) >> (32 - G);
+}
+// Candidate pairs among up to 32 from `first`, as a bit mask, branch-free.
+// Groups of G pairs run unrolled; the loops over groups stay rolled (a
+// 32-pair unroll of both scans overflowed the instruction cache: ncu "no
+// instruction" was the top stall).  The rare candidates are then resolved
+// exactly in increasing pair order, which keeps the oracle's
+// first-lowest-index choice among equal distances.
+__device__ __forceinline__ uint32_t scan_chunk(const RayPre& p, const float4 (*pre)[2], uint32_t first, uint32_t n) {
   constexpr int kGroup = 16;
   uint32_t mask = 0, q = 0;
 #pragma unroll 1
-  for (; q + kGroup <= n; q += kGroup) mask |= scan_group<kGroup>(o, d, rec, first + q) << q;
+  for (; q + kGroup <= n; q += kGroup) mask |= scan_group<kGroup>(p, pre, first + q) << q;
 #pragma unroll 1
-  for (; q < n; ++q) mask |= scan_group<1>(o, d, rec, first + q) << q;
+  for (; q < n; ++q) mask |= scan_group<1>(p, pre, first + q) << q;
   return mask;
 }
 
@@ -142,7 +189,7 @@ struct ShadowQueue {
 };
 
 size_t ray_smem_bytes(uint32_t ns) {
-  return sizeof(float4) * (2 * static_cast<size_t>(ns) + 2 * ((ns + 1) / 2)) +
+  return sizeof(float4) * (2 * static_cast<size_t>(ns) + 4 * ((ns + 1) / 2)) +
          sizeof(ShadowQueue) * (kThreads / 32);
 }
 
@@ -155,29 +202,43 @@ __global__ void __launch_bounds__(kThreads, MB)
   // records (x0, x1, y0, y1), (z0, z1, r0^2, r1^2), so a pair test reads two
   // LDS.128 off one pointer (packed operands aligned).
   extern __shared__ float4 smem[];
+  __shared__ unsigned bound_bits[2];  // max |s| and max r^2 as float bits (>= 0: integer order = float order)
   float4* const sph = smem;
   float4* const mat = smem + ns;
   float4 (*const pair_rec)[2] = reinterpret_cast<float4 (*)[2]>(smem + 2 * ns);
-  ShadowQueue* const sq = reinterpret_cast<ShadowQueue*>(smem + 2 * ns + 2 * ((ns + 1) / 2)) + (threadIdx.x >> 5);
+  float4 (*const pre_rec)[2] = reinterpret_cast<float4 (*)[2]>(smem + 2 * ns + 2 * ((ns + 1) / 2));
+  ShadowQueue* const sq = reinterpret_cast<ShadowQueue*>(smem + 2 * ns + 4 * ((ns + 1) / 2)) + (threadIdx.x >> 5);
+  if (threadIdx.x < 2) bound_bits[threadIdx.x] = 0u;
+  __syncthreads();
   for (uint32_t i = threadIdx.x; i < ns; i += kThreads) {
     const float4 c = scene[i];
     sph[i] = c;
     mat[i] = scene[ns + i];
     float* rec = reinterpret_cast<float*>(pair_rec[i / 2]);
+    float* pre = reinterpret_cast<float*>(pre_rec[i / 2]);
     const uint32_t h = i & 1u;
-    rec[0 + h] = c.x;
-    rec[2 + h] = c.y;
-    rec[4 + h] = c.z;
+    rec[0 + h] = pre[0 + h] = c.x;
+    rec[2 + h] = pre[2 + h] = c.y;
+    rec[4 + h] = pre[4 + h] = c.z;
     rec[6 + h] = mul(c.w, c.w);
+    const double x = c.x, y = c.y, z = c.z, r = c.w;
+    pre[6 + h] = static_cast<float>(x * x + y * y + z * z - r * r);  // q = |s|^2 - r^2
+    // bounds rounded up (x 1.000001): M only has to dominate the error terms
+    atomicMax(&bound_bits[0], __float_as_uint(static_cast<float>(sqrt(x * x + y * y + z * z) * 1.000001)));
+    atomicMax(&bound_bits[1], __float_as_uint(static_cast<float>(r * r * 1.000001)));
   }
   // sphere pairs [0, pairs_end) go through pair_disc, an odd last one alone
   const uint32_t pairs_end = ns & ~1u, npairs = ns / 2;
 
-  const float4* cam4 = scene + 2 * ns;
-  const float4 cam = cam4[0];
-  const float4 lights[3] = {cam4[1], cam4[2], cam4[3]};
-  const float4 pmat = cam4[4], shading = cam4[5], sky = cam4[6];
+  // camera, lights, floor material, shading constants and sky stay in shared
+  // memory (broadcast reads where used): 28 registers the sphere scans need
+  __shared__ float4 env[7];
+  if (threadIdx.x < 7) env[threadIdx.x] = scene[2 * ns + threadIdx.x];
+  const float4& cam = env[0];
+  const float4* const lights = env + 1;
+  const float4 &pmat = env[4], &shading = env[5], &sky = env[6];
   __syncthreads();
+  const float smax = __uint_as_float(bound_bits[0]), rmax2 = __uint_as_float(bound_bits[1]);
 
   const unsigned lane_id = threadIdx.x & 31u;
   const unsigned below = (1u << lane_id) - 1u;
@@ -239,8 +300,9 @@ __global__ void __launch_bounds__(kThreads, MB)
       // ---- one bounce (oracle: trace_pixel loop body) ----
       float tmin = 1e30f;
       int hit = -1;
+      const RayPre rp = ray_pre(L.o, L.d, smax, rmax2);
       for (uint32_t c0 = 0; c0 < npairs; c0 += 32) {
-        for (uint32_t m = scan_chunk(L.o, L.d, pair_rec, c0, npairs - c0); m; m &= m - 1) {
+        for (uint32_t m = scan_chunk(rp, pre_rec, c0, npairs - c0); m; m &= m - 1) {
           const uint32_t pq = c0 + static_cast<uint32_t>(__ffs(m)) - 1, s = 2 * pq;
           float2 b, disc;
           pair_disc(L.o, L.d, pair_rec[pq][0], pair_rec[pq][1], b, disc);
@@ -324,8 +386,9 @@ __global__ void __launch_bounds__(kThreads, MB)
         const V3 po{pp.x, pp.y, pp.z}, ln{g.x, g.y, g.z};
         const float dist = g.w;
         bool shadow = false;
+        const RayPre rp = ray_pre(po, ln, smax, rmax2);
         for (uint32_t c0 = 0; c0 < npairs && !shadow; c0 += 32) {
-          for (uint32_t m = scan_chunk(po, ln, pair_rec, c0, npairs - c0); m && !shadow; m &= m - 1) {
+          for (uint32_t m = scan_chunk(rp, pre_rec, c0, npairs - c0); m && !shadow; m &= m - 1) {
             const uint32_t pq = c0 + static_cast<uint32_t>(__ffs(m)) - 1;
             float2 b, disc;
             pair_disc(po, ln, pair_rec[pq][0], pair_rec[pq][1], b, disc);
@@ -426,8 +489,10 @@ cudaError_t launch(const KernelSpec& spec, const LaunchEnv& env, uint64_t first,
 cudaError_t launch_ray(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
   if (count == 0) return cudaSuccess;
   // ECL_RAY_MB: 128-thread CTAs per SM the registers are sized for.  Measured
-  // (8192^2, candidate scans in 16-pair groups): 8 -> 13.04 ms (64
-  // registers), 10 -> 13.12 (48, spills); before the scans 10 was best.
+  // (8192^2, sign-bit prefiltered scans, scene constants in shared memory):
+  // 6 -> 11.40 ms (80 registers, 8 B spilled), 7 -> 11.15 (72, no spill),
+  // 8 -> 11.01 (64; 16 B of stack, 28 B of spill loads, outside the sphere
+  // scans: the occupancy pays for them), 10 -> 11.87.
   static const int env_mb = [] {
     const char* v = std::getenv("ECL_RAY_MB");
     return v ? std::atoi(v) : 0;

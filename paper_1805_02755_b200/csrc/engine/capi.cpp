@@ -164,6 +164,10 @@ int ecl_engine_native_run(ecl_engine* e, const void* const* inputs, uint32_t n_i
   });
 }
 
+int ecl_engine_native_run_split(ecl_engine* e, uint64_t items_per_launch, double* kernel_ms) {
+  return guarded(e, [&] { *kernel_ms = e->engine->native_run_split(items_per_launch); });
+}
+
 int ecl_engine_kernel_time(ecl_engine* e, double* kernel_ms, uint64_t* launches, int reset) {
   return guarded(e, [&] {
     const KernelTiming t = e->engine->kernel_timing(reset != 0);

@@ -771,6 +771,15 @@ struct Engine::Impl {
     r.total_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
     return r;
   }
+
+  double native_run_split(std::uint64_t items_per_launch) {
+    if (!wall()) throw Error(ErrorCode::ConfigError, "native_run needs cuda devices");
+    ecl_gpu* g = devices[0]->gpu;
+    check(ecl_gpu_sync(g), "sync");
+    float kms = 0.f;
+    check(ecl_gpu_native_run_split(g, items_per_launch, &kms), "native run");
+    return kms;
+  }
 };
 
 Engine::Engine(EngineConfig cfg, ValidatedProgram prog) : impl_(std::make_unique<Impl>(std::move(cfg), std::move(prog))) {
@@ -890,6 +899,8 @@ void Engine::gather(std::span<void* const> outputs) { impl_->gather(outputs); }
 NativeResult Engine::native_run(std::span<const void* const> inputs, std::span<void* const> outputs) {
   return impl_->native_run(inputs, outputs);
 }
+
+double Engine::native_run_split(std::uint64_t items_per_launch) { return impl_->native_run_split(items_per_launch); }
 
 KernelTiming Engine::kernel_timing(bool reset) {
   KernelTiming t;

@@ -89,3 +89,37 @@ def test_raw_executor_vecscale(gpu_available, lib, oracle):
         lib.ecl_kernel_destroy(k)
     finally:
         lib.ecl_gpu_close(g)
+
+
+def test_native_run_split_covers_the_grid(gpu_available, lib, oracle):
+    # the best-native denominator (ecl_gpu_native_run_split): the same grid
+    # as plain sub-launches over the two compute lanes, any piece size
+    so = lib
+    so.ecl_gpu_native_run_split.restype = c_int
+    so.ecl_gpu_native_run_split.argtypes = [c_vp, c_u64, ctypes.POINTER(ctypes.c_float)]
+    g = c_vp()
+    assert so.ecl_gpu_open(0, 2, ctypes.byref(g)) == 0
+    try:
+        n, lws = 3 * 4096 + 128, 128
+        args = (Arg * 2)(Arg(1, 0, 0, -0.5), Arg(1, 0, 0, 3.0))
+        geom = (Geom * 1)(Geom(8, n))
+        k = c_vp()
+        assert so.ecl_kernel_create(b"vecscale", n, lws, args, 2, geom, 1, geom, 1, 1, 1, ctypes.byref(k)) == 0
+        assert so.ecl_gpu_bind(g, k) == 0
+        din, dout = c_vp(), c_vp()
+        assert so.ecl_gpu_buffer(g, 0, 0, ctypes.byref(din)) == 0
+        assert so.ecl_gpu_buffer(g, 1, 0, ctypes.byref(dout)) == 0
+        x = np.linspace(-7, 5, n)
+        assert so.ecl_gpu_upload(g, din, x.ctypes.data, x.nbytes) == 0
+        ms = ctypes.c_float(0)
+        for items in (1000, 0, 4096, 1 << 30):  # 1000 -> 896 (whole work-groups), 0 -> one work-group
+            zero = np.zeros(n)
+            assert so.ecl_gpu_upload(g, dout, zero.ctypes.data, zero.nbytes) == 0
+            assert so.ecl_gpu_native_run_split(g, items, ctypes.byref(ms)) == 0
+            assert ms.value > 0
+            y = np.zeros(n)
+            assert so.ecl_gpu_download(g, y.ctypes.data, dout, y.nbytes) == 0
+            assert np.array_equal(y, oracle.vecscale(-0.5, 3.0, x)), items
+        so.ecl_kernel_destroy(k)
+    finally:
+        so.ecl_gpu_close(g)
