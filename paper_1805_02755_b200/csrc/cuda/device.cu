@@ -948,8 +948,10 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
   uint64_t piece_wg = size_wg;
   bool streaming = false;
   for (const char* p : g->pending_in) streaming = streaming || p != nullptr;
-  if ((copies || streaming) && g->d2h_split_items > 0) {
-    piece_wg = std::max<uint64_t>(1, g->d2h_split_items / s.lws);
+  const uint64_t split_items = (copies || streaming) ? g->d2h_split_items
+                                : (g->lanes > 1 ? s.compute_split_items : 0);
+  if (split_items > 0) {
+    piece_wg = std::max<uint64_t>(1, split_items / s.lws);
     uint64_t po = 0, pc = 0;
     if (out_range(s, offset_wg, std::min(piece_wg, size_wg), &po, &pc) != ECL_OK) piece_wg = size_wg;
   }

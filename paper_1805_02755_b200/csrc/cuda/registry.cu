@@ -235,6 +235,8 @@ int resolve_kernel(KernelSpec& s, std::string* err) {
       if (!one_to_one(s)) return bad(err, "ray writes with a 1:1 out pattern");
       s.ray = RayParams{static_cast<uint32_t>(w), static_cast<uint32_t>(h), static_cast<uint32_t>(ns),
                         static_cast<uint32_t>(depth)};
+      // resident packages as 2^20-item two-lane pieces (see compute_split_items)
+      s.compute_split_items = 1u << 20;
       return ECL_OK;
     }
   }

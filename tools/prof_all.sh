@@ -10,7 +10,7 @@ cap() {  # workload kernel-regex extra-args
 }
 cap mandelbrot mandel_persistent
 cap gaussian gaussian_tiled
-cap binomial binomial_warp
+cap binomial binomial_hw
 cap nbody nbody_step "--steps-override 1"
 cap ray ray_persistent
 cap mandelbrot_f32 mandel_x2
