@@ -555,14 +555,14 @@ def pcie_d2h_gbps(torch, ordinal, nbytes=256 << 20):
 L2_FLUSH_BYTES = 512 << 20
 
 NCU_KERNEL = {"mandelbrot": "mandel_persistent<double", "mandelbrot_f32": "mandel_x2<float",
-              "gaussian": "gaussian_tiled", "binomial": "binomial_warp", "nbody": "nbody_step",
+              "gaussian": "gaussian_tiled", "binomial": "binomial_hw", "nbody": "nbody_step",
               "ray": "ray_persistent"}
 
 
 def ncu_traffic(workload):
     """DRAM bytes (read + write) of the workload's kernel from the committed
-    ncu --set full capture of one launch (profiles/r1/ncu_summary.json)."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1", "ncu_summary.json")
+    ncu --set full capture of one launch (profiles/r2/ncu_summary.json)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2", "ncu_summary.json")
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     try:
         rows = json.load(open(path))
@@ -576,7 +576,7 @@ def ncu_traffic(workload):
             t = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
             return t, (f"dram__bytes_read.sum + dram__bytes_write.sum of one captured launch "
                        f"({r['gpu__time_duration.sum']}) of {NCU_KERNEL[workload]}, bytes per launch "
-                       f"(profiles/r1/ncu_summary.json; compute-bound: the bytes are the launch's outputs)")
+                       f"(profiles/r2/ncu_summary.json; compute-bound: the bytes are the launch's outputs)")
     return None, "kernel not in the committed ncu capture"
 
 
