@@ -56,10 +56,6 @@ template <int G>
 __device__ __forceinline__ float2 shfl_down1(float2 v) {
   return make_float2(__shfl_down_sync(0xffffffffu, v.x, 1, G), __shfl_down_sync(0xffffffffu, v.y, 1, G));
 }
-__device__ __forceinline__ float shfl_from(float v, unsigned src) { return __shfl_sync(0xffffffffu, v, src); }
-__device__ __forceinline__ float2 shfl_from(float2 v, unsigned src) {
-  return make_float2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
-}
 
 // Backward steps j, j-1, ... while j > stop, with NL nodes per lane (lane l
 // holds nodes NL*l .. NL*l+NL-1): w[t] <- w[t] + r*w[t+1].  The neighbour of
@@ -458,7 +454,7 @@ cudaError_t launch_hw(const KernelSpec& spec, const LaunchEnv& env, uint64_t fir
   const uint64_t warps_per_block = kThreads / 32;
   const uint64_t groups = (n_opt + 3) / 4;
   uint64_t blocks = (groups + warps_per_block - 1) / warps_per_block;
-  const uint64_t cap = static_cast<uint64_t>(env.sms) * 8 * 16;
+  const uint64_t cap = static_cast<uint64_t>(env.sms) * 8 * 16;  // measured: a persistent grid (1 wave) 13.3 ms vs 12.7
   if (blocks > cap) blocks = cap;
   binomial_hw<MB, U><<<static_cast<unsigned>(blocks), kThreads, 0, env.stream>>>(
       static_cast<const float*>(env.in[0]), static_cast<float*>(env.out[0]), static_cast<int>(spec.binom.steps),
@@ -559,6 +555,9 @@ cudaError_t launch_binomial(const KernelSpec& spec, const LaunchEnv& env, uint64
   //   3  packed pair per warp, full lattice (round 1)     17.5 ms
   //   4  packed pair per warp + zero window (32 lanes)    17.6 ms: 26 % fewer
   //      FFMA2s, same time — the per-level exchange paced it, hence variant 0
+  // Measured and dropped: 32-option chunks sorted by t0 (fewer > 128-node
+  // windows, FP64 setup once per option) 12.79 ms — the saved FP64 work
+  // came back as register pressure at 6 CTAs/SM; a persistent grid 13.3 ms.
   static const int hw_unroll = [] {  // ECL_BINOMIAL_UNROLL: level-loop unroll of the default kernel
     const char* v = std::getenv("ECL_BINOMIAL_UNROLL");
     return v ? std::atoi(v) : 4;
@@ -573,6 +572,8 @@ cudaError_t launch_binomial(const KernelSpec& spec, const LaunchEnv& env, uint64
       }
     case 3: return launch<2, 4, false>(spec, env, first_opt, n_opt);
     case 4: return launch<2, 4>(spec, env, first_opt, n_opt);
+    default: return launch_sorted<6, 4>(spec, env, first_opt, n_opt);
+      }
     default:
       // measured (MB, unroll): (4,2) 13.57, (4,4) 12.93, (5,2) 12.97,
       // (5,4) 12.84, (6,2) 12.69, (6,4) 12.69 ms

@@ -255,3 +255,40 @@ def test_binomial_streamed_inputs_single_device(gpu_available, oracle):
         res = e.run([rand])
     ok, worst = rel_close(res.outputs[0].view(np.float32), oracle.binomial(rand, steps), 1e-5, atol=1e-6)
     assert ok, worst
+
+
+_PEER_SCRIPT = """
+import sys, numpy as np
+import paper_1805_02755_b200 as P
+from paper_1805_02755_b200 import workloads as W
+from tests._oracle import Oracle
+o = Oracle()
+n, steps = 4096, 3
+pos, vel = o.nbody_init(7, n)
+prog = P.validate_program(W.nbody_spec(n))
+out = [np.zeros((n, 4), np.float32), np.zeros((n, 4), np.float32)]
+devs = [P.cuda_device(f"gpu0{c}", 0) for c in "abc"]
+with P.Engine(P.EngineConfig(devs, P.DynamicConfig(6)), prog) as e:
+    e.run_steps([pos, vel], out, steps, [(0, 0), (1, 1)])
+ep, ev = pos, vel
+for _ in range(steps):
+    ep, ev = o.nbody_step(ep, ev, 0.005, 500.0)
+err = np.abs(out[0] - ep) / np.maximum(np.abs(ep), 1e-6)
+print(float(err.max()))
+"""
+
+
+def test_nbody_exchange_through_the_peer_copy_path(gpu_available):
+    # ECL_FORCE_PEER_COPY=1 routes the per-step owner-slice broadcast between
+    # logical devices on one ordinal through cudaMemcpyPeerAsync — the call
+    # the multi-GPU exchange makes over NVLink (device.cu
+    # ecl_broadcast_output_slice); input replication always uses it
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ECL_FORCE_PEER_COPY="1", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", _PEER_SCRIPT], env=env, capture_output=True, text=True, timeout=300,
+                       cwd=root)
+    assert r.returncode == 0, r.stderr
+    assert float(r.stdout.strip().splitlines()[-1]) <= 1e-4
