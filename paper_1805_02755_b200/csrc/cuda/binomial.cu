@@ -572,8 +572,6 @@ cudaError_t launch_binomial(const KernelSpec& spec, const LaunchEnv& env, uint64
       }
     case 3: return launch<2, 4, false>(spec, env, first_opt, n_opt);
     case 4: return launch<2, 4>(spec, env, first_opt, n_opt);
-    default: return launch_sorted<6, 4>(spec, env, first_opt, n_opt);
-      }
     default:
       // measured (MB, unroll): (4,2) 13.57, (4,4) 12.93, (5,2) 12.97,
       // (5,4) 12.84, (6,2) 12.69, (6,4) 12.69 ms
