@@ -732,7 +732,9 @@ class PinnedBuffer:
     def free(self):
         if getattr(self, "_ptr", None):
             self.array = None
-            N.lib.ecl_host_free(self._ptr)
+            lib = getattr(N, "lib", None)
+            if lib is not None:  # at interpreter exit the module may already be torn down
+                lib.ecl_host_free(self._ptr)
             self._ptr = None
 
     def __del__(self):

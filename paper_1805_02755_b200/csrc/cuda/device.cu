@@ -977,6 +977,7 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
     cudaStream_t cp = g->copy[pl];
     ecl::LaunchEnv env = env_of(g, pl);
     if (widen) env.compact = g->compact_dev;
+    env.host_copies = copies;
     const uint64_t n_wg = std::min(piece_wg, offset_wg + size_wg - wg);
     const uint64_t first = wg * s.lws, count = n_wg * s.lws;
     if (streaming || g->up_live) {

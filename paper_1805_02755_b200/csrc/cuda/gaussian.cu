@@ -24,6 +24,10 @@
 // Packages are arbitrary work-item ranges: tiles cover the rows the range
 // touches and only pixels inside [first, first+count) are written.
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -189,6 +193,221 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ---- Separable path --------------------------------------------------------
+// A rank-1 filter w[i][j] = r[i] c[j] (the Gaussian one is) takes F + F taps
+// per pixel instead of F*F: a horizontal pass over the staged (32+F-1) rows
+// into a shared-memory buffer, then a vertical pass — ~91 FMAs per pixel at
+// F = 31 against 961, which moves the kernel from the FMA pipe towards the
+// memory system (8 B of algorithmic HBM traffic per pixel).  Taps travel in
+// packed pairs through FFMA2 as in gaussian_tiled.  Numerics: the factors
+// are taken in double from the filter's centre row and column and the
+// factorisation is accepted only when every r[i] c[j] matches w[i][j] to
+// 2^-20 relative (a few float ulps), so the result differs from the direct
+// sum by the factorisation's rounding plus a 62-term reassociation (both
+// ~1e-7 relative against the 1e-5 budget).  Any other filter runs the
+// direct kernel.
+template <int F>
+struct SepTaps {
+  __align__(16) float c[F + 1];   // horizontal taps (pairs (2m, 2m+1)), zero-padded
+  __align__(16) float cb[F + 1];  // c shifted by one: pairs (2m+1, 2m+2)
+  float r[F];                     // vertical taps
+};
+
+constexpr int kHPitch = 68;  // horizontal-pass buffer pitch (floats): rows of 64 + 4 (bank spread)
+
+// One 64x32 output tile per CTA (41.7 KB of shared memory at F = 31: 5
+// CTAs per SM, so the hardware overlaps one CTA's TMA rows with the others'
+// passes).  Measured and dropped: persistent CTAs with the input tile
+// double-buffered (prefetch of tile k+1 during tile k) fit 3 CTAs per SM
+// and ran 98 us against 79.
+template <int F, int TO>
+__global__ void __launch_bounds__(kThreads)
+    gaussian_sep(const float* __restrict__ img, float* __restrict__ out, int W, int H, uint64_t first, uint64_t count,
+                 int row0, const __grid_constant__ SepTaps<F> taps) {
+  constexpr int R = F / 2;
+  constexpr int TH = TO + F - 1;  // staged rows (TO output rows per tile)
+  constexpr int NV = 8 + F - 1;
+  constexpr int SHIFT = (4 - R % 4) % 4;
+  constexpr int NL = (SHIFT + NV + 3) / 4;
+  constexpr int NP = (F - 1) / 2;
+  extern __shared__ __align__(128) float sep_smem[];
+  float* const tile = sep_smem;
+  float* const hbuf = sep_smem + TH * kPitch;
+  __shared__ __align__(8) uint64_t bar;
+
+  const int tile_x = blockIdx.x * kTileW;
+  const int tile_y = row0 + blockIdx.y * TO;
+  const bool interior = tile_x >= 16 && tile_x + kTileW + 16 <= W && tile_y - R >= 0 && tile_y + TO + R <= H &&
+                        (W & 3) == 0;
+  if (interior) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) mbar_expect_tx(&bar, TH * 96 * 4);
+    __syncthreads();
+    if (threadIdx.x < TH) {
+      const int gy = tile_y - R + threadIdx.x;
+      bulk_g2s(&tile[threadIdx.x * kPitch], img + static_cast<int64_t>(gy) * W + (tile_x - 16), 96 * 4, &bar);
+    }
+    mbar_wait(&bar, 0);
+  } else {
+    for (int k = threadIdx.x; k < TH * 96; k += kThreads) {
+      const int r = k / 96, c = k - r * 96;
+      const int gy = clampi(tile_y - R + r, 0, H - 1), gx = clampi(tile_x - 16 + c, 0, W - 1);
+      tile[r * kPitch + c] = img[static_cast<int64_t>(gy) * W + gx];
+    }
+    __syncthreads();
+  }
+
+  // Horizontal pass: segment (row, s) = 8 outputs hbuf[row][8s .. 8s+7].
+  // The 8 lanes of an LDS.128 phase take 8 consecutive rows of one segment
+  // column: the 100-float tile pitch and the 68-float buffer pitch put them
+  // on disjoint banks (conflict-free loads and stores).
+  const float2* wa = reinterpret_cast<const float2*>(taps.c);
+  const float2* wb = reinterpret_cast<const float2*>(taps.cb);
+#pragma unroll 1
+  for (int seg = threadIdx.x; seg < ((TH + 7) & ~7) * 8; seg += kThreads) {
+    const int row = (seg & 7) + 8 * (seg >> 6), s8 = (seg >> 3) & 7;
+    if (row >= TH) continue;
+    const float4* src = reinterpret_cast<const float4*>(tile + row * kPitch + (16 + 8 * s8 - R - SHIFT));
+    float2 ev[NL * 2];
+#pragma unroll
+    for (int m = 0; m < NL; ++m) {
+      const float4 q = src[m];
+      ev[2 * m] = make_float2(q.x, q.y);
+      ev[2 * m + 1] = make_float2(q.z, q.w);
+    }
+    float2 acc[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      acc[b] = make_float2(0.0f, 0.0f);
+      const int a0 = SHIFT + b;
+      if ((a0 & 1) == 0) {
+#pragma unroll
+        for (int m = 0; m < NP; ++m) acc[b] = __ffma2_rn(wa[m], ev[a0 / 2 + m], acc[b]);
+        const int a = a0 + F - 1;
+        acc[b].x = fmaf(taps.c[F - 1], (a & 1) ? ev[a >> 1].y : ev[a >> 1].x, acc[b].x);
+      } else {
+        acc[b].x = fmaf(taps.c[0], ev[a0 >> 1].y, acc[b].x);
+#pragma unroll
+        for (int m = 0; m < NP; ++m) acc[b] = __ffma2_rn(wb[m], ev[(a0 + 1) / 2 + m], acc[b]);
+      }
+    }
+    float4* dst = reinterpret_cast<float4*>(hbuf + row * kHPitch + 8 * s8);
+    dst[0] = make_float4(acc[0].x + acc[0].y, acc[1].x + acc[1].y, acc[2].x + acc[2].y, acc[3].x + acc[3].y);
+    dst[1] = make_float4(acc[4].x + acc[4].y, acc[5].x + acc[5].y, acc[6].x + acc[6].y, acc[7].x + acc[7].y);
+  }
+  __syncthreads();
+
+  // Vertical pass: lane = column pair (64 columns per warp), warp = 4 output
+  // rows.  A thread slides down its column pair through 4 + F - 1 buffer
+  // rows (one LDS.64 each) and feeds every output row the tap it owes —
+  // each loaded value serves up to 4 outputs from registers.
+  constexpr int VR = TO / (kThreads / 32);  // output rows per thread
+  const int lane = threadIdx.x & 31, y0 = (threadIdx.x >> 5) * VR;
+  float2 acc[VR];
+#pragma unroll
+  for (int o = 0; o < VR; ++o) acc[o] = make_float2(0.f, 0.f);
+  const float* col = hbuf + y0 * kHPitch + 2 * lane;
+#pragma unroll
+  for (int i = 0; i < VR + F - 1; ++i) {
+    const float2 h = *reinterpret_cast<const float2*>(col + i * kHPitch);
+#pragma unroll
+    for (int o = 0; o < VR; ++o) {
+      const int tap = i - o;
+      if (tap >= 0 && tap < F) acc[o] = __ffma2_rn(make_float2(taps.r[tap], taps.r[tap]), h, acc[o]);
+    }
+  }
+
+  const int gx = tile_x + 2 * lane;
+  if (gx >= W) return;
+#pragma unroll
+  for (int o = 0; o < VR; ++o) {
+    const int gy = tile_y + y0 + o;
+    if (gy >= H) break;
+    const uint64_t base = static_cast<uint64_t>(gy) * W + gx;
+    float* dst = out + base;
+    if (base >= first && base + 2 <= first + count && gx + 2 <= W && (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
+      *reinterpret_cast<float2*>(dst) = acc[o];
+    } else {
+      if (base >= first && base < first + count) dst[0] = acc[o].x;
+      if (gx + 1 < W && base + 1 >= first && base + 1 < first + count) dst[1] = acc[o].y;
+    }
+  }
+}
+
+template <int F, int TO>
+constexpr size_t sep_smem_bytes() {
+  return sizeof(float) * ((TO + F - 1) * kPitch + (TO + F - 1) * kHPitch);
+}
+
+// Factorisation of the F x F filter as r[i] c[j] (see gaussian_sep), or
+// false.  The last filter seen is cached per host thread (a device thread
+// launches every package of its device), so repeated launches with the same
+// filter cost one 4 KB compare.
+struct SepCache {
+  std::vector<float> w;
+  bool ok = false;
+  std::vector<float> r, c;
+};
+
+bool factor_filter(const float* w, int F, const float** r, const float** c) {
+  thread_local SepCache cache;
+  const size_t n = static_cast<size_t>(F) * F;
+  if (cache.w.size() != n || std::memcmp(cache.w.data(), w, n * sizeof(float)) != 0) {
+    cache.w.assign(w, w + n);
+    cache.r.assign(F, 0.0f);
+    cache.c.assign(F, 0.0f);
+    cache.ok = false;
+    const int R = F / 2;
+    const double ctr = w[R * F + R];
+    if (ctr > 0.0 && std::isfinite(ctr)) {
+      const double sc = std::sqrt(ctr);
+      std::vector<double> rd(F), cd(F);
+      for (int i = 0; i < F; ++i) rd[i] = w[i * F + R] / sc;
+      for (int j = 0; j < F; ++j) cd[j] = w[R * F + j] / sc;
+      bool ok = true;
+      for (int i = 0; i < F && ok; ++i)
+        for (int j = 0; j < F && ok; ++j) {
+          const double v = static_cast<double>(w[i * F + j]), p = rd[i] * cd[j];
+          ok = std::isfinite(v) && std::fabs(v - p) <= 0x1p-20 * std::fabs(v);
+        }
+      if (ok) {
+        for (int i = 0; i < F; ++i) cache.r[i] = static_cast<float>(rd[i]);
+        for (int j = 0; j < F; ++j) cache.c[j] = static_cast<float>(cd[j]);
+        cache.ok = true;
+      }
+    }
+  }
+  *r = cache.r.data();
+  *c = cache.c.data();
+  return cache.ok;
+}
+
+template <int F, int TO>
+cudaError_t launch_sep(const GaussianParams& g, const LaunchEnv& env, const float* r, const float* c, uint64_t first,
+                       uint64_t count) {
+  SepTaps<F> taps;
+  for (int j = 0; j <= F; ++j) {
+    taps.c[j] = j < F ? c[j] : 0.0f;
+    taps.cb[j] = j + 1 < F ? c[j + 1] : 0.0f;
+  }
+  for (int i = 0; i < F; ++i) taps.r[i] = r[i];
+  constexpr size_t smem = sep_smem_bytes<F, TO>();
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(gaussian_sep<F, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (attr != cudaSuccess) return attr;
+  const int row0 = static_cast<int>(first / g.width);
+  const int row1 = static_cast<int>((first + count - 1) / g.width);
+  const dim3 grid((g.width + kTileW - 1) / kTileW, (row1 - row0 + TO) / TO);
+  gaussian_sep<F, TO><<<grid, kThreads, smem, env.stream>>>(static_cast<const float*>(env.in[0]),
+                                                        static_cast<float*>(env.out[0]), static_cast<int>(g.width),
+                                                        static_cast<int>(g.height), first, count, row0, taps);
+  return cudaGetLastError();
+}
+
 // Any odd F up to 63: one thread per output, filter from the parameter bank.
 __global__ void __launch_bounds__(kThreads)
     gaussian_generic(const float* __restrict__ img, float* __restrict__ out, int W, int H, int F, uint64_t first,
@@ -237,6 +456,31 @@ cudaError_t launch_gaussian(const KernelSpec& spec, const LaunchEnv& env, uint64
   const GaussianParams& g = spec.gauss;
   const float* w = env.in_host ? static_cast<const float*>(env.in_host[1]) : nullptr;
   if (!w) return cudaErrorInvalidValue;  // the device layer keeps the filter mirrored (host_mirrored_input)
+  // gaussian@1 (or ECL_GAUSSIAN_VARIANT=1 when the id has no @n): always the direct F x F kernel
+  static const int env_variant = [] {
+    const char* v = std::getenv("ECL_GAUSSIAN_VARIANT");
+    return v ? std::atoi(v) : 0;
+  }();
+  const int variant = spec.variant >= 0 ? spec.variant : env_variant;
+  // Pieces whose outputs go straight to host memory run the direct kernel:
+  // the end-to-end step is PCIe-bound (64 MiB each way, ~1.6 ms duplex), and
+  // measured with 2^19-item pieces it reaches that floor with the direct
+  // kernel's 23 us pieces (1.63-1.73 ms) but not with the separable kernel's
+  // 8 us pieces (2.2-2.3 ms; CUPTI shows the H2D stream idling while both
+  // D2H streams are busy).  Resident pieces take the separable kernel.
+  const float *r = nullptr, *c = nullptr;
+  if (variant != 1 && !env.host_copies && (g.filter == 31 || g.filter == 15) && factor_filter(w, static_cast<int>(g.filter), &r, &c)) {
+    // ECL_GAUSSIAN_TILE_ROWS: output rows per separable tile; measured at
+    // 4096^2: 32 rows (5 CTAs/SM) 78 us, 64 rows (3 CTAs/SM, 1.47x instead of
+    // 1.94x horizontal rows per output row) 72 us
+    static const int tall = [] {
+      const char* v = std::getenv("ECL_GAUSSIAN_TILE_ROWS");
+      return v ? std::atoi(v) : 64;
+    }();
+    if (g.filter == 31) return tall == 64 ? launch_sep<31, 64>(g, env, r, c, first, count)
+                                          : launch_sep<31, 32>(g, env, r, c, first, count);
+    return launch_sep<15, 32>(g, env, r, c, first, count);
+  }
   switch (g.filter) {
     case 3: return launch_tiled<3>(g, env, w, first, count);
     case 5: return launch_tiled<5>(g, env, w, first, count);

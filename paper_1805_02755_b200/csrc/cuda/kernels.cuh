@@ -93,6 +93,8 @@ struct LaunchEnv {
   // Host mirrors of the inputs host_mirrored_input() names (nullptr for the
   // others): small inputs a launcher passes by value in its parameters.
   const void* const* in_host = nullptr;
+  // The piece's outputs are copied to host memory right after it (e2e runs).
+  bool host_copies = false;
 };
 
 // Device scratch a kernel needs per binding (e.g. Mandelbrot coordinate tables),

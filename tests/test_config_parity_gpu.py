@@ -214,14 +214,26 @@ def separable_f64(img, w, h, f, sigma):
     return sum(g[i] * rp[i:i + h, :] for i in range(f)).ravel()
 
 
-def test_gaussian_config_full_image(gpu_available, oracle):
+def run_gaussian(e, img, filt, out, resident):
+    """host: outputs copied to host buffers in the run (the engine's pieces
+    then take the direct F x F kernel); resident: outputs stay in the device
+    partitions (the separable kernel) and are gathered afterwards."""
+    if resident:
+        t = e.run_into([img, filt], None)
+        e.gather([out])
+        return t
+    return e.run_into([img, filt], [out])
+
+
+@pytest.mark.parametrize("resident", [False, True], ids=["host", "resident"])
+def test_gaussian_config_full_image(gpu_available, oracle, resident):
     w = h = 4096
     f = 31
     img, filt = W.gaussian_inputs(w, h, f, seed=42)
     prog = P.validate_program(W.gaussian_spec(w, h, f))
     out = np.empty(w * h, np.float32)
     with P.Engine(P.EngineConfig(devices(1), P.StaticConfig()), prog) as e:
-        e.run_into([img, filt], [out])
+        run_gaussian(e, img, filt, out, resident)
     exp = oracle.gaussian(img, filt, w, h, f)
     err = rel_err(out, exp)
     assert err.max() <= 1e-5, f"max rel err {err.max():.2e} at pixel {err.argmax()}"
@@ -229,7 +241,8 @@ def test_gaussian_config_full_image(gpu_available, oracle):
     assert ind.max() <= 1e-5, f"vs f64 separable: {ind.max():.2e}"
 
 
-def test_gaussian_config_co_executed(gpu_available, oracle):
+@pytest.mark.parametrize("resident", [False, True], ids=["host", "resident"])
+def test_gaussian_config_co_executed(gpu_available, oracle, resident):
     """The same image split by HGuided over 3 devices: bands start mid-row and
     every seam reads its neighbours' halo rows from the device's replica."""
     w = h = 4096
@@ -238,7 +251,7 @@ def test_gaussian_config_co_executed(gpu_available, oracle):
     prog = P.validate_program(W.gaussian_spec(w, h, f))
     out = np.empty(w * h, np.float32)
     with P.Engine(P.EngineConfig(devices(3), P.HGuidedConfig()), prog) as e:
-        t = e.run_into([img, filt], [out])
+        t = run_gaussian(e, img, filt, out, resident)
     assert len(t.packages) > 3
     rows = set()
     for p in t.packages:
@@ -280,3 +293,39 @@ def test_gaussian_engines_on_one_gpu_concurrently(gpu_available, oracle):
     for x in th:
         x.join()
     assert not errs, errs
+
+
+# ---- Gaussian separable path (rank-1 filters) -----------------------------------
+
+def rank1_filter(f, seed):
+    rng = np.random.default_rng(seed)
+    r, c = rng.uniform(0.2, 1.0, f), rng.uniform(0.2, 1.0, f)
+    w = np.outer(r, c)
+    return (w / w.sum()).astype(np.float32).ravel()
+
+
+@pytest.mark.parametrize("w,h,f,kind", [
+    (4096, 256, 31, "gaussian"), (1000, 333, 31, "rank1"), (640, 200, 15, "gaussian"), (96, 70, 31, "rank1"),
+    (1024, 130, 31, "dense"), (4096, 96, 15, "dense"), (129, 64, 31, "gaussian"),
+])
+def test_gaussian_separable_path(gpu_available, oracle, w, h, f, kind):
+    """Resident runs factor the filter: rank-1 filters (Gaussian or any outer
+    product) take the separable kernel, any other filter the direct one —
+    both within 1e-5 of the oracle's direct sum, on images whose tiles are
+    all border tiles (96x70) or partially so, over co-executed packages."""
+    img, gfilt = W.gaussian_inputs(w, h, f, seed=w + h)
+    if kind == "gaussian":
+        filt = gfilt
+    elif kind == "rank1":
+        filt = rank1_filter(f, seed=h)
+    else:  # not separable
+        filt = np.random.default_rng(f).uniform(0.0, 1.0, f * f).astype(np.float32)
+        filt /= filt.sum(dtype=np.float64)
+    import math
+    prog = P.validate_program(W.gaussian_spec(w, h, f, lws=math.gcd(w * h, 64)))
+    out = np.empty(w * h, np.float32)
+    with P.Engine(P.EngineConfig(devices(2), P.DynamicConfig(7)), prog) as e:
+        t = run_gaussian(e, img, filt, out, True)
+    assert P.tiles_exactly(t.packages, prog.total_work_groups())
+    exp = oracle.gaussian(img, filt, w, h, f)
+    assert rel_err(out, exp).max() <= 1e-5
