@@ -608,7 +608,7 @@ def ncu_traffic(workload):
             t = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
             return t, (f"dram__bytes_read.sum + dram__bytes_write.sum of one captured launch "
                        f"({r['gpu__time_duration.sum']}) of {NCU_KERNEL[workload]}, bytes per launch "
-                       f"(profiles/r2/ncu_summary.json; compute-bound: the bytes are the launch's outputs)")
+                       f"(profiles/r2/ncu_summary.json)")
     return None, "kernel not in the committed ncu capture"
 
 
