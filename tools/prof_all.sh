@@ -9,7 +9,7 @@ cap() {  # workload kernel-regex extra-args
   echo "$1 ncu rc=$?"
 }
 cap mandelbrot mandel_persistent
-cap gaussian gaussian_tiled
+cap gaussian gaussian_sep
 cap binomial binomial_hw
 cap nbody nbody_step "--steps-override 1"
 cap ray ray_persistent
