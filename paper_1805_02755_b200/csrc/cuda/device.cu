@@ -1100,12 +1100,24 @@ int ecl_gpu_wait(ecl_gpu* g, uint64_t seq) {
   return ECL_OK;
 }
 
+// Completion wait of a package's kernels: poll the event for a short while
+// before blocking.  A blocking wait wakes the device thread ~5 us after the
+// kernel ends (measured with CUPTI on a 72 us Gaussian step); polling costs
+// one host core for at most ~0.5 ms per package, then falls back.
+static cudaError_t await_event(cudaEvent_t ev) {
+  for (int i = 0; i < 1500; ++i) {
+    const cudaError_t q = cudaEventQuery(ev);
+    if (q != cudaErrorNotReady) return q;
+  }
+  return cudaEventSynchronize(ev);
+}
+
 int ecl_gpu_wait_compute(ecl_gpu* g, uint64_t seq) {
   Slot* sp = find_slot(g, seq);
   if (!sp) return fail(ECL_CONFIG_ERROR, "wait_compute: unknown package");
   if (int rc = set_device(g)) return rc;
-  ECL_CK(cudaEventSynchronize(sp->end));
-  if (sp->two_lanes) ECL_CK(cudaEventSynchronize(sp->end2));
+  ECL_CK(await_event(sp->end));
+  if (sp->two_lanes) ECL_CK(await_event(sp->end2));
   return ECL_OK;
 }
 
