@@ -17,7 +17,8 @@
  * partition.  Each ecl_gpu is driven by exactly one host thread.  Completion
  * is observed through events (ecl_gpu_wait_compute / ecl_gpu_wait /
  * ecl_gpu_poll); the per-package host callback of ecl_gpu_submit is optional
- * (the engine passes none and blocks on the kernel-end events).
+ * (the engine passes none and waits on the kernel-end events: a short poll,
+ * then a blocking synchronize).
  *
  * Status codes: ECL_OK (0) or the negated coexec::ErrorCode + 1 (error.hpp:11-39
  * order), so a caller maps them 1:1 onto coexec::Error; device faults map to
