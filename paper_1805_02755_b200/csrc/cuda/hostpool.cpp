@@ -55,8 +55,13 @@ class Pool {
   Pool() {
     // Leave two cores for the engine's device threads and CUDA's own threads:
     // a descheduled widen worker stalls its piece for a whole time slice.
+    // Under torchrun (one process per GPU, LOCAL_WORLD_SIZE processes on the
+    // host) the cores are shared: each process takes its share after two
+    // cores per process for device threads.
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    unsigned n = hw > 4 ? hw - 2 : hw;
+    unsigned lw = 1;
+    if (const char* v = std::getenv("LOCAL_WORLD_SIZE"); v && std::atoi(v) > 1) lw = static_cast<unsigned>(std::atoi(v));
+    unsigned n = hw > 2 * lw + 2 ? (hw - 2 * lw) / lw : std::max(1u, hw / lw);
     if (const char* v = std::getenv("ECL_WIDEN_THREADS"); v && std::atoi(v) > 0) n = static_cast<unsigned>(std::atoi(v));
     for (unsigned i = 0; i < n; ++i) threads_.emplace_back([this] { loop(); });
   }
