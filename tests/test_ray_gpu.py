@@ -57,3 +57,23 @@ def test_ray_variants_bit_exact(gpu_available, oracle, kernel):
         res = e.run([scene])
     exp, _ = oracle.ray(scene, ns, w, h, 4)
     assert np.array_equal(res.outputs[0].view(np.float32).reshape(-1, 4), exp)
+
+
+@pytest.mark.parametrize("w,h,n_dev,sched", [
+    (1600, 1400, 1, P.StaticConfig()),        # 2.24M pixels: three 2^20-pixel two-lane pieces
+    (2048, 1536, 2, P.HGuidedConfig()),       # pieces inside co-executed packages
+])
+def test_ray_resident_two_lane_pieces(gpu_available, oracle, w, h, n_dev, sched):
+    """Device-resident runs cut Ray's packages into 2^20-pixel launches that
+    alternate over the device's two compute lanes (compute_split_items);
+    the gathered image is still the oracle's, bit for bit."""
+    ns, depth = 64, 4
+    scene = W.ray_scene(ns, seed=9)
+    prog = P.validate_program(W.ray_spec(w, h, ns, depth))
+    out = np.empty((w * h, 4), np.float32)
+    with P.Engine(P.EngineConfig(devices(n_dev), sched), prog) as e:
+        t = e.run_into([scene], None)
+        e.gather([out])
+    assert P.tiles_exactly(t.packages, prog.total_work_groups())
+    exp, _ = oracle.ray(scene, ns, w, h, depth)
+    assert np.array_equal(out.view(np.uint32), exp.view(np.uint32))
