@@ -215,52 +215,21 @@ struct SepTaps {
 
 constexpr int kHPitch = 68;  // horizontal-pass buffer pitch (floats): rows of 64 + 4 (bank spread)
 
-// One 64x32 output tile per CTA (41.7 KB of shared memory at F = 31: 5
-// CTAs per SM, so the hardware overlaps one CTA's TMA rows with the others'
+// One 64 x TO output tile per CTA (TO = 64: 63 KB of shared memory, 3 CTAs
+// per SM; the hardware overlaps one CTA's TMA rows with the others'
 // passes).  Measured and dropped: persistent CTAs with the input tile
-// double-buffered (prefetch of tile k+1 during tile k) fit 3 CTAs per SM
-// and ran 98 us against 79.
+// double-buffered (prefetch of tile k+1 during tile k): 98 us with 32-row
+// tiles, 105 us with 64-row tiles, against 79 and 72 us.
+// The two passes of the separable kernel on one staged tile (all threads).
 template <int F, int TO>
-__global__ void __launch_bounds__(kThreads)
-    gaussian_sep(const float* __restrict__ img, float* __restrict__ out, int W, int H, uint64_t first, uint64_t count,
-                 int row0, const __grid_constant__ SepTaps<F> taps) {
+__device__ __forceinline__ void sep_hpass(const float* __restrict__ tile, float* __restrict__ hbuf,
+                                          const SepTaps<F>& taps) {
   constexpr int R = F / 2;
-  constexpr int TH = TO + F - 1;  // staged rows (TO output rows per tile)
+  constexpr int TH = TO + F - 1;
   constexpr int NV = 8 + F - 1;
   constexpr int SHIFT = (4 - R % 4) % 4;
   constexpr int NL = (SHIFT + NV + 3) / 4;
   constexpr int NP = (F - 1) / 2;
-  extern __shared__ __align__(128) float sep_smem[];
-  float* const tile = sep_smem;
-  float* const hbuf = sep_smem + TH * kPitch;
-  __shared__ __align__(8) uint64_t bar;
-
-  const int tile_x = blockIdx.x * kTileW;
-  const int tile_y = row0 + blockIdx.y * TO;
-  const bool interior = tile_x >= 16 && tile_x + kTileW + 16 <= W && tile_y - R >= 0 && tile_y + TO + R <= H &&
-                        (W & 3) == 0;
-  if (interior) {
-    if (threadIdx.x == 0) {
-      mbar_init(&bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) mbar_expect_tx(&bar, TH * 96 * 4);
-    __syncthreads();
-    if (threadIdx.x < TH) {
-      const int gy = tile_y - R + threadIdx.x;
-      bulk_g2s(&tile[threadIdx.x * kPitch], img + static_cast<int64_t>(gy) * W + (tile_x - 16), 96 * 4, &bar);
-    }
-    mbar_wait(&bar, 0);
-  } else {
-    for (int k = threadIdx.x; k < TH * 96; k += kThreads) {
-      const int r = k / 96, c = k - r * 96;
-      const int gy = clampi(tile_y - R + r, 0, H - 1), gx = clampi(tile_x - 16 + c, 0, W - 1);
-      tile[r * kPitch + c] = img[static_cast<int64_t>(gy) * W + gx];
-    }
-    __syncthreads();
-  }
-
   // Horizontal pass: segment (row, s) = 8 outputs hbuf[row][8s .. 8s+7].
   // The 8 lanes of an LDS.128 phase take 8 consecutive rows of one segment
   // column: the 100-float tile pitch and the 68-float buffer pitch put them
@@ -299,8 +268,12 @@ __global__ void __launch_bounds__(kThreads)
     dst[0] = make_float4(acc[0].x + acc[0].y, acc[1].x + acc[1].y, acc[2].x + acc[2].y, acc[3].x + acc[3].y);
     dst[1] = make_float4(acc[4].x + acc[4].y, acc[5].x + acc[5].y, acc[6].x + acc[6].y, acc[7].x + acc[7].y);
   }
-  __syncthreads();
+}
 
+template <int F, int TO>
+__device__ __forceinline__ void sep_vpass(const float* __restrict__ hbuf, float* __restrict__ out, int W, int H,
+                                          uint64_t first, uint64_t count, int tile_x, int tile_y,
+                                          const SepTaps<F>& taps) {
   // Vertical pass: lane = column pair (64 columns per warp), warp = 4 output
   // rows.  A thread slides down its column pair through 4 + F - 1 buffer
   // rows (one LDS.64 each) and feeds every output row the tap it owes —
@@ -336,6 +309,48 @@ __global__ void __launch_bounds__(kThreads)
       if (gx + 1 < W && base + 1 >= first && base + 1 < first + count) dst[1] = acc[o].y;
     }
   }
+}
+
+template <int F, int TO>
+__global__ void __launch_bounds__(kThreads)
+    gaussian_sep(const float* __restrict__ img, float* __restrict__ out, int W, int H, uint64_t first, uint64_t count,
+                 int row0, const __grid_constant__ SepTaps<F> taps) {
+  constexpr int R = F / 2;
+  constexpr int TH = TO + F - 1;  // staged rows (TO output rows per tile)
+  extern __shared__ __align__(128) float sep_smem[];
+  float* const tile = sep_smem;
+  float* const hbuf = sep_smem + TH * kPitch;
+  __shared__ __align__(8) uint64_t bar;
+
+  const int tile_x = blockIdx.x * kTileW;
+  const int tile_y = row0 + blockIdx.y * TO;
+  const bool interior = tile_x >= 16 && tile_x + kTileW + 16 <= W && tile_y - R >= 0 && tile_y + TO + R <= H &&
+                        (W & 3) == 0;
+  if (interior) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) mbar_expect_tx(&bar, TH * 96 * 4);
+    __syncthreads();
+    if (threadIdx.x < TH) {
+      const int gy = tile_y - R + threadIdx.x;
+      bulk_g2s(&tile[threadIdx.x * kPitch], img + static_cast<int64_t>(gy) * W + (tile_x - 16), 96 * 4, &bar);
+    }
+    mbar_wait(&bar, 0);
+  } else {
+    for (int k = threadIdx.x; k < TH * 96; k += kThreads) {
+      const int r = k / 96, c = k - r * 96;
+      const int gy = clampi(tile_y - R + r, 0, H - 1), gx = clampi(tile_x - 16 + c, 0, W - 1);
+      tile[r * kPitch + c] = img[static_cast<int64_t>(gy) * W + gx];
+    }
+    __syncthreads();
+  }
+
+  sep_hpass<F, TO>(tile, hbuf, taps);
+  __syncthreads();
+  sep_vpass<F, TO>(hbuf, out, W, H, first, count, tile_x, tile_y, taps);
 }
 
 template <int F, int TO>
