@@ -230,8 +230,9 @@ int ecl_gpu_set_copy_split(ecl_gpu* gpu, uint64_t items);
  * bytes against host-DRAM traffic (default 8 = all widened). */
 int ecl_gpu_set_widen_fraction(ecl_gpu* gpu, uint32_t per_8);
 
-/* Kernel time of the most recent submit() / native_run() launches summed
- * since the last reset (for roofline accounting). */
+/* Package kernel time (CUDA events, summed over packages) and the number of
+ * kernel launches (every piece of every package, and native runs) since the
+ * last reset (for roofline accounting and the bench's gpu_launches). */
 int ecl_gpu_kernel_time(ecl_gpu* gpu, double* total_ms, uint64_t* launches, int reset);
 
 /* Measured vector peaks of device `ordinal` (roofline denominators for the

@@ -985,6 +985,7 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
     }
     cudaError_t e = ecl::launch_kernel(s, env, first, count);
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+    g->launches += 1;  // every kernel launch (a package may run as several pieces)
     if (g->tally_on) {
       e = ecl::launch_tally(g->tally, first, count, st);
       if (e != cudaSuccess) return cuda_fail(e, "tally launch");
@@ -1066,7 +1067,6 @@ int ecl_gpu_package_times(ecl_gpu* g, uint64_t seq, double* t_start, double* t_e
   *t_end = g->epoch_host_ms + b;
   if (!slot.timed) {
     g->kernel_ms += k;
-    g->launches += 1;
     slot.timed = true;
   }
   slot.busy = false;

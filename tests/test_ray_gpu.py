@@ -72,8 +72,12 @@ def test_ray_resident_two_lane_pieces(gpu_available, oracle, w, h, n_dev, sched)
     prog = P.validate_program(W.ray_spec(w, h, ns, depth))
     out = np.empty((w * h, 4), np.float32)
     with P.Engine(P.EngineConfig(devices(n_dev), sched), prog) as e:
+        e.kernel_timing(reset=True)
         t = e.run_into([scene], None)
+        _, launches = e.kernel_timing(reset=True)
         e.gather([out])
     assert P.tiles_exactly(t.packages, prog.total_work_groups())
+    # every piece is counted as a launch: at least one per 2^20 pixels
+    assert launches >= max(len(t.packages), -(-w * h // (1 << 20)))
     exp, _ = oracle.ray(scene, ns, w, h, depth)
     assert np.array_equal(out.view(np.uint32), exp.view(np.uint32))
