@@ -948,8 +948,9 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
   uint64_t piece_wg = size_wg;
   bool streaming = false;
   for (const char* p : g->pending_in) streaming = streaming || p != nullptr;
-  const uint64_t split_items = (copies || streaming) ? g->d2h_split_items
-                                : (g->lanes > 1 ? s.compute_split_items : 0);
+  const uint64_t compute_split = g->lanes > 1 ? s.compute_split_items : 0;
+  const uint64_t split_items = copies ? g->d2h_split_items
+                                      : (compute_split ? compute_split : (streaming ? g->d2h_split_items : 0));
   if (split_items > 0) {
     piece_wg = std::max<uint64_t>(1, split_items / s.lws);
     uint64_t po = 0, pc = 0;
