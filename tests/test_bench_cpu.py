@@ -102,3 +102,36 @@ def test_reference_arm_loads_no_product_code(tmp_path):
     assert probe == {"rc": 0, "imported": [], "libs": []}
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["config"]["work_items_per_step"] == 4096 * 4096
+
+
+def test_binomial_zero_skip_ceiling_matches_a_brute_force_count():
+    # the closed form steps(steps+1)/2 - t0(t0-1)/2 of nonzero node updates
+    # against a direct count on the lattice of a few options
+    wl = bench.WORKLOADS["binomial"](P, W, np)
+    n = wl.STEPS
+    rv = W.binomial_inputs(64, seed=3)[0].astype(np.float64)
+    S, K, T = 5 * (1 - rv) + 30 * rv, 1 * (1 - rv) + 100 * rv, 0.25 * (1 - rv) + 10 * rv
+    v = 0.30 * np.sqrt(T / n)
+    t = np.arange(n + 1)
+    for o in range(len(rv)):
+        leaf = S[o] * np.exp(v[o] * (2 * t - n)) - K[o]
+        nz = (leaf > 0).astype(int)
+        count = 0
+        for j in range(n, 0, -1):  # level j-1 computed from level j: nodes 0..j-1
+            nz = np.maximum(nz[:-1], nz[1:])
+            count += int(nz.sum())
+        t0 = int((leaf <= 0).sum())
+        assert count == n * (n + 1) // 2 - t0 * (t0 - 1) // 2
+    c, why = wl.skip_ceiling()
+    assert 1.33 < c < 3.0 and "nonzero" in why.lower()
+
+
+def test_gaussian_roofline_is_hbm_with_both_flop_counts():
+    wl = bench.WORKLOADS["gaussian"](P, W, np)
+    ro = wl.roofline_override(0.1, 1, 70.0)
+    px = wl.WIDTH * wl.HEIGHT
+    assert ro["bound"] == "hbm" and ro["unit"] == "GB/s"
+    assert ro["achieved"] == pytest.approx(8.0 * px / 1e-4 / 1e9)
+    assert ro["frac"] == pytest.approx(ro["achieved"] / ro["peak"])
+    assert ro["separable_fp32"]["flops_per_step"] == 4.0 * wl.F * px
+    assert ro["direct_form"]["flops_per_step"] == wl.flops() == 2.0 * wl.F ** 2 * px
