@@ -773,9 +773,6 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
         sched.k = args.k
         sched.adaptive = args.adaptive
     prog = P.validate_program(wl.spec())
-    if shared and wl.steps_per_run > 1:
-        raise SystemExit(f"{wl.name}: iterative runs exchange state over NVLink from one process; "
-                         "run without torchrun (--gpus N)")
     eng_shared = {k: v for k, v in shared.items() if k != "host_buffer"} if shared else None
     eng = P.Engine(P.EngineConfig(devs, sched, shared=eng_shared), prog)
     stream = torch.cuda.current_stream()

@@ -209,6 +209,21 @@ int ecl_gpu_sync(ecl_gpu* gpu);
 int ecl_gpu_enable_tally(ecl_gpu* gpu, int enable);
 int ecl_gpu_download_tally(ecl_gpu* gpu, uint32_t* host_counts);
 
+/* ---- cross-process exchange (one process per GPU) ----------------------- */
+/* CUDA IPC for iterative programs driven by several processes: a process
+ * exports its bound buffers (64-byte handles), its peers import them once
+ * and pull the owner slices of each step into their own partition (NVLink
+ * peer copies between GPUs; on one GPU, device copies between contexts). */
+#define ECL_IPC_HANDLE_BYTES 64
+int ecl_gpu_export_buffer(ecl_gpu* gpu, int is_output, uint32_t index, void* handle);
+int ecl_gpu_import_buffer(ecl_gpu* gpu, const void* handle, void** dptr);
+int ecl_gpu_release_import(ecl_gpu* gpu, void* dptr);
+/* Copies elements [elem_offset, elem_offset + elem_count) of output `index`
+ * from `src_base` (an imported peer buffer of the same geometry) into this
+ * device's output `index`; ordered before later launches on every lane. */
+int ecl_gpu_pull_output_slice(ecl_gpu* gpu, uint32_t index, const void* src_base, uint64_t elem_offset,
+                              uint64_t elem_count);
+
 /* ---- native baseline (overhead denominator) --------- */
 /* One launch over the whole grid on the compute stream; *kernel_ms is the
  * CUDA-event time of that launch.  Synchronous. */

@@ -51,6 +51,12 @@ class SharedCoordinator {
   /// whether any rank failed.
   std::vector<Package> end_run(bool* peer_failed);
   void barrier();
+  /// Small per-rank blobs (CUDA IPC handles, device lists) exchanged through
+  /// the segment: publish writes this rank's slot; after a barrier() every
+  /// rank can fetch any rank's slot.  n <= kBlobBytes, slot < kBlobSlots.
+  static constexpr std::size_t kBlobBytes = 64, kBlobSlots = 16, kMaxRanks = 64;
+  void publish(std::uint32_t slot, const void* data, std::size_t n);
+  void fetch(std::uint32_t rank, std::uint32_t slot, void* data, std::size_t n) const;
 
   /// The run's adaptive-HGuided powers (identical on every rank: end_run
   /// replays the whole decision log first); empty if not learned.

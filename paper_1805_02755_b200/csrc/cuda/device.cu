@@ -1151,6 +1151,45 @@ int ecl_gpu_download_tally(ecl_gpu* g, uint32_t* host) {
   return ECL_OK;
 }
 
+int ecl_gpu_export_buffer(ecl_gpu* g, int is_output, uint32_t index, void* handle) {
+  if (!g->spec) return fail(ECL_CONFIG_ERROR, "export before bind");
+  const auto& bufs = is_output ? g->out : g->in;
+  if (index >= bufs.size()) return fail(ECL_CONFIG_ERROR, "export: buffer index out of range");
+  if (int rc = set_device(g)) return rc;
+  static_assert(sizeof(cudaIpcMemHandle_t) == ECL_IPC_HANDLE_BYTES, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  ECL_CK(cudaIpcGetMemHandle(&h, bufs[index]));
+  std::memcpy(handle, &h, sizeof(h));
+  return ECL_OK;
+}
+
+int ecl_gpu_import_buffer(ecl_gpu* g, const void* handle, void** dptr) {
+  if (int rc = set_device(g)) return rc;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  ECL_CK(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return ECL_OK;
+}
+
+int ecl_gpu_release_import(ecl_gpu* g, void* dptr) {
+  if (int rc = set_device(g)) return rc;
+  ECL_CK(cudaIpcCloseMemHandle(dptr));
+  return ECL_OK;
+}
+
+int ecl_gpu_pull_output_slice(ecl_gpu* g, uint32_t index, const void* src_base, uint64_t elem_offset,
+                              uint64_t elem_count) {
+  if (!g->spec || index >= g->out.size()) return fail(ECL_CONFIG_ERROR, "pull: output index out of range");
+  const uint64_t esz = g->spec->outputs[index].element_size_bytes;
+  if ((elem_offset + elem_count) * esz > g->out_bytes[index]) return fail(ECL_CONFIG_ERROR, "pull: slice out of range");
+  if (int rc = set_device(g)) return rc;
+  if (int rc = join_lanes(g)) return rc;
+  ECL_CK(cudaMemcpyAsync(static_cast<char*>(g->out[index]) + elem_offset * esz,
+                         static_cast<const char*>(src_base) + elem_offset * esz, elem_count * esz, cudaMemcpyDefault,
+                         g->lane[0]));
+  return fan_out_lane0(g);
+}
+
 int ecl_gpu_native_run(ecl_gpu* g, float* kernel_ms) {
   if (!g->spec) return fail(ECL_CONFIG_ERROR, "native run before bind");
   if (int rc = set_device(g)) return rc;

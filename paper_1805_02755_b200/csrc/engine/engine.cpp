@@ -18,6 +18,8 @@
 // caller, so the product never evaluates kernels on the CPU.
 #include "coexec/engine.hpp"
 
+#include <array>
+
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -521,14 +523,71 @@ struct Engine::Impl {
   // other GPU over NVLink (the per-step allgatherv of the new state) and each
   // device swaps input i with output o in place.  Final outputs are gathered
   // from the owners of the last step's packages.
+  // Cross-process state of an iterative run (one process per GPU): every
+  // process exports the two allocations of each swapped (input, output)
+  // pair of its device — they trade roles every step — and imports its
+  // peers' through CUDA IPC, so a step's owner slices can be pulled from
+  // the owner's output.  Slot 0 of each rank's blob: its device indices.
+  struct PeerBuffers {
+    Impl* eng = nullptr;
+    std::vector<int> rank_of;                              // device index -> rank
+    std::vector<std::vector<std::array<void*, 2>>> bufs;  // [rank][swap] = {output at even steps, at odd}
+    void open(Impl& e, std::span<const std::pair<std::uint32_t, std::uint32_t>> swaps) {
+      eng = &e;
+      SharedCoordinator& sh = *e.shared;
+      const std::uint32_t me = sh.config().rank, world = sh.config().world;
+      if (e.devices.size() != 1)
+        throw Error(ErrorCode::ConfigError, "run_steps across processes: each process drives exactly one device");
+      std::uint32_t local[16] = {};
+      local[0] = 1;
+      local[1] = e.devices[0]->index;
+      sh.publish(0, local, sizeof(local));
+      for (std::size_t sw = 0; sw < swaps.size(); ++sw) {
+        unsigned char h[ECL_IPC_HANDLE_BYTES];
+        check(ecl_gpu_export_buffer(e.devices[0]->gpu, 1, swaps[sw].second, h), "export");
+        sh.publish(static_cast<std::uint32_t>(1 + 2 * sw), h, sizeof(h));
+        check(ecl_gpu_export_buffer(e.devices[0]->gpu, 0, swaps[sw].first, h), "export");
+        sh.publish(static_cast<std::uint32_t>(2 + 2 * sw), h, sizeof(h));
+      }
+      sh.barrier();
+      rank_of.assign(e.cfg.devices.size(), -1);
+      bufs.assign(world, {});
+      for (std::uint32_t r = 0; r < world; ++r) {
+        std::uint32_t dev[16];
+        sh.fetch(r, 0, dev, sizeof(dev));
+        for (std::uint32_t j = 0; j < dev[0] && j < 15; ++j)
+          if (dev[1 + j] < rank_of.size()) rank_of[dev[1 + j]] = static_cast<int>(r);
+        if (r == me) continue;
+        bufs[r].assign(swaps.size(), {nullptr, nullptr});
+        for (std::size_t sw = 0; sw < swaps.size(); ++sw)
+          for (int half = 0; half < 2; ++half) {
+            unsigned char h[ECL_IPC_HANDLE_BYTES];
+            sh.fetch(r, static_cast<std::uint32_t>(1 + 2 * sw + half), h, sizeof(h));
+            check(ecl_gpu_import_buffer(e.devices[0]->gpu, h, &bufs[r][sw][half]), "import");
+          }
+      }
+    }
+    const void* output_of(std::uint32_t device, std::size_t sw, std::uint32_t step) const {
+      const int r = device < rank_of.size() ? rank_of[device] : -1;
+      if (r < 0 || bufs[r].empty()) throw Error(ErrorCode::ConfigError, "run_steps: no process owns device " +
+                                                                           std::to_string(device));
+      return bufs[r][sw][step & 1u];
+    }
+    ~PeerBuffers() {
+      if (!eng) return;
+      for (auto& per_rank : bufs)
+        for (auto& pair : per_rank)
+          for (void* p : pair)
+            if (p) (void)ecl_gpu_release_import(eng->devices[0]->gpu, p);
+    }
+  };
+
   ExecutionTrace run_steps(std::span<const void* const> inputs, std::span<void* const> outputs, std::uint32_t steps,
                            std::span<const std::pair<std::uint32_t, std::uint32_t>> swaps) {
     const ProgramSpec& s = prog.spec();
     if (steps == 0) throw Error(ErrorCode::ConfigError, "run_steps needs at least one step");
-    if (shared)
-      throw Error(ErrorCode::ConfigError,
-                  "run_steps exchanges state between GPUs over NVLink peer copies: drive every device from one "
-                  "process (no cfg.shared)");
+    if (shared && 1 + 2 * swaps.size() > SharedCoordinator::kBlobSlots)
+      throw Error(ErrorCode::ConfigError, "run_steps: too many swap pairs for the cross-process exchange");
     check_inputs(inputs);
     for (const auto& [i, o] : swaps)
       if (i >= s.in_buffers.size() || o >= s.out_buffers.size() ||
@@ -537,6 +596,8 @@ struct Engine::Impl {
     const bool tally = begin_run(inputs);
     std::vector<ecl_gpu*> g = gpus();
     std::vector<Package> all, step;
+    PeerBuffers peers;
+    if (shared && steps > 1) peers.open(*this, swaps);
     for (std::uint32_t k = 0; k < steps; ++k) {
       if (tally && k > 0)
         for (auto& d : devices) check(ecl_gpu_enable_tally(d->gpu, 1), "tally");
@@ -548,16 +609,33 @@ struct Engine::Impl {
       }
       inputs_streaming = false;  // streamed up during the first step
       if (k + 1 < steps) {
-        if (g.size() > 1)
-          for (const Package& p : step) {
-            const OutRange r = out_range_for(p, prog);
-            for (const auto& [i, o] : swaps)
-              check(ecl_broadcast_output_slice(g.data(), static_cast<std::uint32_t>(g.size()), p.device_index, o,
-                                               r.offset, r.count),
-                    "exchange");
+        for (const Package& p : step) {
+          const OutRange r = out_range_for(p, prog);
+          const int slot = local_slot(p.device_index);
+          if (slot >= 0) {
+            // owner drives it here: NVLink peer copies to this process's other devices
+            if (g.size() > 1)
+              for (const auto& [i, o] : swaps)
+                check(ecl_broadcast_output_slice(g.data(), static_cast<std::uint32_t>(g.size()),
+                                                 static_cast<std::uint32_t>(slot), o, r.offset, r.count),
+                      "exchange");
+          } else {
+            // a peer process owns it: every local device pulls the slice from
+            // the owner's (IPC-imported) output of this step
+            for (std::size_t sw = 0; sw < swaps.size(); ++sw)
+              for (auto& d : devices)
+                check(ecl_gpu_pull_output_slice(d->gpu, swaps[sw].second, peers.output_of(p.device_index, sw, k),
+                                                r.offset, r.count),
+                      "pull");
           }
+        }
         for (auto& d : devices)
           for (const auto& [i, o] : swaps) check(ecl_gpu_swap_io(d->gpu, i, o), "swap");
+        if (shared) {
+          // pulls complete before any peer overwrites the buffers they read
+          for (auto& d : devices) check(ecl_gpu_sync(d->gpu), "sync");
+          shared->barrier();
+        }
       }
       all.insert(all.end(), step.begin(), step.end());
     }

@@ -70,10 +70,12 @@ struct SharedCoordinator::Region {
   std::uint64_t n_done;
   LogEntry log[kMaxLog];
   DoneRec done[kMaxLog];
+  unsigned char blobs[SharedCoordinator::kMaxRanks][SharedCoordinator::kBlobSlots][SharedCoordinator::kBlobBytes];
 };
 
 SharedCoordinator::SharedCoordinator(SharedConfig cfg) : cfg_(std::move(cfg)) {
-  if (cfg_.world < 1 || cfg_.rank >= cfg_.world) throw Error(ErrorCode::ConfigError, "shared: bad rank/world");
+  if (cfg_.world < 1 || cfg_.rank >= cfg_.world || cfg_.world > kMaxRanks)
+    throw Error(ErrorCode::ConfigError, "shared: bad rank/world");
   if (cfg_.name.empty() || cfg_.name[0] != '/') throw Error(ErrorCode::ConfigError, "shared: name must start with '/'");
   bytes_ = sizeof(Region);
   int fd = -1;
@@ -232,6 +234,19 @@ std::vector<Package> SharedCoordinator::end_run(bool* peer_failed) {
   }
   std::sort(out.begin(), out.end(), [](const Package& a, const Package& b) { return a.seq < b.seq; });
   return out;
+}
+
+void SharedCoordinator::publish(std::uint32_t slot, const void* data, std::size_t n) {
+  if (slot >= kBlobSlots || n > kBlobBytes) throw Error(ErrorCode::ConfigError, "shared: blob slot/size out of range");
+  Lock lock(&region_->mu);
+  std::memcpy(region_->blobs[cfg_.rank][slot], data, n);
+}
+
+void SharedCoordinator::fetch(std::uint32_t rank, std::uint32_t slot, void* data, std::size_t n) const {
+  if (rank >= cfg_.world || slot >= kBlobSlots || n > kBlobBytes)
+    throw Error(ErrorCode::ConfigError, "shared: blob rank/slot/size out of range");
+  Lock lock(&region_->mu);
+  std::memcpy(data, region_->blobs[rank][slot], n);
 }
 
 std::uint64_t SharedCoordinator::remaining() const {
