@@ -754,11 +754,40 @@ def run_ours(args, world, rank, local):
 
     wl = WORKLOADS[args.workload](P, W, np)
     line = bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, rank)
+    if not dist and n == 1 and args.workload == "mandelbrot" and not args.no_other_workloads:
+        # the other BASELINE configs, measured in the same run so the driver's
+        # own bench record carries them (compact: no CPU baseline, NBody with
+        # two timed 10-step runs)
+        line["other_workloads"] = {}
+        for name in ("ray", "binomial", "gaussian", "nbody"):
+            sub = argparse.Namespace(**vars(args))
+            sub.workload, sub.no_cpu_baseline, sub.copy_split, sub.min_package = name, True, 0, 0
+            if name == "nbody":
+                sub.steps = min(sub.steps, 2)
+            w2 = WORKLOADS[name](P, W, np)
+            full = bench_engine(sub, n, w2, P, N, np, torch, barrier, max_over_ranks, shared, rank)
+            line["other_workloads"][name] = compact_line(full)
     if dist:
         torch.distributed.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
+
+
+def compact_line(full):
+    """The fields of a workload's bench line that summarise it inside another
+    line (other_workloads)."""
+    r, c = full["roofline"], full["coexec"]
+    keep_r = ("bound", "achieved", "peak", "unit", "frac", "ceiling_frac", "frac_of_ceiling", "skip_ceiling_frac",
+              "frac_of_skip_ceiling")
+    return {"workload": full["config"]["workload"], "value": full["value"], "unit": full["unit"],
+            "ms_per_step": full["ms_per_step"], "steps": full["steps"], "warmup": full["warmup"],
+            "dtype": full["dtype"], "e2e": {k: full["e2e"][k] for k in ("value", "ms_per_step")},
+            "step_ms": full.get("step_ms"), "roofline": {k: r[k] for k in keep_r if k in r},
+            "coexec": {k: c.get(k) for k in ("native_kernel_ms", "overhead_pct_device", "packages_per_step",
+                                             "outputs_sane")},
+            "gpu_launches": full["gpu_launches"],
+            "clocks": {k: full["clocks"].get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons")}}
 
 
 def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, rank):
@@ -1074,6 +1103,8 @@ def main(argv=None):
                     help="work-items per sub-launch when a package copies to the host or streams its inputs up "
                          "(0: the workload's default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-workloads", action="store_true",
+                    help="default Mandelbrot run on one GPU: skip the compact lines of the other configs")
     args = ap.parse_args(argv)
     if args.impl == "ours":
         args.warmup = max(3, args.warmup)
