@@ -24,6 +24,7 @@
 // Packages are arbitrary work-item ranges: tiles cover the rows the range
 // touches and only pixels inside [first, first+count) are written.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -411,9 +412,17 @@ cudaError_t launch_sep(const GaussianParams& g, const LaunchEnv& env, const floa
   }
   for (int i = 0; i < F; ++i) taps.r[i] = r[i];
   constexpr size_t smem = sep_smem_bytes<F, TO>();
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(gaussian_sep<F, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (attr != cudaSuccess) return attr;
+  // the dynamic shared-memory limit is a per-device function attribute: set
+  // it once on every device that launches this kernel (idempotent if two
+  // device threads race)
+  static std::atomic<uint64_t> attr_set{0};
+  const uint64_t bit = uint64_t{1} << (env.device & 63);
+  if (!(attr_set.load(std::memory_order_relaxed) & bit)) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(gaussian_sep<F, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr_set.fetch_or(bit, std::memory_order_relaxed);
+  }
   const int row0 = static_cast<int>(first / g.width);
   const int row1 = static_cast<int>((first + count - 1) / g.width);
   const dim3 grid((g.width + kTileW - 1) / kTileW, (row1 - row0 + TO) / TO);
