@@ -215,6 +215,14 @@ int ecl_gpu_download_tally(ecl_gpu* gpu, uint32_t* host_counts);
  * and pull the owner slices of each step into their own partition (NVLink
  * peer copies between GPUs; on one GPU, device copies between contexts). */
 #define ECL_IPC_HANDLE_BYTES 64
+/* Fused exchange for kernels that support it (*supported = 1, NBody): the
+ * next launches also store their outputs into the given peer buffers —
+ * n_peers x n_outputs device pointers, peer-major, NULL = skip — over NVLink
+ * as they compute them, so an iterative run needs no separate per-step
+ * exchange.  n_peers = 0 clears.  Fails when a peer device is not
+ * peer-accessible from this one. */
+int ecl_gpu_peer_writes(const ecl_gpu* gpu, int* supported);
+int ecl_gpu_set_peer_outputs(ecl_gpu* gpu, void* const* ptrs, uint32_t n_peers);
 int ecl_gpu_export_buffer(ecl_gpu* gpu, int is_output, uint32_t index, void* handle);
 int ecl_gpu_import_buffer(ecl_gpu* gpu, const void* handle, void** dptr);
 int ecl_gpu_release_import(ecl_gpu* gpu, void* dptr);

@@ -116,6 +116,8 @@ struct ecl_gpu {
   bool tally_on = false;
   double kernel_ms = 0.0;
   uint64_t launches = 0;
+  std::vector<void*> peer_out;  // fused exchange: n_peers x outputs (ecl_gpu_set_peer_outputs)
+  uint32_t n_peers = 0;
   uint64_t d2h_split_items = 1ull << 23;  // sub-launch size when copies are pipelined
   uint32_t* compact_dev = nullptr;        // replicate > 1: one value per work-item (device)
   uint32_t* compact_host = nullptr;       // page-locked landing zone of the compact copies
@@ -298,6 +300,10 @@ ecl::LaunchEnv env_of(const ecl_gpu* g, int lane) {
   env.scratch = g->scratch;
   env.device = g->ordinal;
   env.in_host = g->in_host_ptr.data();
+  if (g->n_peers) {
+    env.peer_out = g->peer_out.data();
+    env.n_peers = g->n_peers;
+  }
   return env;
 }
 
@@ -1148,6 +1154,43 @@ int ecl_gpu_download_tally(ecl_gpu* g, uint32_t* host) {
   if (int rc = set_device(g)) return rc;
   if (int rc = sync_all(g)) return rc;
   ECL_CK(cudaMemcpy(host, g->tally, g->tally_items * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return ECL_OK;
+}
+
+int ecl_gpu_set_peer_outputs(ecl_gpu* g, void* const* ptrs, uint32_t n_peers) {
+  if (!g->spec) return fail(ECL_CONFIG_ERROR, "peer outputs before bind");
+  if (n_peers == 0) {
+    g->peer_out.clear();
+    g->n_peers = 0;
+    return ECL_OK;
+  }
+  if (!g->spec->peer_writes) return fail(ECL_CONFIG_ERROR, "the bound kernel does not write to peer buffers");
+  if (n_peers > ecl::kMaxPeerWrites) return fail(ECL_CONFIG_ERROR, "too many peers for a fused exchange");
+  const size_t n = static_cast<size_t>(n_peers) * g->out.size();
+  for (size_t k = 0; k < n; ++k) {
+    if (!ptrs[k]) continue;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, ptrs[k]) != cudaSuccess || a.type != cudaMemoryTypeDevice) {
+      cudaGetLastError();
+      return fail(ECL_CONFIG_ERROR, "peer output is not device memory");
+    }
+    if (a.device != g->ordinal) {
+      enable_peer(g->ordinal, a.device);
+      std::lock_guard lock(g_peer_m);
+      if (g_peer[g->ordinal & 63][a.device & 63] != 1)
+        return fail(ECL_CONFIG_ERROR, "no peer access to the device of a peer output");
+    }
+  }
+  if (int rc = set_device(g)) return rc;
+  if (int rc = join_lanes(g)) return rc;  // launches already queued keep the previous targets
+  g->peer_out.assign(ptrs, ptrs + n);
+  g->n_peers = n_peers;
+  return fan_out_lane0(g);
+}
+
+int ecl_gpu_peer_writes(const ecl_gpu* g, int* supported) {
+  if (!g->spec) return fail(ECL_CONFIG_ERROR, "peer_writes before bind");
+  *supported = g->spec->peer_writes ? 1 : 0;
   return ECL_OK;
 }
 

@@ -65,6 +65,10 @@ struct KernelSpec {
   // Set for kernels whose single long launch is measurably slower than the
   // same work as two-stream pieces (Ray: 11.0 ms vs 9.9 ms at 8192^2).
   uint64_t compute_split_items = 0;
+  // The kernel can store its outputs into peer devices' buffers as it
+  // computes them (LaunchEnv::peer_out): an iterative run then needs no
+  // separate per-step exchange of those outputs.
+  bool peer_writes = false;
   std::vector<ecl_arg> args;
   std::vector<ecl_buffer_geom> inputs, outputs;
   // parsed arguments
@@ -95,7 +99,15 @@ struct LaunchEnv {
   const void* const* in_host = nullptr;
   // The piece's outputs are copied to host memory right after it (e2e runs).
   bool host_copies = false;
+  // Fused exchange (kernels with KernelSpec::peer_writes): the current output
+  // buffers of the other devices of an iterative run, n_peers x outputs
+  // pointers (peer-major; nullptr = none); the kernel stores its results
+  // there too, over NVLink, as it computes them.
+  void* const* peer_out = nullptr;
+  uint32_t n_peers = 0;
 };
+
+constexpr uint32_t kMaxPeerWrites = 8;  // peers a fused-exchange kernel writes to
 
 // Device scratch a kernel needs per binding (e.g. Mandelbrot coordinate tables),
 // filled once by prepare_kernel when the program is bound to a device.

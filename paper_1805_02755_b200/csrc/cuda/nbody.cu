@@ -46,10 +46,21 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
 // coordinate): every interaction step is an FADD2/FFMA2/FMUL2 on the pair
 // (the source body is a broadcast .F32 operand), halving the FP32 issue
 // slots; only the two MUFU.RSQ stay scalar.
+// Fused exchange: the other devices' output buffers of this step (pos, vel
+// per peer); the new state of every body this launch integrates is stored
+// there too — the per-step allgather rides on the kernel's own stores over
+// NVLink instead of following it as a copy.
+struct PeerOut {
+  float4* pos[kMaxPeerWrites];
+  float4* vel[kMaxPeerWrites];
+  uint32_t n;
+};
+
 template <int S, int B2, int MB>
 __global__ void __launch_bounds__(kThreads, MB)
     nbody_step(const float4* __restrict__ pos, const float4* __restrict__ vel, uint64_t n, float dt, float eps2,
-               float4* __restrict__ npos, float4* __restrict__ nvel, uint64_t first, uint64_t count) {
+               float4* __restrict__ npos, float4* __restrict__ nvel, uint64_t first, uint64_t count,
+               const __grid_constant__ PeerOut peers) {
   constexpr int T = kThreads / S, B = 2 * B2;
   __shared__ float4 tile[kTile];
   __shared__ float3 part[S > 1 ? (S - 1) * B * T : 1];
@@ -124,9 +135,15 @@ __global__ void __launch_bounds__(kThreads, MB)
     const uint64_t i = base + static_cast<uint64_t>(b) * T;
     if (i >= first + count) continue;
     const float4 v = vel[i];
-    npos[i] = make_float4(p[b].x + v.x * dt + acc[b].x * hdt2, p[b].y + v.y * dt + acc[b].y * hdt2,
-                          p[b].z + v.z * dt + acc[b].z * hdt2, p[b].w);
-    nvel[i] = make_float4(v.x + acc[b].x * dt, v.y + acc[b].y * dt, v.z + acc[b].z * dt, v.w);
+    const float4 np = make_float4(p[b].x + v.x * dt + acc[b].x * hdt2, p[b].y + v.y * dt + acc[b].y * hdt2,
+                                  p[b].z + v.z * dt + acc[b].z * hdt2, p[b].w);
+    const float4 nv = make_float4(v.x + acc[b].x * dt, v.y + acc[b].y * dt, v.z + acc[b].z * dt, v.w);
+    npos[i] = np;
+    nvel[i] = nv;
+    for (uint32_t q = 0; q < peers.n; ++q) {
+      if (peers.pos[q]) peers.pos[q][i] = np;
+      if (peers.vel[q]) peers.vel[q][i] = nv;
+    }
   }
 }
 
@@ -134,10 +151,16 @@ template <int S, int B2, int MB = 1>
 cudaError_t launch(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
   const uint64_t per_block = static_cast<uint64_t>(kThreads / S) * 2 * B2;
   const uint64_t blocks = (count + per_block - 1) / per_block;
+  PeerOut peers{};
+  peers.n = env.n_peers < kMaxPeerWrites ? env.n_peers : kMaxPeerWrites;
+  for (uint32_t q = 0; q < peers.n; ++q) {
+    peers.pos[q] = static_cast<float4*>(env.peer_out[2 * q]);
+    peers.vel[q] = static_cast<float4*>(env.peer_out[2 * q + 1]);
+  }
   nbody_step<S, B2, MB><<<static_cast<unsigned>(blocks), kThreads, 0, env.stream>>>(
       static_cast<const float4*>(env.in[0]), static_cast<const float4*>(env.in[1]), spec.nbody.bodies,
       spec.nbody.dt, spec.nbody.eps2, static_cast<float4*>(env.out[0]), static_cast<float4*>(env.out[1]), first,
-      count);
+      count, peers);
   return cudaGetLastError();
 }
 

@@ -196,6 +196,7 @@ int resolve_kernel(KernelSpec& s, std::string* err) {
             return bad(err, "nbody buffers are float4[bodies]");
       if (!one_to_one(s)) return bad(err, "nbody writes with a 1:1 out pattern");
       s.nbody = NBodyParams{n, static_cast<float>(dt), static_cast<float>(eps2)};
+      s.peer_writes = true;  // fused per-step exchange (nbody.cu)
       return ECL_OK;
     }
     case KernelKind::Binomial: {

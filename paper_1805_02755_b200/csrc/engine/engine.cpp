@@ -582,6 +582,54 @@ struct Engine::Impl {
     }
   };
 
+  // Fused exchange (kernels with peer writes, NBody): every launch of step
+  // k stores its results into the current output buffers of every other
+  // device as well, so the step's allgather happens inside the kernel, over
+  // NVLink, tile by tile, instead of as copies after it.  ECL_FUSED_EXCHANGE=0
+  // keeps the post-step copies (A/B); a device without peer access falls
+  // back to them too.
+  bool fused_exchange_possible(std::span<const std::pair<std::uint32_t, std::uint32_t>> swaps) const {
+    static const bool enabled = [] {
+      const char* v = std::getenv("ECL_FUSED_EXCHANGE");
+      return !(v && std::string(v) == "0");
+    }();
+    if (!enabled || swaps.empty() || cfg.devices.size() < 2 || cfg.devices.size() - 1 > 8) return false;
+    for (auto& d : devices) {
+      int ok = 0;
+      if (ecl_gpu_peer_writes(d->gpu, &ok) != ECL_OK || !ok) return false;
+    }
+    return true;
+  }
+
+  // Points each local device's fused stores at the other devices' outputs of
+  // step k (nullptr on the last step: nothing to exchange).
+  void set_peer_targets(const PeerBuffers& peers, std::span<const std::pair<std::uint32_t, std::uint32_t>> swaps,
+                        std::uint32_t k, bool exchange) {
+    const std::size_t nout = prog.spec().out_buffers.size(), ndev = cfg.devices.size();
+    for (auto& d : devices) {
+      if (!exchange) {
+        check(ecl_gpu_set_peer_outputs(d->gpu, nullptr, 0), "peer outputs");
+        continue;
+      }
+      std::vector<void*> ptrs;
+      for (std::uint32_t other = 0; other < ndev; ++other) {
+        if (other == d->index) continue;
+        std::vector<void*> row(nout, nullptr);
+        for (std::size_t sw = 0; sw < swaps.size(); ++sw) {
+          const std::uint32_t o = swaps[sw].second;
+          const int slot = local_slot(other);
+          if (slot >= 0) {
+            check(ecl_gpu_buffer(devices[slot]->gpu, 1, o, &row[o]), "peer buffer");
+          } else {
+            row[o] = const_cast<void*>(peers.output_of(other, sw, k));
+          }
+        }
+        ptrs.insert(ptrs.end(), row.begin(), row.end());
+      }
+      check(ecl_gpu_set_peer_outputs(d->gpu, ptrs.data(), static_cast<std::uint32_t>(ndev - 1)), "peer outputs");
+    }
+  }
+
   ExecutionTrace run_steps(std::span<const void* const> inputs, std::span<void* const> outputs, std::uint32_t steps,
                            std::span<const std::pair<std::uint32_t, std::uint32_t>> swaps) {
     const ProgramSpec& s = prog.spec();
@@ -598,7 +646,19 @@ struct Engine::Impl {
     std::vector<Package> all, step;
     PeerBuffers peers;
     if (shared && steps > 1) peers.open(*this, swaps);
+    bool fused = steps > 1 && fused_exchange_possible(swaps);
     for (std::uint32_t k = 0; k < steps; ++k) {
+      if (fused) {
+        try {
+          set_peer_targets(peers, swaps, k, k + 1 < steps);
+        } catch (const Error&) {
+          if (k != 0 || shared) throw;  // ranks must agree: a rank cannot fall back alone
+          // no peer access for in-kernel stores (e.g. a PCIe box without
+          // P2P): the post-step copies exchange the state instead
+          for (auto& d : devices) (void)ecl_gpu_set_peer_outputs(d->gpu, nullptr, 0);
+          fused = false;
+        }
+      }
       if (tally && k > 0)
         for (auto& d : devices) check(ecl_gpu_enable_tally(d->gpu, 1), "tally");
       try {
@@ -608,7 +668,7 @@ struct Engine::Impl {
         throw;
       }
       inputs_streaming = false;  // streamed up during the first step
-      if (k + 1 < steps) {
+      if (k + 1 < steps && !fused) {
         for (const Package& p : step) {
           const OutRange r = out_range_for(p, prog);
           const int slot = local_slot(p.device_index);
@@ -629,16 +689,19 @@ struct Engine::Impl {
                       "pull");
           }
         }
-        for (auto& d : devices)
-          for (const auto& [i, o] : swaps) check(ecl_gpu_swap_io(d->gpu, i, o), "swap");
         if (shared) {
           // pulls complete before any peer overwrites the buffers they read
           for (auto& d : devices) check(ecl_gpu_sync(d->gpu), "sync");
           shared->barrier();
         }
       }
+      if (k + 1 < steps)
+        for (auto& d : devices)
+          for (const auto& [i, o] : swaps) check(ecl_gpu_swap_io(d->gpu, i, o), "swap");
       all.insert(all.end(), step.begin(), step.end());
     }
+    if (fused)
+      for (auto& d : devices) check(ecl_gpu_set_peer_outputs(d->gpu, nullptr, 0), "peer outputs");
     last_packages = step;
     last_resident = true;
     bool any_out = false;

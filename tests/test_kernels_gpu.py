@@ -292,3 +292,38 @@ def test_nbody_exchange_through_the_peer_copy_path(gpu_available):
                        cwd=root)
     assert r.returncode == 0, r.stderr
     assert float(r.stdout.strip().splitlines()[-1]) <= 1e-4
+
+
+_FUSED_SCRIPT = """
+import sys, numpy as np
+import paper_1805_02755_b200 as P
+from paper_1805_02755_b200 import workloads as W
+from tests._oracle import Oracle
+n, steps = 6144, 5
+pos, vel = Oracle().nbody_init(11, n)
+prog = P.validate_program(W.nbody_spec(n))
+out = [np.zeros((n, 4), np.float32), np.zeros((n, 4), np.float32)]
+devs = [P.cuda_device(f"gpu0{c}", 0) for c in "abc"]
+with P.Engine(P.EngineConfig(devs, P.DynamicConfig(9)), prog) as e:
+    e.run_steps([pos, vel], out, steps, [(0, 0), (1, 1)])
+np.save(sys.argv[1], np.concatenate(out))
+"""
+
+
+def test_nbody_fused_exchange_equals_post_step_copies(gpu_available, tmp_path):
+    # ECL_FUSED_EXCHANGE: the kernel's own stores into the other devices'
+    # buffers (default) against the post-step owner-slice copies — the same
+    # values land in the same places, so the final state is bit-identical
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for fused in ("1", "0"):
+        f = tmp_path / f"f{fused}.npy"
+        env = dict(os.environ, ECL_FUSED_EXCHANGE=fused, PYTHONPATH=root)
+        r = subprocess.run([sys.executable, "-c", _FUSED_SCRIPT, str(f)], env=env, capture_output=True, text=True,
+                           timeout=300, cwd=root)
+        assert r.returncode == 0, r.stderr
+        outs.append(np.load(f))
+    assert outs[0].view(np.uint32).tolist() == outs[1].view(np.uint32).tolist()
