@@ -123,3 +123,49 @@ def test_native_run_split_covers_the_grid(gpu_available, lib, oracle):
         so.ecl_kernel_destroy(k)
     finally:
         so.ecl_gpu_close(g)
+
+
+def test_peer_outputs_refused_for_kernels_without_peer_writes(gpu_available, lib):
+    # ecl_gpu_set_peer_outputs: only kernels that store into peer buffers
+    # (NBody) accept targets; host memory is refused as a target
+    so = lib
+    so.ecl_gpu_set_peer_outputs.restype = c_int
+    so.ecl_gpu_set_peer_outputs.argtypes = [c_vp, ctypes.POINTER(c_vp), c_u32]
+    so.ecl_gpu_peer_writes.restype = c_int
+    so.ecl_gpu_peer_writes.argtypes = [c_vp, ctypes.POINTER(c_int)]
+    g = c_vp()
+    assert so.ecl_gpu_open(0, 2, ctypes.byref(g)) == 0
+    try:
+        n, lws = 4096, 128
+        args = (Arg * 2)(Arg(1, 0, 0, 1.0), Arg(1, 0, 0, 0.0))
+        geom = (Geom * 1)(Geom(8, n))
+        k = c_vp()
+        assert so.ecl_kernel_create(b"vecscale", n, lws, args, 2, geom, 1, geom, 1, 1, 1, ctypes.byref(k)) == 0
+        assert so.ecl_gpu_bind(g, k) == 0
+        ok = c_int(-1)
+        assert so.ecl_gpu_peer_writes(g, ctypes.byref(ok)) == 0 and ok.value == 0
+        dout = c_vp()
+        assert so.ecl_gpu_buffer(g, 1, 0, ctypes.byref(dout)) == 0
+        ptrs = (c_vp * 1)(dout)
+        assert N.code_name(so.ecl_gpu_set_peer_outputs(g, ptrs, 1)) == "ConfigError"
+        assert so.ecl_gpu_set_peer_outputs(g, None, 0) == 0  # clearing is always fine
+        so.ecl_kernel_destroy(k)
+
+        # NBody accepts device targets and refuses host memory
+        nb = 1024
+        args = (Arg * 2)(Arg(1, 0, 0, 0.005), Arg(1, 0, 0, 500.0))
+        geom4 = (Geom * 2)(Geom(16, nb), Geom(16, nb))
+        nargs = (Arg * 3)(Arg(0, 0, nb, 0.0), Arg(1, 0, 0, 0.005), Arg(1, 0, 0, 500.0))
+        assert so.ecl_kernel_create(b"nbody", nb, 64, nargs, 3, geom4, 2, geom4, 2, 1, 1, ctypes.byref(k)) == 0
+        assert so.ecl_gpu_bind(g, k) == 0
+        assert so.ecl_gpu_peer_writes(g, ctypes.byref(ok)) == 0 and ok.value == 1
+        d0, d1 = c_vp(), c_vp()
+        assert so.ecl_gpu_buffer(g, 0, 0, ctypes.byref(d0)) == 0 and so.ecl_gpu_buffer(g, 0, 1, ctypes.byref(d1)) == 0
+        assert so.ecl_gpu_set_peer_outputs(g, (c_vp * 2)(d0, d1), 1) == 0
+        host = np.zeros(64)
+        bad = (c_vp * 2)(host.ctypes.data, d1)
+        assert N.code_name(so.ecl_gpu_set_peer_outputs(g, bad, 1)) == "ConfigError"
+        assert so.ecl_gpu_set_peer_outputs(g, None, 0) == 0
+        so.ecl_kernel_destroy(k)
+    finally:
+        so.ecl_gpu_close(g)
