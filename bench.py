@@ -386,7 +386,7 @@ class Binomial(Workload):
 
 
 class Ray(Workload):
-    ceiling = (17.0 / 20.0, "17 counted flops per sphere test in the 10 FMA-pipe lane-ops of the conservative "
+    ceiling = (17.0 / 16.0, "17 counted flops per sphere test in the 8 FMA-pipe lane-ops of the conservative "
                             "fused scan (candidates then run the exact 16-op IEEE test; shading not counted here)")
     name = "ray"
     WIDTH = HEIGHT = 8192

@@ -97,7 +97,7 @@ __device__ __forceinline__ void pair_disc(V3 o, V3 d, float4 r0, float4 r1, floa
 //   e    = o.d - s.d                      (o.d per ray, s.d: 3 FMA)
 //   cc   = (|o|^2 + q) - 2 o.s            (q = |s|^2 - r^2 per sphere, o.s: 3 FMA)
 //   disc'= e*e - cc
-// (10 packed instructions per pair instead of 16) and rejects a sphere only
+// (8 packed instructions per pair instead of 16, see scan_group) and rejects a sphere only
 // when disc' < -M, M = 2^-17 ((|o|_1 + max|s|)^2 + max r^2).  Error bound
 // (u = 2^-24, R >= |o| + |s|, |d| = 1): the IEEE-ordered exact path's disc
 // is within 17.1 u R^2 + 3 u r^2 of the real-number discriminant, disc'
@@ -107,8 +107,8 @@ __device__ __forceinline__ void pair_disc(V3 o, V3 d, float4 r0, float4 r1, floa
 // root_of), so the image stays bit-identical; only provable misses are
 // skipped.
 struct RayPre {
-  float2 ox, oy, oz, dx, dy, dz;  // (v, v) pairs: FFMA2 operands
-  float2 od, moo;                 // o.d and M - |o|^2
+  float2 ox, oy, oz, hx, hy, hz;  // (v, v) pairs: FFMA2 operands; h = d / 2
+  float2 nod, moo;                // -(o.d) and M - |o|^2
   uint32_t all;                   // ~0u: M overflowed, every pair is a candidate
 };
 __device__ __forceinline__ RayPre ray_pre(V3 o, V3 d, float smax, float rmax2) {
@@ -116,24 +116,28 @@ __device__ __forceinline__ RayPre ray_pre(V3 o, V3 d, float smax, float rmax2) {
   p.ox = make_float2(o.x, o.x);
   p.oy = make_float2(o.y, o.y);
   p.oz = make_float2(o.z, o.z);
-  p.dx = make_float2(d.x, d.x);
-  p.dy = make_float2(d.y, d.y);
-  p.dz = make_float2(d.z, d.z);
+  p.hx = make_float2(0.5f * d.x, 0.5f * d.x);  // exact: scaling by a power of two
+  p.hy = make_float2(0.5f * d.y, 0.5f * d.y);
+  p.hz = make_float2(0.5f * d.z, 0.5f * d.z);
   const float od = fmaf(o.z, d.z, fmaf(o.y, d.y, o.x * d.x));
   const float oo = fmaf(o.z, o.z, fmaf(o.y, o.y, o.x * o.x));
   const float R = fabsf(o.x) + fabsf(o.y) + fabsf(o.z) + smax;
   const float M = 0x1p-17f * fmaf(R, R, rmax2);
-  p.od = make_float2(od, od);
+  p.nod = make_float2(-od, -od);
   p.moo = make_float2(M - oo, M - oo);
   // with M finite every magnitude below is finite (no NaN); otherwise skip nothing
   p.all = M < INFINITY ? 0u : ~0u;
   return p;
 }
-// pre[i] = (x0, x1, y0, y1), (z0, z1, q0, q1) for sphere pair i.  The scan
-// evaluates t = disc' + M = e*e + ((M - |o|^2 - q) + 2 o.s) and collects the
-// sign bits: a sphere is rejected iff t < 0, a pair iff both are — one AND of
-// the two words and one funnel shift per pair, no compares.  Bit G-1-k of
-// the collected word is pair k's "both rejected".
+// pre[i] = (2x0, 2x1, 2y0, 2y1), (2z0, 2z1, q0, q1) for sphere pair i (the
+// doubled centre 2s serves both products: (2s).(d/2) = s.d exactly, and
+// (2s).o = 2 o.s).  Per pair, 8 packed FMA-pipe instructions:
+//   e'  = (2s).(d/2) - o.d                      = -e   (3 FFMA2, from -o.d)
+//   acc = (M - |o|^2 - q) + (2s).o                     (1 FADD2 + 3 FFMA2)
+//   t   = e'^2 + acc = disc' + M                        (1 FFMA2)
+// A sphere is rejected iff t < 0, a pair iff both are: the sign bits are
+// collected with one AND of the two words and one funnel shift per pair,
+// no compares.  Bit G-1-k of the collected word is pair k's "both rejected".
 template <int G>
 __device__ __forceinline__ uint32_t scan_group(const RayPre& p, const float4 (*pre)[2], uint32_t first) {
   static_assert(G >= 1 && G <= 32, "group of at most 32 pairs");
@@ -143,11 +147,9 @@ __device__ __forceinline__ uint32_t scan_group(const RayPre& p, const float4 (*p
     const float4 r0 = pre[first + k][0], r1 = pre[first + k][1];
     const float2 X = make_float2(r0.x, r0.y), Y = make_float2(r0.z, r0.w);
     const float2 Z = make_float2(r1.x, r1.y), Q = make_float2(r1.z, r1.w);
-    const float2 sd = __ffma2_rn(Z, p.dz, __ffma2_rn(Y, p.dy, __fmul2_rn(X, p.dx)));
-    const float2 os = __ffma2_rn(Z, p.oz, __ffma2_rn(Y, p.oy, __fmul2_rn(X, p.ox)));
-    const float2 e = __fadd2_rn(p.od, neg2(sd));
-    const float2 mc = __ffma2_rn(os, make_float2(2.0f, 2.0f), __fadd2_rn(p.moo, neg2(Q)));  // M - cc
-    const float2 t = __ffma2_rn(e, e, mc);
+    const float2 e = __ffma2_rn(Z, p.hz, __ffma2_rn(Y, p.hy, __ffma2_rn(X, p.hx, p.nod)));
+    const float2 acc = __ffma2_rn(Z, p.oz, __ffma2_rn(Y, p.oy, __ffma2_rn(X, p.ox, __fadd2_rn(p.moo, neg2(Q)))));
+    const float2 t = __ffma2_rn(e, e, acc);
     miss = __funnelshift_l(__float_as_uint(t.x) & __float_as_uint(t.y), miss, 1);
   }
   const uint32_t cand = (~miss | p.all) & (G == 32 ? ~0u : ((1u << G) - 1u));
@@ -217,9 +219,12 @@ __global__ void __launch_bounds__(kThreads, MB)
     float* rec = reinterpret_cast<float*>(pair_rec[i / 2]);
     float* pre = reinterpret_cast<float*>(pre_rec[i / 2]);
     const uint32_t h = i & 1u;
-    rec[0 + h] = pre[0 + h] = c.x;
-    rec[2 + h] = pre[2 + h] = c.y;
-    rec[4 + h] = pre[4 + h] = c.z;
+    rec[0 + h] = c.x;
+    rec[2 + h] = c.y;
+    rec[4 + h] = c.z;
+    pre[0 + h] = 2.0f * c.x;  // exact
+    pre[2 + h] = 2.0f * c.y;
+    pre[4 + h] = 2.0f * c.z;
     rec[6 + h] = mul(c.w, c.w);
     const double x = c.x, y = c.y, z = c.z, r = c.w;
     pre[6 + h] = static_cast<float>(x * x + y * y + z * z - r * r);  // q = |s|^2 - r^2
@@ -489,10 +494,12 @@ cudaError_t launch(const KernelSpec& spec, const LaunchEnv& env, uint64_t first,
 cudaError_t launch_ray(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
   if (count == 0) return cudaSuccess;
   // ECL_RAY_MB: 128-thread CTAs per SM the registers are sized for.  Measured
-  // (8192^2, sign-bit prefiltered scans, scene constants in shared memory):
-  // 6 -> 11.40 ms (80 registers, 8 B spilled), 7 -> 11.15 (72, no spill),
-  // 8 -> 11.01 (64; 16 B of stack, 28 B of spill loads, outside the sphere
-  // scans: the occupancy pays for them), 10 -> 11.87.
+  // (8192^2 native single launch, sign-bit prefiltered scans, scene constants
+  // in shared memory): 6 -> 11.40 ms (80 registers, 8 B spilled),
+  // 7 -> 11.15 (72, no spill), 8 -> 11.01 (64; 16 B of stack, 28 B of spill
+  // loads, outside the sphere scans: the occupancy pays for them), 10 -> 11.87.
+  // With the 8-instruction scan (bench step, two-lane pieces): 7 -> 9.38,
+  // 8 -> 9.23, 10 -> 9.50.
   static const int env_mb = [] {
     const char* v = std::getenv("ECL_RAY_MB");
     return v ? std::atoi(v) : 0;
