@@ -100,30 +100,88 @@ __global__ void coord_tables(const Viewport<Real> vp, Real* __restrict__ tab) {
 // One speculative block of RB iterations for this lane, replayed exactly
 // when its flag is raised (see the comment at the call site).  Warp-uniform
 // control: every lane of the warp calls it with the same RB.
-template <typename Real, int RB>
+//
+// Loop = true (settled warps): end-checked blocks repeat in a tight loop
+// until a live lane raises its flag or the next block could reach max_it,
+// so the outer loop's refill ballot, block-length vote and store check run
+// once per pixel event instead of once per block (ncu, 16384^2 x 2048: 57
+// control instructions per 32-iteration block against 192 FP64 ones, each
+// FP64 instruction holding the issue port two cycles).  The block that
+// raised a flag ends exactly like a single block: unflagged lanes commit,
+// flagged lanes replay it from its saved state.
+template <typename Real, int RB, bool Loop = false>
 __device__ __forceinline__ void spec_block(Real& zx, Real& zy, uint32_t& n, bool& alive, bool far, Real cx, Real cy,
                                            uint32_t max_it) {
   using A = Arith<Real>;
   using Bits = typename A::Bits;
-  const Real zx0 = zx, zy0 = zy;
-  const uint32_t n0 = n;
-  uint32_t acc = 0;
+  Real zx0 = zx, zy0 = zy;
+  uint32_t n0 = n;
+  bool fast;
   if (__all_sync(kFull, far || !alive)) {
+    bool done = false;
+    if constexpr (Loop) {
+      // Blocks every live lane can take before max_it; the loop runs all but
+      // the last, which the regular block below handles with its max_it rule.
+      uint32_t room = alive ? (max_it - n) / RB : 0xffffffffu;
+      room = __reduce_min_sync(kFull, room);
+      uint32_t k = 0;
+      for (; k + 1 < room; ++k) {
+        zx0 = zx;
+        zy0 = zy;
 #pragma unroll
-    for (int r = 0; r < RB - 1; ++r) {
+        for (int r = 0; r < RB - 1; ++r) {
+          const Real xx = A::mul(zx, zx);
+          const Real yy = A::mul(zy, zy);
+          const Real t = A::mul(zx, zy);
+          zy = A::twice_plus(t, cy);
+          zx = A::add(A::sub(xx, yy), cx);
+        }
+        const Real xx = A::mul(zx, zx);
+        const Real yy = A::mul(zy, zy);
+        const uint32_t acc = A::high(xx) | A::high(yy);
+        const Real t = A::mul(zx, zy);
+        zy = A::twice_plus(t, cy);
+        zx = A::add(A::sub(xx, yy), cx);
+        const bool flag = alive && (acc & 0x40000000u) != 0u;
+        if (__any_sync(kFull, flag)) {  // this block ends like a regular one
+          n += k * RB;
+          n0 = n;
+          fast = alive && !flag;
+          if (fast) n = n0 + RB;  // n0 + RB <= max_it: k + 1 < room
+          done = true;
+          break;
+        }
+      }
+      if (!done) {
+        n += k * RB;
+        n0 = n;
+        zx0 = zx;
+        zy0 = zy;
+      }
+    }
+    if (!done) {
+#pragma unroll
+      for (int r = 0; r < RB - 1; ++r) {
+        const Real xx = A::mul(zx, zx);
+        const Real yy = A::mul(zy, zy);
+        const Real t = A::mul(zx, zy);
+        zy = A::twice_plus(t, cy);
+        zx = A::add(A::sub(xx, yy), cx);
+      }
       const Real xx = A::mul(zx, zx);
       const Real yy = A::mul(zy, zy);
+      const uint32_t acc = A::high(xx) | A::high(yy);
       const Real t = A::mul(zx, zy);
       zy = A::twice_plus(t, cy);
       zx = A::add(A::sub(xx, yy), cx);
+      fast = alive && n0 + RB <= max_it && (acc & 0x40000000u) == 0u;
+      if (fast) {
+        n = n0 + RB;
+        alive = n < max_it;
+      }
     }
-    const Real xx = A::mul(zx, zx);
-    const Real yy = A::mul(zy, zy);
-    acc = A::high(xx) | A::high(yy);
-    const Real t = A::mul(zx, zy);
-    zy = A::twice_plus(t, cy);
-    zx = A::add(A::sub(xx, yy), cx);
   } else {
+    uint32_t acc = 0;
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
       const Real xx = A::mul(zx, zx);
@@ -133,11 +191,11 @@ __device__ __forceinline__ void spec_block(Real& zx, Real& zy, uint32_t& n, bool
       zy = A::twice_plus(t, cy);
       zx = A::add(A::sub(xx, yy), cx);
     }
-  }
-  const bool fast = alive && n0 + RB <= max_it && (acc & 0x40000000u) == 0u;
-  if (fast) {
-    n = n0 + RB;
-    alive = n < max_it;
+    fast = alive && n0 + RB <= max_it && (acc & 0x40000000u) == 0u;
+    if (fast) {
+      n = n0 + RB;
+      alive = n < max_it;
+    }
   }
   bool live = alive && !fast;  // lanes replaying the block exactly
   if (__any_sync(kFull, live)) {
@@ -177,7 +235,8 @@ __device__ __forceinline__ void spec_block(Real& zx, Real& zy, uint32_t& n, bool
 // a few hundred iterations (a 400k-pixel sample of the config: 89 % of the
 // interior pixels detected, at 561 iterations on average instead of 2048).
 // Off by default: the bench's headline runs every reference iteration.
-template <typename Real, int R, int MB = kMinBlocks<Real>, int RL = R, uint32_t kSettle = 32, bool Periodic = false>
+template <typename Real, int R, int MB = kMinBlocks<Real>, int RL = R, uint32_t kSettle = 32, bool Periodic = false,
+          bool Tight = true>
 __global__ void __launch_bounds__(kThreads, MB)
     mandel_persistent(const Viewport<Real> vp, const Real* __restrict__ tab, uint64_t first, uint64_t count,
                       uint4* __restrict__ out, uint32_t* __restrict__ compact, unsigned* __restrict__ ctrl) {
@@ -281,7 +340,8 @@ __global__ void __launch_bounds__(kThreads, MB)
     // iterations (long orbits, mostly the set's interior) -> RL-iteration
     // blocks, amortizing the block control; otherwise R, so pixels that
     // escape early waste fewer speculative iterations.
-    if (__all_sync(kFull, !alive || n >= kSettle)) spec_block<Real, RL>(zx, zy, n, alive, far, cx, cy, max_it);
+    if (__all_sync(kFull, !alive || n >= kSettle))
+      spec_block<Real, RL, Tight && !Periodic>(zx, zy, n, alive, far, cx, cy, max_it);
     else spec_block<Real, R>(zx, zy, n, alive, far, cx, cy, max_it);
     if constexpr (Periodic) {
       if (valid && alive) {
@@ -585,12 +645,13 @@ Viewport<Real> make_viewport(const MandelParams& p) {
   return vp;
 }
 
-template <typename Real, int R, int MB = kMinBlocks<Real>, int RL = R, uint32_t kSettle = 32, bool Periodic = false>
+template <typename Real, int R, int MB = kMinBlocks<Real>, int RL = R, uint32_t kSettle = 32, bool Periodic = false,
+          bool Tight = true>
 cudaError_t launch_real(const MandelParams& p, const LaunchEnv& env, uint64_t first, uint64_t count) {
   static int blocks_per_sm = 0;
   if (blocks_per_sm == 0) {
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &blocks_per_sm, mandel_persistent<Real, R, MB, RL, kSettle, Periodic>, kThreads, 0);
+        &blocks_per_sm, mandel_persistent<Real, R, MB, RL, kSettle, Periodic, Tight>, kThreads, 0);
     if (e != cudaSuccess) return e;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
@@ -601,7 +662,7 @@ cudaError_t launch_real(const MandelParams& p, const LaunchEnv& env, uint64_t fi
   uint64_t grid = static_cast<uint64_t>(env.sms) * static_cast<uint64_t>(blocks_per_sm);
   if (blocks_needed < grid) grid = blocks_needed;
   if (grid == 0) return cudaSuccess;
-  mandel_persistent<Real, R, MB, RL, kSettle, Periodic><<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
+  mandel_persistent<Real, R, MB, RL, kSettle, Periodic, Tight><<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
       vp, tab, first, count, static_cast<uint4*>(env.out[0]), env.compact, env.ctrl);
   return cudaGetLastError();
 }
@@ -693,6 +754,8 @@ cudaError_t launch_mandelbrot(const KernelSpec& spec, const LaunchEnv& env, uint
     // exact early exit for periodic orbits (see mandel_persistent): same
     // counts, a fraction of the interior's iterations
     case 14: return launch_real<double, 8, 4, 32, 32, true>(spec.mandel, env, first, count);
+    // the default without the tight settled loop (one outer-loop pass per block)
+    case 15: return launch_real<double, 8, 4, 32, 32, false, false>(spec.mandel, env, first, count);
     // measured (16384^2 x 2048): (8, 32 after 32 iterations) 38.85 ms; fixed 16: 41.2 ms;
     // (16, 32) 39.2; (8, 64) 39.1; (16, 64) 39.3; settle after 16 / 64: 39.2; (8, 24) 39.8
     default: return launch_real<double, 8, 4, 32>(spec.mandel, env, first, count);

@@ -123,7 +123,7 @@ def test_kernel_variant_ids():
             lib.ecl_kernel_destroy(k)
         return rc
 
-    for ok in ("mandelbrot", "mandelbrot@0", "mandelbrot@5", "mandelbrot@13", "mandelbrot@14"):
+    for ok in ("mandelbrot", "mandelbrot@0", "mandelbrot@5", "mandelbrot@13", "mandelbrot@14", "mandelbrot@15"):
         assert create(ok) == 0, ok
-    for bad in ("mandelbrot@15", "mandelbrot@", "mandelbrot@x", "mandelbrot@-1"):
+    for bad in ("mandelbrot@16", "mandelbrot@", "mandelbrot@x", "mandelbrot@-1"):
         assert N.code_name(create(bad)) == "UnknownKernel", bad
