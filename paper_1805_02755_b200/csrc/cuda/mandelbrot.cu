@@ -142,7 +142,10 @@ __device__ __forceinline__ void spec_block(Real& zx, Real& zy, uint32_t& n, bool
         const Real t = A::mul(zx, zy);
         zy = A::twice_plus(t, cy);
         zx = A::add(A::sub(xx, yy), cx);
-        const bool flag = alive && (acc & 0x40000000u) != 0u;
+        // acc >= 2^30 <=> bit 30 of a square's high word (a square's sign
+        // bit is clear unless it is NaN, whose exponent sets bit 30 too):
+        // one compare instead of shift, mask and compare.
+        const bool flag = alive && acc >= 0x40000000u;
         if (__any_sync(kFull, flag)) {  // this block ends like a regular one
           n += k * RB;
           n0 = n;
@@ -174,7 +177,7 @@ __device__ __forceinline__ void spec_block(Real& zx, Real& zy, uint32_t& n, bool
       const Real t = A::mul(zx, zy);
       zy = A::twice_plus(t, cy);
       zx = A::add(A::sub(xx, yy), cx);
-      fast = alive && n0 + RB <= max_it && (acc & 0x40000000u) == 0u;
+      fast = alive && n0 + RB <= max_it && acc < 0x40000000u;
       if (fast) {
         n = n0 + RB;
         alive = n < max_it;
@@ -191,7 +194,7 @@ __device__ __forceinline__ void spec_block(Real& zx, Real& zy, uint32_t& n, bool
       zy = A::twice_plus(t, cy);
       zx = A::add(A::sub(xx, yy), cx);
     }
-    fast = alive && n0 + RB <= max_it && (acc & 0x40000000u) == 0u;
+    fast = alive && n0 + RB <= max_it && acc < 0x40000000u;
     if (fast) {
       n = n0 + RB;
       alive = n < max_it;
