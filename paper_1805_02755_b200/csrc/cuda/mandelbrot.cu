@@ -222,6 +222,9 @@ __device__ __forceinline__ void spec_block(Real& zx, Real& zy, uint32_t& n, bool
         n += 1u;
       }
       live = live && n < max_it;
+      // every replaying lane has escaped (or hit max_it): the rest of the
+      // block would change nothing
+      if ((r & 1) == 1 && r + 1 < RB && !__any_sync(kFull, live)) break;
     }
     if (alive && !fast) alive = live;
   }
