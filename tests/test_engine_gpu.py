@@ -363,13 +363,18 @@ def test_adaptive_hguided_learns_and_carries_powers(gpu_available, oracle):
     """Measured-throughput HGuided: a run measures every device's
     work-items/ms over non-overlapping busy time; the next run starts from
     those rates.  Device 0 runs the periodic-orbit variant (mandelbrot@14,
-    same counts, fewer iterations) so the two logical devices differ."""
-    w, it = 2048, 2048
-    spec = W.mandelbrot_spec(w, w, it)
+    same counts, fewer iterations) so the two logical devices differ.  The
+    viewport lies inside the main cardioid, so every pixel costs the same
+    (max_iter iterations, or an early periodic exit): the measured rates do
+    not depend on which rows a device happened to draw."""
+    w, it = 1024, 2048
+    vp = (-0.5, -0.3, 0.1, 0.3)
+    spec = W.mandelbrot_spec(w, w, it, viewport=vp)
     prog = P.validate_program(spec)
     devs = devices(2)
     devs[0].kernel = "mandelbrot@14"
-    exp = expand_4to1(oracle.mandelbrot(w, w, it))
+    exp = expand_4to1(oracle.mandelbrot(w, w, it, viewport=vp))
+    assert (exp == it).all()  # all interior
     with P.Engine(P.EngineConfig(devs, P.HGuidedConfig(adaptive=True)), prog) as e:
         assert e.learned_powers() == []
         first = e.run([])
