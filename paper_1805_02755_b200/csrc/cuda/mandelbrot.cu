@@ -765,7 +765,8 @@ cudaError_t launch_mandelbrot(const KernelSpec& spec, const LaunchEnv& env, uint
     // measured (16384^2 x 2048): (8, 32 after 32 iterations) 38.85 ms; fixed 16: 41.2 ms;
     // (16, 32) 39.2; (8, 64) 39.1; (16, 64) 39.3; settle after 16 / 64: 39.2; (8, 24) 39.8.
     // With the tight settled loop (kernel only): (8, 32) 36.5 ms; 5 CTAs/SM 36.7;
-    // settle after 16: 37.0; (16, 32) 36.9; (8, 64) 38.0.
+    // settle after 16: 37.0; (16, 32) 36.9; (8, 64) 38.0; (4, 32) 37.8; settle after
+    // 24 / 48: 36.9 / 37.1; (12, 36) 39.3.
     default: return launch_real<double, 8, 4, 32>(spec.mandel, env, first, count);
   }
 }
