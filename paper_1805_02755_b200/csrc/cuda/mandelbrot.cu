@@ -433,33 +433,96 @@ struct Slot2 {
 };
 
 // One speculative block of RB iterations on both slots of a lane (see
-// spec_block); warp-uniform RB.
-template <typename Real, int RB>
+// spec_block); warp-uniform RB.  Loop = true: the tight settled loop of
+// spec_block, on both slots.
+template <typename Real, int RB, bool Loop = false>
 __device__ __forceinline__ void spec_block2(typename Pair<Real>::V& zx, typename Pair<Real>::V& zy, Slot2& sa,
                                             Slot2& sb, typename Pair<Real>::V cx, typename Pair<Real>::V cy,
                                             uint32_t max_it) {
   using A = Pair<Real>;
   using V = typename A::V;
-  const V zx0 = zx, zy0 = zy;
-  const uint32_t na0 = sa.n, nb0 = sb.n;
-  uint32_t acc_a = 0, acc_b = 0;
+  V zx0 = zx, zy0 = zy;
+  uint32_t na0 = sa.n, nb0 = sb.n;
+  bool fast_a, fast_b;
   if (__all_sync(kFull, (sa.far || !sa.alive) && (sb.far || !sb.alive))) {  // end-checked block
+    bool done = false;
+    if constexpr (Loop) {
+      const uint32_t ra = sa.alive ? (max_it - sa.n) / RB : 0xffffffffu;
+      const uint32_t rb = sb.alive ? (max_it - sb.n) / RB : 0xffffffffu;
+      const uint32_t room = __reduce_min_sync(kFull, ra < rb ? ra : rb);
+      uint32_t k = 0;
+      for (; k + 1 < room; ++k) {
+        zx0 = zx;
+        zy0 = zy;
 #pragma unroll
-    for (int r = 0; r < RB - 1; ++r) {
+        for (int r = 0; r < RB - 1; ++r) {
+          const V xx = A::mul0(zx, zx);
+          const V yy = A::mul0(zy, zy);
+          const V t = A::mul0(zx, zy);
+          zy = A::twice_plus(t, cy);
+          zx = A::add(A::sub(xx, yy), cx);
+        }
+        const V xx = A::mul0(zx, zx);
+        const V yy = A::mul0(zy, zy);
+        const uint32_t acc_a = A::hi(xx.x) | A::hi(yy.x);
+        const uint32_t acc_b = A::hi(xx.y) | A::hi(yy.y);
+        const V t = A::mul0(zx, zy);
+        zy = A::twice_plus(t, cy);
+        zx = A::add(A::sub(xx, yy), cx);
+        // acc >= 2^30 <=> bit 30 of a square (see spec_block)
+        const bool flag_a = sa.alive && acc_a >= 0x40000000u;
+        const bool flag_b = sb.alive && acc_b >= 0x40000000u;
+        if (__any_sync(kFull, flag_a || flag_b)) {  // this block ends like a regular one
+          sa.n += k * RB;
+          sb.n += k * RB;
+          na0 = sa.n;
+          nb0 = sb.n;
+          fast_a = sa.alive && !flag_a;
+          fast_b = sb.alive && !flag_b;
+          if (fast_a) sa.n = na0 + RB;  // < max_it: k + 1 < room
+          if (fast_b) sb.n = nb0 + RB;
+          done = true;
+          break;
+        }
+      }
+      if (!done) {
+        sa.n += k * RB;
+        sb.n += k * RB;
+        na0 = sa.n;
+        nb0 = sb.n;
+        zx0 = zx;
+        zy0 = zy;
+      }
+    }
+    if (!done) {
+#pragma unroll
+      for (int r = 0; r < RB - 1; ++r) {
+        const V xx = A::mul0(zx, zx);
+        const V yy = A::mul0(zy, zy);
+        const V t = A::mul0(zx, zy);
+        zy = A::twice_plus(t, cy);
+        zx = A::add(A::sub(xx, yy), cx);
+      }
       const V xx = A::mul0(zx, zx);
       const V yy = A::mul0(zy, zy);
+      const uint32_t acc_a = A::hi(xx.x) | A::hi(yy.x);
+      const uint32_t acc_b = A::hi(xx.y) | A::hi(yy.y);
       const V t = A::mul0(zx, zy);
       zy = A::twice_plus(t, cy);
       zx = A::add(A::sub(xx, yy), cx);
+      fast_a = sa.alive && na0 + RB <= max_it && acc_a < 0x40000000u;
+      fast_b = sb.alive && nb0 + RB <= max_it && acc_b < 0x40000000u;
+      if (fast_a) {
+        sa.n = na0 + RB;
+        sa.alive = sa.n < max_it;
+      }
+      if (fast_b) {
+        sb.n = nb0 + RB;
+        sb.alive = sb.n < max_it;
+      }
     }
-    const V xx = A::mul0(zx, zx);
-    const V yy = A::mul0(zy, zy);
-    acc_a = A::hi(xx.x) | A::hi(yy.x);
-    acc_b = A::hi(xx.y) | A::hi(yy.y);
-    const V t = A::mul0(zx, zy);
-    zy = A::twice_plus(t, cy);
-    zx = A::add(A::sub(xx, yy), cx);
   } else {
+    uint32_t acc_a = 0, acc_b = 0;
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
       const V xx = A::mul0(zx, zx);
@@ -470,16 +533,16 @@ __device__ __forceinline__ void spec_block2(typename Pair<Real>::V& zx, typename
       zy = A::twice_plus(t, cy);
       zx = A::add(A::sub(xx, yy), cx);
     }
-  }
-  const bool fast_a = sa.alive && na0 + RB <= max_it && (acc_a & 0x40000000u) == 0u;
-  const bool fast_b = sb.alive && nb0 + RB <= max_it && (acc_b & 0x40000000u) == 0u;
-  if (fast_a) {
-    sa.n = na0 + RB;
-    sa.alive = sa.n < max_it;
-  }
-  if (fast_b) {
-    sb.n = nb0 + RB;
-    sb.alive = sb.n < max_it;
+    fast_a = sa.alive && na0 + RB <= max_it && acc_a < 0x40000000u;
+    fast_b = sb.alive && nb0 + RB <= max_it && acc_b < 0x40000000u;
+    if (fast_a) {
+      sa.n = na0 + RB;
+      sa.alive = sa.n < max_it;
+    }
+    if (fast_b) {
+      sb.n = nb0 + RB;
+      sb.alive = sb.n < max_it;
+    }
   }
   bool live_a = sa.alive && !fast_a, live_b = sb.alive && !fast_b;
   if (__any_sync(kFull, live_a || live_b)) {
@@ -523,7 +586,7 @@ __device__ __forceinline__ void spec_block2(typename Pair<Real>::V& zx, typename
 
 constexpr uint32_t kSettle2 = 32;
 
-template <typename Real, int R, int MB, int RL = R>
+template <typename Real, int R, int MB, int RL = R, bool Tight = true>
 __global__ void __launch_bounds__(kThreads, MB)
     mandel_x2(const Viewport<Real> vp, const Real* __restrict__ tab, uint64_t first, uint64_t count,
               uint4* __restrict__ out, uint32_t* __restrict__ compact, unsigned* __restrict__ ctrl) {
@@ -605,7 +668,7 @@ __global__ void __launch_bounds__(kThreads, MB)
     // Speculative block on both slots (see mandel_persistent); long blocks
     // once every live pixel of the warp has settled.
     if (__all_sync(kFull, (!sa.alive || sa.n >= kSettle2) && (!sb.alive || sb.n >= kSettle2)))
-      spec_block2<Real, RL>(zx, zy, sa, sb, cx, cy, max_it);
+      spec_block2<Real, RL, Tight>(zx, zy, sa, sb, cx, cy, max_it);
     else
       spec_block2<Real, R>(zx, zy, sa, sb, cx, cy, max_it);
     if (sa.valid && !sa.alive) {
@@ -673,11 +736,11 @@ cudaError_t launch_real(const MandelParams& p, const LaunchEnv& env, uint64_t fi
   return cudaGetLastError();
 }
 
-template <typename Real, int R, int MB, int RL = R>
+template <typename Real, int R, int MB, int RL = R, bool Tight = true>
 cudaError_t launch_x2(const MandelParams& p, const LaunchEnv& env, uint64_t first, uint64_t count) {
   static int blocks_per_sm = 0;
   if (blocks_per_sm == 0) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, mandel_x2<Real, R, MB, RL>, kThreads, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, mandel_x2<Real, R, MB, RL, Tight>, kThreads, 0);
     if (e != cudaSuccess) return e;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
@@ -687,7 +750,7 @@ cudaError_t launch_x2(const MandelParams& p, const LaunchEnv& env, uint64_t firs
   uint64_t grid = static_cast<uint64_t>(env.sms) * static_cast<uint64_t>(blocks_per_sm);
   if (blocks_needed < grid) grid = blocks_needed;
   if (grid == 0) return cudaSuccess;
-  mandel_x2<Real, R, MB, RL><<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
+  mandel_x2<Real, R, MB, RL, Tight><<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
       vp, static_cast<const Real*>(env.scratch), first, count, static_cast<uint4*>(env.out[0]), env.compact,
       env.ctrl);
   return cudaGetLastError();
@@ -719,6 +782,8 @@ cudaError_t launch_mandelbrot(const KernelSpec& spec, const LaunchEnv& env, uint
       return v && std::atoi(v) == 1;
     }();
     const bool scalar = spec.variant >= 0 ? spec.variant == 1 : scalar_env;
+    // mandelbrot_f32@2: the default without the tight settled loop
+    if (spec.variant == 2) return launch_x2<float, 16, 4, 32, false>(spec.mandel, env, first, count);
     static const int mb = [] {  // ECL_MANDEL_F32_MB: resident CTAs per SM
       const char* v = std::getenv("ECL_MANDEL_F32_MB");
       return v ? std::atoi(v) : 0;

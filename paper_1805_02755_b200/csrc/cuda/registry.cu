@@ -112,7 +112,7 @@ int resolve_kernel(KernelSpec& s, std::string* err) {
     int max_variant = 0;  // per kind: the variants its launcher implements
     switch (s.kind) {
       case KernelKind::Mandelbrot: max_variant = 15; break;
-      case KernelKind::MandelbrotF32: max_variant = 1; break;
+      case KernelKind::MandelbrotF32: max_variant = 2; break;
       case KernelKind::Binomial: max_variant = 4; break;
       case KernelKind::NBody: max_variant = 1; break;
       case KernelKind::Ray: max_variant = 2; break;

@@ -284,7 +284,7 @@ def test_specialization_must_be_a_variant_of_the_program_kernel(gpu_available):
     assert e.value.code == P.ErrorCode.ConfigError
 
 
-@pytest.mark.parametrize("kernel", [f"mandelbrot@{v}" for v in range(16)] + ["mandelbrot_f32@0", "mandelbrot_f32@1"])
+@pytest.mark.parametrize("kernel", [f"mandelbrot@{v}" for v in range(16)] + ["mandelbrot_f32@0", "mandelbrot_f32@1", "mandelbrot_f32@2"])
 def test_every_mandelbrot_variant_is_bit_exact(gpu_available, oracle, kernel):
     # tuning variants selectable per device must all reproduce the reference
     w, h, it = 640, 480, 1000
