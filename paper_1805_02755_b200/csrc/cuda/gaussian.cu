@@ -496,7 +496,8 @@ cudaError_t launch_gaussian(const KernelSpec& spec, const LaunchEnv& env, uint64
   if (variant != 1 && !env.host_copies && (g.filter == 31 || g.filter == 15) && factor_filter(w, static_cast<int>(g.filter), &r, &c)) {
     // ECL_GAUSSIAN_TILE_ROWS: output rows per separable tile; measured at
     // 4096^2: 32 rows (5 CTAs/SM) 78 us, 64 rows (3 CTAs/SM, 1.47x instead of
-    // 1.94x horizontal rows per output row) 72 us
+    // 1.94x horizontal rows per output row) 72 us; also measured: 40 rows
+    // 77 us, 48 rows (4 CTAs/SM) 72, 56 rows 75, 96 rows 77, 128 rows 75
     static const int tall = [] {
       const char* v = std::getenv("ECL_GAUSSIAN_TILE_ROWS");
       return v ? std::atoi(v) : 64;
