@@ -114,13 +114,18 @@ __global__ void __launch_bounds__(kThreads)
     if (threadIdx.x == 0) {
       mbar_init(&bar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&bar, TH * 96 * 4);
     }
     __syncthreads();
-    if (threadIdx.x == 0) mbar_expect_tx(&bar, TH * 96 * 4);
-    __syncthreads();
-    if (threadIdx.x < TH) {
-      const int gy = tile_y - R + threadIdx.x;
-      bulk_g2s(&tile[threadIdx.x * kPitch], img + static_cast<int64_t>(gy) * W + (tile_x - 16), 96 * 4, &bar);
+    // One bulk copy per staged row.  The copy takes warp-uniform operands, so
+    // a warp issues its lanes' copies one after another: rows go round-robin
+    // over all warps (row = lane * warps + warp), not to the first TH threads.
+    {
+      const int rr = static_cast<int>(threadIdx.x & 31) * (kThreads / 32) + static_cast<int>(threadIdx.x >> 5);
+      if (rr < TH) {
+        const int gy = tile_y - R + rr;
+        bulk_g2s(&tile[rr * kPitch], img + static_cast<int64_t>(gy) * W + (tile_x - 16), 96 * 4, &bar);
+      }
     }
     mbar_wait(&bar, 0);
   } else {
@@ -216,14 +221,17 @@ struct SepTaps {
 
 constexpr int kHPitch = 68;  // horizontal-pass buffer pitch (floats): rows of 64 + 4 (bank spread)
 
-// One 64 x TO output tile per CTA (TO = 64: 63 KB of shared memory, 3 CTAs
-// per SM; the hardware overlaps one CTA's TMA rows with the others'
-// passes).  Measured and dropped: persistent CTAs with the input tile
-// double-buffered (prefetch of tile k+1 during tile k): 98 us with 32-row
-// tiles, 105 us with 64-row tiles, against 79 and 72 us.
+// One 64 x TO output tile per CTA.  Default (INPLACE): the horizontal pass
+// overwrites the staged tile, 37 KB of shared memory and 5 CTAs per SM
+// (register-limited) at TO = 64: 67-68 us at 4096^2 against 72-73 us with a
+// separate pass buffer (63 KB, 3 CTAs per SM; gaussian@2).  Measured and
+// dropped: persistent CTAs with the input tile double-buffered (prefetch of
+// tile k+1 during tile k; ncu: the TMA wait disappears, but 2-3 CTAs per SM
+// cannot keep the FMA pipe fed): round 2a 98 us (32-row tiles) and 105 us
+// (64-row), round 2b in place 82 us (64-row, 2 CTAs/SM), 89 (56), 94 (48).
 // The two passes of the separable kernel on one staged tile (all threads).
-template <int F, int TO>
-__device__ __forceinline__ void sep_hpass(const float* __restrict__ tile, float* __restrict__ hbuf,
+template <int F, int TO, bool INPLACE>
+__device__ __forceinline__ void sep_hpass(float* __restrict__ tile, float* __restrict__ hbuf,
                                           const SepTaps<F>& taps) {
   constexpr int R = F / 2;
   constexpr int TH = TO + F - 1;
@@ -231,17 +239,25 @@ __device__ __forceinline__ void sep_hpass(const float* __restrict__ tile, float*
   constexpr int SHIFT = (4 - R % 4) % 4;
   constexpr int NL = (SHIFT + NV + 3) / 4;
   constexpr int NP = (F - 1) / 2;
+  // in place, every thread runs every iteration (barriers inside): pad the
+  // segment count to whole CTA passes (the padding rows store nothing)
+  constexpr int NSEG = INPLACE ? (((TH + 7) & ~7) * 8 + kThreads - 1) / kThreads * kThreads : ((TH + 7) & ~7) * 8;
   // Horizontal pass: segment (row, s) = 8 outputs hbuf[row][8s .. 8s+7].
   // The 8 lanes of an LDS.128 phase take 8 consecutive rows of one segment
   // column: the 100-float tile pitch and the 68-float buffer pitch put them
-  // on disjoint banks (conflict-free loads and stores).
+  // on disjoint banks (conflict-free loads and stores).  INPLACE: the outputs
+  // overwrite the first 64 floats of their own tile row (one iteration's
+  // segments cover whole rows, 32 of them, and no other iteration reads
+  // those rows), after a barrier that orders every read of the rows before
+  // the first write — no separate buffer, 37 KB instead of 63 KB per CTA.
   const float2* wa = reinterpret_cast<const float2*>(taps.c);
   const float2* wb = reinterpret_cast<const float2*>(taps.cb);
 #pragma unroll 1
-  for (int seg = threadIdx.x; seg < ((TH + 7) & ~7) * 8; seg += kThreads) {
+  for (int seg = threadIdx.x; seg < NSEG; seg += kThreads) {
     const int row = (seg & 7) + 8 * (seg >> 6), s8 = (seg >> 3) & 7;
-    if (row >= TH) continue;
-    const float4* src = reinterpret_cast<const float4*>(tile + row * kPitch + (16 + 8 * s8 - R - SHIFT));
+    if (!INPLACE && row >= TH) continue;
+    const int lrow = row < TH ? row : TH - 1;  // padding rows (in-place only): read a real row, store nothing
+    const float4* src = reinterpret_cast<const float4*>(tile + lrow * kPitch + (16 + 8 * s8 - R - SHIFT));
     float2 ev[NL * 2];
 #pragma unroll
     for (int m = 0; m < NL; ++m) {
@@ -265,13 +281,16 @@ __device__ __forceinline__ void sep_hpass(const float* __restrict__ tile, float*
         for (int m = 0; m < NP; ++m) acc[b] = __ffma2_rn(wb[m], ev[(a0 + 1) / 2 + m], acc[b]);
       }
     }
-    float4* dst = reinterpret_cast<float4*>(hbuf + row * kHPitch + 8 * s8);
-    dst[0] = make_float4(acc[0].x + acc[0].y, acc[1].x + acc[1].y, acc[2].x + acc[2].y, acc[3].x + acc[3].y);
-    dst[1] = make_float4(acc[4].x + acc[4].y, acc[5].x + acc[5].y, acc[6].x + acc[6].y, acc[7].x + acc[7].y);
+    if (INPLACE) __syncthreads();
+    if (row < TH) {
+      float4* dst = reinterpret_cast<float4*>(INPLACE ? tile + row * kPitch + 8 * s8 : hbuf + row * kHPitch + 8 * s8);
+      dst[0] = make_float4(acc[0].x + acc[0].y, acc[1].x + acc[1].y, acc[2].x + acc[2].y, acc[3].x + acc[3].y);
+      dst[1] = make_float4(acc[4].x + acc[4].y, acc[5].x + acc[5].y, acc[6].x + acc[6].y, acc[7].x + acc[7].y);
+    }
   }
 }
 
-template <int F, int TO>
+template <int F, int TO, int HP>
 __device__ __forceinline__ void sep_vpass(const float* __restrict__ hbuf, float* __restrict__ out, int W, int H,
                                           uint64_t first, uint64_t count, int tile_x, int tile_y,
                                           const SepTaps<F>& taps) {
@@ -284,10 +303,10 @@ __device__ __forceinline__ void sep_vpass(const float* __restrict__ hbuf, float*
   float2 acc[VR];
 #pragma unroll
   for (int o = 0; o < VR; ++o) acc[o] = make_float2(0.f, 0.f);
-  const float* col = hbuf + y0 * kHPitch + 2 * lane;
+  const float* col = hbuf + y0 * HP + 2 * lane;
 #pragma unroll
   for (int i = 0; i < VR + F - 1; ++i) {
-    const float2 h = *reinterpret_cast<const float2*>(col + i * kHPitch);
+    const float2 h = *reinterpret_cast<const float2*>(col + i * HP);
 #pragma unroll
     for (int o = 0; o < VR; ++o) {
       const int tap = i - o;
@@ -296,11 +315,10 @@ __device__ __forceinline__ void sep_vpass(const float* __restrict__ hbuf, float*
   }
 
   const int gx = tile_x + 2 * lane;
-  if (gx >= W) return;
 #pragma unroll
   for (int o = 0; o < VR; ++o) {
     const int gy = tile_y + y0 + o;
-    if (gy >= H) break;
+    if (gx >= W || gy >= H) break;
     const uint64_t base = static_cast<uint64_t>(gy) * W + gx;
     float* dst = out + base;
     if (base >= first && base + 2 <= first + count && gx + 2 <= W && (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
@@ -312,7 +330,7 @@ __device__ __forceinline__ void sep_vpass(const float* __restrict__ hbuf, float*
   }
 }
 
-template <int F, int TO>
+template <int F, int TO, bool INPLACE>
 __global__ void __launch_bounds__(kThreads)
     gaussian_sep(const float* __restrict__ img, float* __restrict__ out, int W, int H, uint64_t first, uint64_t count,
                  int row0, const __grid_constant__ SepTaps<F> taps) {
@@ -331,13 +349,18 @@ __global__ void __launch_bounds__(kThreads)
     if (threadIdx.x == 0) {
       mbar_init(&bar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&bar, TH * 96 * 4);
     }
     __syncthreads();
-    if (threadIdx.x == 0) mbar_expect_tx(&bar, TH * 96 * 4);
-    __syncthreads();
-    if (threadIdx.x < TH) {
-      const int gy = tile_y - R + threadIdx.x;
-      bulk_g2s(&tile[threadIdx.x * kPitch], img + static_cast<int64_t>(gy) * W + (tile_x - 16), 96 * 4, &bar);
+    // One bulk copy per staged row.  The copy takes warp-uniform operands, so
+    // a warp issues its lanes' copies one after another: rows go round-robin
+    // over all warps (row = lane * warps + warp), not to the first TH threads.
+    {
+      const int rr = static_cast<int>(threadIdx.x & 31) * (kThreads / 32) + static_cast<int>(threadIdx.x >> 5);
+      if (rr < TH) {
+        const int gy = tile_y - R + rr;
+        bulk_g2s(&tile[rr * kPitch], img + static_cast<int64_t>(gy) * W + (tile_x - 16), 96 * 4, &bar);
+      }
     }
     mbar_wait(&bar, 0);
   } else {
@@ -349,14 +372,17 @@ __global__ void __launch_bounds__(kThreads)
     __syncthreads();
   }
 
-  sep_hpass<F, TO>(tile, hbuf, taps);
+  sep_hpass<F, TO, INPLACE>(tile, hbuf, taps);
   __syncthreads();
-  sep_vpass<F, TO>(hbuf, out, W, H, first, count, tile_x, tile_y, taps);
+  if (INPLACE)
+    sep_vpass<F, TO, kPitch>(tile, out, W, H, first, count, tile_x, tile_y, taps);
+  else
+    sep_vpass<F, TO, kHPitch>(hbuf, out, W, H, first, count, tile_x, tile_y, taps);
 }
 
-template <int F, int TO>
+template <int F, int TO, bool INPLACE>
 constexpr size_t sep_smem_bytes() {
-  return sizeof(float) * ((TO + F - 1) * kPitch + (TO + F - 1) * kHPitch);
+  return sizeof(float) * ((TO + F - 1) * kPitch + (INPLACE ? 0 : (TO + F - 1) * kHPitch));
 }
 
 // Factorisation of the F x F filter as r[i] c[j] (see gaussian_sep), or
@@ -402,7 +428,7 @@ bool factor_filter(const float* w, int F, const float** r, const float** c) {
   return cache.ok;
 }
 
-template <int F, int TO>
+template <int F, int TO, bool INPLACE>
 cudaError_t launch_sep(const GaussianParams& g, const LaunchEnv& env, const float* r, const float* c, uint64_t first,
                        uint64_t count) {
   SepTaps<F> taps;
@@ -411,7 +437,7 @@ cudaError_t launch_sep(const GaussianParams& g, const LaunchEnv& env, const floa
     taps.cb[j] = j + 1 < F ? c[j + 1] : 0.0f;
   }
   for (int i = 0; i < F; ++i) taps.r[i] = r[i];
-  constexpr size_t smem = sep_smem_bytes<F, TO>();
+  constexpr size_t smem = sep_smem_bytes<F, TO, INPLACE>();
   // the dynamic shared-memory limit is a per-device function attribute: set
   // it once on every device that launches this kernel (idempotent if two
   // device threads race)
@@ -419,14 +445,14 @@ cudaError_t launch_sep(const GaussianParams& g, const LaunchEnv& env, const floa
   const uint64_t bit = uint64_t{1} << (env.device & 63);
   if (!(attr_set.load(std::memory_order_relaxed) & bit)) {
     const cudaError_t e =
-        cudaFuncSetAttribute(gaussian_sep<F, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaFuncSetAttribute(gaussian_sep<F, TO, INPLACE>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     attr_set.fetch_or(bit, std::memory_order_relaxed);
   }
   const int row0 = static_cast<int>(first / g.width);
   const int row1 = static_cast<int>((first + count - 1) / g.width);
   const dim3 grid((g.width + kTileW - 1) / kTileW, (row1 - row0 + TO) / TO);
-  gaussian_sep<F, TO><<<grid, kThreads, smem, env.stream>>>(static_cast<const float*>(env.in[0]),
+  gaussian_sep<F, TO, INPLACE><<<grid, kThreads, smem, env.stream>>>(static_cast<const float*>(env.in[0]),
                                                         static_cast<float*>(env.out[0]), static_cast<int>(g.width),
                                                         static_cast<int>(g.height), first, count, row0, taps);
   return cudaGetLastError();
@@ -495,16 +521,30 @@ cudaError_t launch_gaussian(const KernelSpec& spec, const LaunchEnv& env, uint64
   const float *r = nullptr, *c = nullptr;
   if (variant != 1 && !env.host_copies && (g.filter == 31 || g.filter == 15) && factor_filter(w, static_cast<int>(g.filter), &r, &c)) {
     // ECL_GAUSSIAN_TILE_ROWS: output rows per separable tile; measured at
-    // 4096^2: 32 rows (5 CTAs/SM) 78 us, 64 rows (3 CTAs/SM, 1.47x instead of
-    // 1.94x horizontal rows per output row) 72 us; also measured: 40 rows
-    // 77 us, 48 rows (4 CTAs/SM) 72, 56 rows 75, 96 rows 77, 128 rows 75
+    // 4096^2 with the pass buffer (gaussian@2): 32 rows (5 CTAs/SM) 78 us,
+    // 64 rows (3 CTAs/SM, 1.47x instead of 1.94x horizontal rows per output
+    // row) 72 us; also 40 rows 77 us, 48 rows (4 CTAs/SM) 72, 56 rows 75,
+    // 96 rows 77, 128 rows 75.  In place (default): 32 rows 78 us, 64 rows
+    // 67-68, 96 rows 67-68, 128 rows 71.
+    // ECL_GAUSSIAN_SEP_INPLACE=0: the pass-buffer kernel (as gaussian@2).
     static const int tall = [] {
       const char* v = std::getenv("ECL_GAUSSIAN_TILE_ROWS");
       return v ? std::atoi(v) : 64;
     }();
-    if (g.filter == 31) return tall == 64 ? launch_sep<31, 64>(g, env, r, c, first, count)
-                                          : launch_sep<31, 32>(g, env, r, c, first, count);
-    return launch_sep<15, 32>(g, env, r, c, first, count);
+    static const int inplace = [] {
+      const char* v = std::getenv("ECL_GAUSSIAN_SEP_INPLACE");
+      return v ? std::atoi(v) : 1;
+    }();
+    if (g.filter == 31) {
+      if (variant == 2 || !inplace)
+        return tall == 64 ? launch_sep<31, 64, false>(g, env, r, c, first, count)
+                          : launch_sep<31, 32, false>(g, env, r, c, first, count);
+      if (tall == 128) return launch_sep<31, 128, true>(g, env, r, c, first, count);
+      if (tall == 96) return launch_sep<31, 96, true>(g, env, r, c, first, count);
+      return tall == 64 ? launch_sep<31, 64, true>(g, env, r, c, first, count)
+                        : launch_sep<31, 32, true>(g, env, r, c, first, count);
+    }
+    return launch_sep<15, 32, false>(g, env, r, c, first, count);
   }
   switch (g.filter) {
     case 3: return launch_tiled<3>(g, env, w, first, count);

@@ -116,7 +116,7 @@ int resolve_kernel(KernelSpec& s, std::string* err) {
       case KernelKind::Binomial: max_variant = 4; break;
       case KernelKind::NBody: max_variant = 1; break;
       case KernelKind::Ray: max_variant = 2; break;
-      case KernelKind::Gaussian: max_variant = 1; break;
+      case KernelKind::Gaussian: max_variant = 2; break;
       default: break;
     }
     if (s.variant > max_variant) {

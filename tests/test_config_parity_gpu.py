@@ -329,3 +329,19 @@ def test_gaussian_separable_path(gpu_available, oracle, w, h, f, kind):
     assert P.tiles_exactly(t.packages, prog.total_work_groups())
     exp = oracle.gaussian(img, filt, w, h, f)
     assert rel_err(out, exp).max() <= 1e-5
+
+
+@pytest.mark.parametrize("kernel", ["gaussian@0", "gaussian@2"], ids=["in-place", "pass-buffer"])
+def test_gaussian_separable_variants_full_image(gpu_available, oracle, kernel):
+    """Both separable kernels — the default whose horizontal pass overwrites
+    the staged tile, and gaussian@2 with a separate pass buffer — over the
+    full 4096^2 config image, resident, within 1e-5 of the oracle."""
+    w = h = 4096
+    f = 31
+    img, filt = W.gaussian_inputs(w, h, f, seed=11)
+    prog = P.validate_program(W.gaussian_spec(w, h, f))
+    out = np.empty(w * h, np.float32)
+    devs = [P.cuda_device("gpu0", 0, kernel=kernel)]
+    with P.Engine(P.EngineConfig(devs, P.StaticConfig()), prog) as e:
+        run_gaussian(e, img, filt, out, True)
+    assert rel_err(out, oracle.gaussian(img, filt, w, h, f)).max() <= 1e-5
