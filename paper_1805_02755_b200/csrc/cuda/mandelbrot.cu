@@ -32,6 +32,7 @@
 // the divergence of the irregular set costs at most R-1 idle iterations per
 // pixel instead of the warp-wide maximum.  Results are one uint4 per pixel:
 // the four identical counts of the reference's 4:1 pattern (:217-222).
+#include <atomic>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -717,12 +718,16 @@ Viewport<Real> make_viewport(const MandelParams& p) {
 template <typename Real, int R, int MB = kMinBlocks<Real>, int RL = R, uint32_t kSettle = 32, bool Periodic = false,
           bool Tight = true>
 cudaError_t launch_real(const MandelParams& p, const LaunchEnv& env, uint64_t first, uint64_t count) {
-  static int blocks_per_sm = 0;
+  // resident CTAs per SM: a property of the instantiation (device threads
+  // may race to fill it with the same value)
+  static std::atomic<int> occ{0};
+  int blocks_per_sm = occ.load(std::memory_order_relaxed);
   if (blocks_per_sm == 0) {
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &blocks_per_sm, mandel_persistent<Real, R, MB, RL, kSettle, Periodic, Tight>, kThreads, 0);
     if (e != cudaSuccess) return e;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
+    occ.store(blocks_per_sm, std::memory_order_relaxed);
   }
   const Viewport<Real> vp = make_viewport<Real>(p);
   const Real* tab = static_cast<const Real*>(env.scratch);
@@ -738,11 +743,13 @@ cudaError_t launch_real(const MandelParams& p, const LaunchEnv& env, uint64_t fi
 
 template <typename Real, int R, int MB, int RL = R, bool Tight = true>
 cudaError_t launch_x2(const MandelParams& p, const LaunchEnv& env, uint64_t first, uint64_t count) {
-  static int blocks_per_sm = 0;
+  static std::atomic<int> occ{0};
+  int blocks_per_sm = occ.load(std::memory_order_relaxed);
   if (blocks_per_sm == 0) {
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, mandel_x2<Real, R, MB, RL, Tight>, kThreads, 0);
     if (e != cudaSuccess) return e;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
+    occ.store(blocks_per_sm, std::memory_order_relaxed);
   }
   const Viewport<Real> vp = make_viewport<Real>(p);
   const uint64_t claims = (count + kTailChunk - 1) / kTailChunk;

@@ -17,6 +17,7 @@
 // deepest reflection.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -466,23 +467,30 @@ __global__ void __launch_bounds__(kThreads, MB)
 
 template <int MB>
 cudaError_t launch(const KernelSpec& spec, const LaunchEnv& env, uint64_t first, uint64_t count) {
-  static int blocks_per_sm = 0;
-  if (blocks_per_sm == 0) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ray_persistent<MB>, kThreads,
-                                                                  ray_smem_bytes(spec.ray.spheres));
-    if (e != cudaSuccess) return e;
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
-  const uint64_t chunks = (count + kChunk - 1) / kChunk;
-  const uint64_t blocks_needed = (chunks + kThreads / 32 - 1) / (kThreads / 32);
-  uint64_t grid = static_cast<uint64_t>(env.sms) * static_cast<uint64_t>(blocks_per_sm);
-  if (blocks_needed < grid) grid = blocks_needed;
+  // Resident CTAs per SM depend on the scene's shared memory: cached as
+  // (smem bytes << 8 | CTAs) for the last scene size seen (device threads
+  // may race to fill it; every writer stores the same value for a size).
+  static std::atomic<uint64_t> occ_cache{0};
   const size_t smem = ray_smem_bytes(spec.ray.spheres);
   if (smem > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(ray_persistent<MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
+  uint64_t cached = occ_cache.load(std::memory_order_relaxed);
+  int blocks_per_sm = static_cast<int>(cached & 0xffu);
+  if ((cached >> 8) != smem || blocks_per_sm == 0) {
+    const cudaError_t e =
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ray_persistent<MB>, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+    occ_cache.store((static_cast<uint64_t>(smem) << 8) | static_cast<uint64_t>(blocks_per_sm & 0xff),
+                    std::memory_order_relaxed);
+  }
+  const uint64_t chunks = (count + kChunk - 1) / kChunk;
+  const uint64_t blocks_needed = (chunks + kThreads / 32 - 1) / (kThreads / 32);
+  uint64_t grid = static_cast<uint64_t>(env.sms) * static_cast<uint64_t>(blocks_per_sm);
+  if (blocks_needed < grid) grid = blocks_needed;
   ray_persistent<MB><<<static_cast<unsigned>(grid), kThreads, smem, env.stream>>>(
       static_cast<const float4*>(env.in[0]), spec.ray.spheres, spec.ray.width, spec.ray.height, spec.ray.max_depth,
       static_cast<float4*>(env.out[0]), first, count, env.ctrl);
