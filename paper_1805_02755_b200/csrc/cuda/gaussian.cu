@@ -129,10 +129,18 @@ __global__ void __launch_bounds__(kThreads)
     }
     mbar_wait(&bar, 0);
   } else {
-    for (int k = threadIdx.x; k < TH * 96; k += kThreads) {
-      const int r = k / 96, c = k - r * 96;
-      const int gy = clampi(tile_y - R + r, 0, H - 1), gx = clampi(tile_x - 16 + c, 0, W - 1);
-      tile[r * kPitch + c] = img[static_cast<int64_t>(gy) * W + gx];
+    // border tile: clamp-to-edge loads, one warp per row (coalesced, the
+    // three column clamps hoisted out of the row loop)
+    {
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      int gx[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) gx[q] = clampi(tile_x - 16 + lane + 32 * q, 0, W - 1);
+      for (int r = warp; r < TH; r += kThreads / 32) {
+        const float* src = img + static_cast<int64_t>(clampi(tile_y - R + r, 0, H - 1)) * W;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) tile[r * kPitch + lane + 32 * q] = src[gx[q]];
+      }
     }
     __syncthreads();
   }
@@ -364,10 +372,18 @@ __global__ void __launch_bounds__(kThreads)
     }
     mbar_wait(&bar, 0);
   } else {
-    for (int k = threadIdx.x; k < TH * 96; k += kThreads) {
-      const int r = k / 96, c = k - r * 96;
-      const int gy = clampi(tile_y - R + r, 0, H - 1), gx = clampi(tile_x - 16 + c, 0, W - 1);
-      tile[r * kPitch + c] = img[static_cast<int64_t>(gy) * W + gx];
+    // border tile: clamp-to-edge loads, one warp per row (coalesced, the
+    // three column clamps hoisted out of the row loop)
+    {
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      int gx[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) gx[q] = clampi(tile_x - 16 + lane + 32 * q, 0, W - 1);
+      for (int r = warp; r < TH; r += kThreads / 32) {
+        const float* src = img + static_cast<int64_t>(clampi(tile_y - R + r, 0, H - 1)) * W;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) tile[r * kPitch + lane + 32 * q] = src[gx[q]];
+      }
     }
     __syncthreads();
   }
