@@ -163,6 +163,12 @@ def test_nbody_step_matches_oracle(gpu_available, oracle, n, n_dev, sched):
     epos, evel = oracle.nbody_step(pos, vel, 0.005, 500.0)
     ok, worst = rel_close(npos, epos, 1e-4)
     assert ok, f"positions max rel err {worst}"
+    # positions through the displacement p' - p (= a dt^2 / 2 from rest),
+    # which is what the step computes; the f32 store of p' adds <= 1 ulp
+    d_got = npos[:, :3].astype(np.float64) - pos[:, :3]
+    d_exp = epos[:, :3].astype(np.float64) - pos[:, :3]
+    bound = 1e-4 * np.linalg.norm(d_exp, axis=1)[:, None] + 2 * np.spacing(np.abs(epos[:, :3])).astype(np.float64)
+    assert (np.abs(d_got - d_exp) <= bound).all(), float((np.abs(d_got - d_exp) - bound).max())
     # velocities start at 0, so they are pure acc*dt: compare against the
     # scale of the field (f32 accumulation over n terms)
     scale = float(np.abs(evel[:, :3]).max())
