@@ -1000,11 +1000,14 @@ def bench_engine(args, n, wl, P, N, np, torch, barrier, max_over_ranks, shared, 
             spec0 = prog.spec()
             if wl.name.startswith("mandelbrot"):
                 wms = ctypes.c_double(0.0)
-                N.lib.ecl_probe_host_widen(spec0.global_work_size, 4, ctypes.byref(wms))
+                # counts < 65536 cross PCIe as uint16 (1/8 of the output bytes), else uint32 (1/4)
+                share = 8.0 if wl.ITERS < 65536 else 4.0
+                N.lib.ecl_probe_host_widen_width(spec0.global_work_size, 4, 2 if share == 8.0 else 4,
+                                                 ctypes.byref(wms))
                 floor["host_widen_ms"] = wms.value
-                floor["e2e_floor_ms"] = max(pcie_ms / 4.0, wms.value)
-                floor["basis"] = ("compact counts cross PCIe (1/4 of the output bytes) and the host widens them "
-                                  "4:1 into the caller's buffer: max(PCIe at N links, host widening), and the "
+                floor["e2e_floor_ms"] = max(pcie_ms / share, wms.value)
+                floor["basis"] = (f"compact counts cross PCIe (1/{share:.0f} of the output bytes) and the host widens "
+                                  "them 4:1 into the caller's buffer: max(PCIe at N links, host widening), and the "
                                   "host widening is shared by all N GPUs, so end-to-end scaling flattens at it")
             else:
                 floor["e2e_floor_ms"] = pcie_ms

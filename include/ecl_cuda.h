@@ -273,6 +273,9 @@ int ecl_probe_mandel_mix_f32(int ordinal, double* tflops);
  * between host buffers on the widen pool's thread count — the host-DRAM floor
  * of end-to-end runs with replicated outputs (Mandelbrot). */
 int ecl_probe_host_widen(uint64_t items, uint32_t replicate, double* ms);
+/* The same from `src_bytes`-byte values (2: the 16-bit compact counts of a
+ * program whose counts fit 16 bits, 4: as above). */
+int ecl_probe_host_widen_width(uint64_t items, uint32_t replicate, uint32_t src_bytes, double* ms);
 
 const char* ecl_last_error(void);
 

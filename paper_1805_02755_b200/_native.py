@@ -90,6 +90,7 @@ _sig("ecl_kernel_is_plugin", c_int, c_char_p)
 _sig("ecl_engine_run_kernel", c_int, c_void_p, c_char_p, PVOID, c_u32, PVOID, c_u32)
 _sig("ecl_peer_access", c_int, c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int))
 _sig("ecl_probe_host_widen", c_int, c_u64, c_u32, ctypes.POINTER(c_dbl))
+_sig("ecl_probe_host_widen_width", c_int, c_u64, c_u32, c_u32, ctypes.POINTER(c_dbl))
 _sig("ecl_probe_vector_peaks", c_int, c_int, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl))
 
 ERROR_NAMES = [

@@ -773,7 +773,12 @@ int ecl_peer_access(int dst, int src, int* can_access, int* enabled) {
 }
 
 int ecl_probe_host_widen(uint64_t items, uint32_t replicate, double* ms) {
-  *ms = ecl::widen_probe_ms(items, replicate);
+  return ecl_probe_host_widen_width(items, replicate, 4, ms);
+}
+
+int ecl_probe_host_widen_width(uint64_t items, uint32_t replicate, uint32_t src_bytes, double* ms) {
+  if (src_bytes != 2 && src_bytes != 4) return fail(ECL_CONFIG_ERROR, "widen probe: src_bytes must be 2 or 4");
+  *ms = ecl::widen_probe_ms(items, replicate, src_bytes);
   return *ms >= 0.0 ? ECL_OK : fail(ECL_CONFIG_ERROR, "widen probe: allocation failed");
 }
 
@@ -875,8 +880,8 @@ static int stream_inputs_for(ecl_gpu* g, const ecl::KernelSpec& s, uint64_t firs
   return ECL_OK;
 }
 
-// The compact copies of one piece (items [first, first+count), one uint32
-// each) on copy stream `cp`, and the host widening of each into `dst` (the
+// The compact copies of one piece (items [first, first+count), one value of
+// s.compact_bytes each) on copy stream `cp`, and the host widening of each into `dst` (the
 // piece's slice of the caller's output, `replicate` values per item).  The
 // copy may go in chunks (ECL_WIDEN_CHUNK), each widened as soon as it lands;
 // measured on the 16-core Xeon host: 2^20-item chunks = whole pieces (54.5
@@ -885,9 +890,10 @@ static int stream_inputs_for(ecl_gpu* g, const ecl::KernelSpec& s, uint64_t firs
 static int enqueue_compact_copies(ecl_gpu* g, Slot& slot, const ecl::KernelSpec& s, uint64_t first, uint64_t count,
                                   uint32_t* dst, cudaStream_t cp, size_t* piece_no) {
   const uint64_t chunk = g->ring ? g->ring_items : g->widen_chunk_items;
+  const uint32_t cb = s.compact_bytes;  // 2: 16-bit counts
   for (uint64_t c0 = 0; c0 < count; c0 += chunk) {
     const uint64_t cn = std::min(chunk, count - c0);
-    uint32_t* land = g->compact_host ? g->compact_host + first + c0 : nullptr;
+    char* land = g->compact_host ? reinterpret_cast<char*>(g->compact_host) + (first + c0) * cb : nullptr;
     uint32_t* release = nullptr;
     uint32_t release_value = 0;
     if (g->ring) {  // next staging slot, once its previous contents are widened
@@ -897,11 +903,12 @@ static int enqueue_compact_copies(ecl_gpu* g, Slot& slot, const ecl::KernelSpec&
       const unsigned long long flag = reinterpret_cast<unsigned long long>(g->ring_released_dev) + 4ull * r;
       if (wait_value_fn()(cp, flag, uses, 0 /* CU_STREAM_WAIT_VALUE_GEQ */) != 0)
         return fail(ECL_KERNEL_PANIC, "staging ring: stream wait failed");
-      land = g->ring + static_cast<uint64_t>(r) * g->ring_items;
+      land = reinterpret_cast<char*>(g->ring + static_cast<uint64_t>(r) * g->ring_items);
       release = g->ring_released + r;
       release_value = uses + 1;
     }
-    ECL_CK(cudaMemcpyAsync(land, g->compact_dev + first + c0, cn * sizeof(uint32_t), cudaMemcpyDeviceToHost, cp));
+    ECL_CK(cudaMemcpyAsync(land, reinterpret_cast<const char*>(g->compact_dev) + (first + c0) * cb, cn * cb,
+                           cudaMemcpyDeviceToHost, cp));
     if (slot.piece_done.size() <= *piece_no) {
       cudaEvent_t ev;
       // blocking-sync: widen workers sleep on it instead of spinning a core
@@ -910,7 +917,7 @@ static int enqueue_compact_copies(ecl_gpu* g, Slot& slot, const ecl::KernelSpec&
     }
     cudaEvent_t ev = slot.piece_done[(*piece_no)++];
     ECL_CK(cudaEventRecord(ev, cp));
-    ecl::widen_async(g->ordinal, ev, land, dst + c0 * s.replicate, cn, s.replicate, &slot.widen, release,
+    ecl::widen_async(g->ordinal, ev, land, cb, dst + c0 * s.replicate, cn, s.replicate, &slot.widen, release,
                      release_value);
   }
   return ECL_OK;
@@ -983,7 +990,10 @@ int ecl_gpu_submit(ecl_gpu* g, uint64_t seq, uint64_t offset_wg, uint64_t size_w
     cudaStream_t st = g->lane[pl];
     cudaStream_t cp = g->copy[pl];
     ecl::LaunchEnv env = env_of(g, pl);
-    if (widen) env.compact = g->compact_dev;
+    if (widen) {
+      env.compact = g->compact_dev;
+      env.compact_bytes = s.compact_bytes;
+    }
     env.host_copies = copies;
     const uint64_t n_wg = std::min(piece_wg, offset_wg + size_wg - wg);
     const uint64_t first = wg * s.lws, count = n_wg * s.lws;

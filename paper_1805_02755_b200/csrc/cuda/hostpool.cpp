@@ -3,13 +3,16 @@
 // The Mandelbrot kernel writes four identical uint32 counts per work-item
 // (the reference's 4:1 out pattern, workloads.hpp:217-222).  Shipping all
 // four over PCIe costs 16 B/pixel (4 GiB at the config, ~75 ms at 57 GB/s);
-// the device layer instead copies the one count per pixel (4 B/pixel) into
+// the device layer instead copies the one count per pixel (2 B/pixel when
+// max_iter < 65536, else 4) into
 // page-locked staging slots (device.cu ring_setup) and this pool widens
 // every piece into the caller's buffer as soon as its copy has landed, with
 // non-temporal 128-bit stores on all host cores, overlapped with the
 // remaining kernels and copies.  The caller's buffer ends up byte-identical to a full D2H.
 #include <cuda_runtime.h>
 #include <immintrin.h>
+
+#include <sys/mman.h>
 
 #include <algorithm>
 #include <chrono>
@@ -30,7 +33,8 @@ namespace {
 struct Job {
   int device;
   cudaEvent_t ready;
-  const uint32_t* src;
+  const void* src;
+  uint32_t src_bytes;  // 4, or 2 (16-bit compact values)
   uint32_t* dst;
   uint64_t count;
   uint32_t rep;
@@ -56,6 +60,31 @@ __attribute__((target("avx512f"))) void widen4_avx512(const uint32_t* src, uint3
   for (; i < count; ++i)
     _mm_stream_si128(reinterpret_cast<__m128i*>(dst + 4 * i), _mm_set1_epi32(static_cast<int>(src[i])));
   _mm_sfence();
+}
+
+// The same from 16-bit values: half the source bytes (the staging copies and
+// their reads), the destination stores unchanged.
+__attribute__((target("avx512f"))) void widen4_u16_avx512(const uint16_t* src, uint32_t* dst, uint64_t count) {
+  uint64_t i = 0;
+  for (; i < count && (reinterpret_cast<uintptr_t>(dst + 4 * i) & 63) != 0; ++i)
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + 4 * i), _mm_set1_epi32(static_cast<int>(src[i])));
+  const __m512i idx = _mm512_set_epi32(3, 3, 3, 3, 2, 2, 2, 2, 1, 1, 1, 1, 0, 0, 0, 0);
+  for (; i + 4 <= count; i += 4) {
+    const __m128i w = _mm_cvtepu16_epi32(_mm_loadl_epi64(reinterpret_cast<const __m128i*>(src + i)));
+    _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + 4 * i), _mm512_permutexvar_epi32(idx, _mm512_castsi128_si512(w)));
+  }
+  for (; i < count; ++i)
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + 4 * i), _mm_set1_epi32(static_cast<int>(src[i])));
+  _mm_sfence();
+}
+
+void widen16(const uint16_t* src, uint32_t* dst, uint64_t count, uint32_t rep) {
+  if (rep == 4 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && __builtin_cpu_supports("avx512f")) {
+    widen4_u16_avx512(src, dst, count);
+    return;
+  }
+  for (uint64_t i = 0; i < count; ++i)
+    for (uint32_t r = 0; r < rep; ++r) dst[i * rep + r] = src[i];
 }
 
 void widen(const uint32_t* src, uint32_t* dst, uint64_t count, uint32_t rep) {
@@ -110,7 +139,7 @@ class Pool {
     std::vector<Job> parts;
     for (uint64_t o = 0; o < j.count; o += sub) {
       Job p = j;
-      p.src = j.src + o;
+      p.src = static_cast<const char*>(j.src) + o * j.src_bytes;
       p.dst = j.dst + o * j.rep;
       p.count = std::min(sub, j.count - o);
       parts.push_back(p);
@@ -155,7 +184,10 @@ class Pool {
         cudaGetLastError();
         j.ticket->failed.store(true);
       } else {
-        widen(j.src, j.dst, j.count, j.rep);
+        if (j.src_bytes == 2)
+          widen16(static_cast<const uint16_t*>(j.src), j.dst, j.count, j.rep);
+        else
+          widen(static_cast<const uint32_t*>(j.src), j.dst, j.count, j.rep);
       }
       if (j.release) __atomic_store_n(j.release, j.release_value, __ATOMIC_RELEASE);
       {
@@ -182,28 +214,40 @@ Pool& pool() {
 
 }  // namespace
 
-void widen_async(int device, cudaEvent_t ready, const uint32_t* src, uint32_t* dst, uint64_t count, uint32_t rep,
-                 WidenTicket* ticket, uint32_t* release, uint32_t release_value) {
-  pool().submit(Job{device, ready, src, dst, count, rep, ticket, release, release_value});
+void widen_async(int device, cudaEvent_t ready, const void* src, uint32_t src_bytes, uint32_t* dst, uint64_t count,
+                 uint32_t rep, WidenTicket* ticket, uint32_t* release, uint32_t release_value) {
+  pool().submit(Job{device, ready, src, src_bytes == 2 ? 2u : 4u, dst, count, rep, ticket, release, release_value});
 }
 
 unsigned widen_workers() { return pool().size(); }
 
-double widen_probe_ms(uint64_t items, uint32_t rep) {
+double widen_probe_ms(uint64_t items, uint32_t rep, uint32_t src_bytes) {
   // The pool's own arithmetic and thread count on fresh huge-page buffers,
   // without the CUDA event gating: what host DRAM sustains for widening.
   const unsigned n = std::max(1u, pool().size());
   std::vector<uint32_t> src(items);
+  std::vector<uint16_t> src16(src_bytes == 2 ? items : 0);
   for (uint64_t i = 0; i < items; ++i) src[i] = static_cast<uint32_t>(i);
-  void* raw = nullptr;
-  if (posix_memalign(&raw, 1 << 21, items * rep * sizeof(uint32_t)) != 0) return -1.0;
+  for (uint64_t i = 0; i < src16.size(); ++i) src16[i] = static_cast<uint16_t>(i);
+  // destination on transparent huge pages, like the page-locked output
+  // buffers callers hand the engine (device.cu pinned_alloc)
+  const size_t huge = size_t{2} << 20;
+  const size_t len = (items * rep * sizeof(uint32_t) + huge - 1) / huge * huge;
+  void* raw = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (raw == MAP_FAILED) return -1.0;
+  madvise(raw, len, MADV_HUGEPAGE);
   auto* dst = static_cast<uint32_t*>(raw);
   auto pass = [&] {
     std::vector<std::thread> ts;
     const uint64_t per = (items + n - 1) / n;
     for (unsigned t = 0; t < n; ++t) {
       const uint64_t a = std::min<uint64_t>(items, t * per), b = std::min<uint64_t>(items, a + per);
-      ts.emplace_back([&, a, b] { widen(src.data() + a, dst + a * rep, b - a, rep); });
+      ts.emplace_back([&, a, b] {
+        if (src_bytes == 2)
+          widen16(src16.data() + a, dst + a * rep, b - a, rep);
+        else
+          widen(src.data() + a, dst + a * rep, b - a, rep);
+      });
     }
     for (auto& t : ts) t.join();
   };
@@ -211,7 +255,7 @@ double widen_probe_ms(uint64_t items, uint32_t rep) {
   const auto t0 = std::chrono::steady_clock::now();
   pass();
   const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  free(raw);
+  munmap(raw, len);
   return ms;
 }
 

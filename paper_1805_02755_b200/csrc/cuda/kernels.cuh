@@ -60,6 +60,10 @@ struct KernelSpec {
   // (Mandelbrot's 4:1 pattern); the kernel also writes one compact value per
   // item (LaunchEnv::compact) so host copies move 1/replicate of the bytes.
   uint32_t replicate = 1;
+  // Bytes per compact value: 2 when every value fits 16 bits (Mandelbrot
+  // counts with max_iterations < 65536), halving the compact D2H copies and
+  // the host's reads of them; 4 otherwise.
+  uint32_t compact_bytes = 4;
   // > 0: even with resident outputs a package runs as sub-launches of about
   // this many work-items alternating over the device's two compute lanes.
   // Set for kernels whose single long launch is measurably slower than the
@@ -93,6 +97,7 @@ struct LaunchEnv {
   unsigned* ctrl = nullptr;    // zeroed per-device control words (work counters)
   void* scratch = nullptr;     // per-device, per-binding kernel scratch (scratch_bytes())
   uint32_t* compact = nullptr;  // replicate > 1 and host copies pending: one value per item
+  uint32_t compact_bytes = 4;   // KernelSpec::compact_bytes: 2 = the values are stored as uint16
   int device = 0;               // CUDA ordinal
   // Host mirrors of the inputs host_mirrored_input() names (nullptr for the
   // others): small inputs a launcher passes by value in its parameters.
@@ -108,6 +113,21 @@ struct LaunchEnv {
 };
 
 constexpr uint32_t kMaxPeerWrites = 8;  // peers a fused-exchange kernel writes to
+
+// The compact output a replicating kernel writes (LaunchEnv::compact,
+// compact_bytes): one value per item, 16- or 32-bit.
+struct CompactOut {
+  void* p = nullptr;
+  uint32_t bytes = 4;
+  __host__ __device__ explicit operator bool() const { return p != nullptr; }
+  __device__ __forceinline__ void put(uint64_t i, uint32_t v) const {
+    if (bytes == 2)
+      static_cast<uint16_t*>(p)[i] = static_cast<uint16_t>(v);
+    else
+      static_cast<uint32_t*>(p)[i] = v;
+  }
+};
+inline CompactOut compact_of(const LaunchEnv& env) { return CompactOut{env.compact, env.compact_bytes}; }
 
 // Device scratch a kernel needs per binding (e.g. Mandelbrot coordinate tables),
 // filled once by prepare_kernel when the program is bound to a device.

@@ -246,7 +246,7 @@ template <typename Real, int R, int MB = kMinBlocks<Real>, int RL = R, uint32_t 
           bool Tight = true>
 __global__ void __launch_bounds__(kThreads, MB)
     mandel_persistent(const Viewport<Real> vp, const Real* __restrict__ tab, uint64_t first, uint64_t count,
-                      uint4* __restrict__ out, uint32_t* __restrict__ compact, unsigned* __restrict__ ctrl) {
+                      uint4* __restrict__ out, const CompactOut compact, unsigned* __restrict__ ctrl) {
   using A = Arith<Real>;
   using Bits = typename A::Bits;
   const unsigned lane = threadIdx.x & 31u;
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, MB)
     }
     if (valid && !alive) {
       out[idx] = make_uint4(n, n, n, n);
-      if (compact) compact[idx] = n;  // host-bound copy: one count per pixel
+      if (compact) compact.put(idx, n);  // host-bound copy: one count per pixel
       valid = false;
     }
   }
@@ -590,7 +590,7 @@ constexpr uint32_t kSettle2 = 32;
 template <typename Real, int R, int MB, int RL = R, bool Tight = true>
 __global__ void __launch_bounds__(kThreads, MB)
     mandel_x2(const Viewport<Real> vp, const Real* __restrict__ tab, uint64_t first, uint64_t count,
-              uint4* __restrict__ out, uint32_t* __restrict__ compact, unsigned* __restrict__ ctrl) {
+              uint4* __restrict__ out, const CompactOut compact, unsigned* __restrict__ ctrl) {
   using A = Pair<Real>;
   using V = typename A::V;
   const unsigned lane = threadIdx.x & 31u;
@@ -674,12 +674,12 @@ __global__ void __launch_bounds__(kThreads, MB)
       spec_block2<Real, R>(zx, zy, sa, sb, cx, cy, max_it);
     if (sa.valid && !sa.alive) {
       out[sa.idx] = make_uint4(sa.n, sa.n, sa.n, sa.n);
-      if (compact) compact[sa.idx] = sa.n;
+      if (compact) compact.put(sa.idx, sa.n);
       sa.valid = false;
     }
     if (sb.valid && !sb.alive) {
       out[sb.idx] = make_uint4(sb.n, sb.n, sb.n, sb.n);
-      if (compact) compact[sb.idx] = sb.n;
+      if (compact) compact.put(sb.idx, sb.n);
       sb.valid = false;
     }
   }
@@ -737,7 +737,7 @@ cudaError_t launch_real(const MandelParams& p, const LaunchEnv& env, uint64_t fi
   if (blocks_needed < grid) grid = blocks_needed;
   if (grid == 0) return cudaSuccess;
   mandel_persistent<Real, R, MB, RL, kSettle, Periodic, Tight><<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
-      vp, tab, first, count, static_cast<uint4*>(env.out[0]), env.compact, env.ctrl);
+      vp, tab, first, count, static_cast<uint4*>(env.out[0]), compact_of(env), env.ctrl);
   return cudaGetLastError();
 }
 
@@ -758,7 +758,7 @@ cudaError_t launch_x2(const MandelParams& p, const LaunchEnv& env, uint64_t firs
   if (blocks_needed < grid) grid = blocks_needed;
   if (grid == 0) return cudaSuccess;
   mandel_x2<Real, R, MB, RL, Tight><<<static_cast<unsigned>(grid), kThreads, 0, env.stream>>>(
-      vp, static_cast<const Real*>(env.scratch), first, count, static_cast<uint4*>(env.out[0]), env.compact,
+      vp, static_cast<const Real*>(env.scratch), first, count, static_cast<uint4*>(env.out[0]), compact_of(env),
       env.ctrl);
   return cudaGetLastError();
 }

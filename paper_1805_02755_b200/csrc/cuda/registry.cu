@@ -154,6 +154,7 @@ int resolve_kernel(KernelSpec& s, std::string* err) {
         return bad(err, "mandelbrot: width, height and max_iterations must be positive");
       if (w * h != s.gws) return bad(err, "mandelbrot: width*height must equal global_work_size");
       s.replicate = 4;  // four identical counts per pixel (workloads.hpp:217-222)
+      s.compact_bytes = s.mandel.max_iterations < 65536u ? 2 : 4;  // a count is <= max_iterations
       return ECL_OK;
     }
     case KernelKind::Synthetic:
