@@ -25,6 +25,7 @@
 // scalar full lattice (binomial@1).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -385,12 +386,63 @@ __device__ __forceinline__ float2 warp_lattice(const float2* leaves_buf, int ste
   return phases<32, kNodesPerLane, float2, 32, U>(c, steps, r, s, buf, lane);
 }
 
+// Option records computed ahead (default; binomial@5 keeps the setup inside
+// the lattice kernel): one thread per option runs
+// option_params once, instead of eight lanes per option inside the lattice
+// kernel (its FP64 setup was ~7 % of the lattice kernel's instructions,
+// each FP64 instruction holding an issue slot two cycles).  Same function,
+// same arguments: the records are bit-identical to the in-kernel ones.
+// 12.69 -> 11.71 ms at 8M x 254 including the setup launch (64 B per option
+// through HBM, 0.5 GB written and read back).  Two earlier attempts at one
+// setup per option *inside* the lattice kernel (32-option chunks, records in
+// shared memory) lost to register pressure (12.79, 13.50 ms); here the
+// lattice kernel only loads finished records.
+struct __align__(16) OptionRec {
+  double K, base, f, u2, tail;
+  float r, s;
+  int t0, pad;
+};
+
+__global__ void __launch_bounds__(256)
+    binomial_setup(const float* __restrict__ rand, OptionRec* __restrict__ recs, int steps, uint64_t first_opt,
+                   uint64_t n_opt) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n_opt; i += stride) {
+    const Option o = option_params<32, kNodesPerLane>(rand[first_opt + i], steps);
+    OptionRec rec;
+    rec.K = o.K;
+    rec.base = o.base;
+    rec.f = o.f;
+    rec.u2 = o.u2;
+    rec.tail = o.tail;
+    rec.r = o.r;
+    rec.s = o.s;
+    rec.t0 = o.t0;
+    rec.pad = 0;
+    recs[first_opt + i] = rec;
+  }
+}
+
+__device__ __forceinline__ Option load_option(const OptionRec* __restrict__ recs, uint64_t i) {
+  const OptionRec rec = recs[i];
+  Option o;
+  o.K = rec.K;
+  o.base = rec.base;
+  o.f = rec.f;
+  o.u2 = rec.u2;
+  o.tail = rec.tail;
+  o.r = rec.r;
+  o.s = rec.s;
+  o.t0 = rec.t0;
+  return o;
+}
+
 // U: unroll of the level loops (code size: the kernel is instruction-fetch
 // sensitive, see half_lattice).
-template <int MB, int U>
+template <int MB, int U, bool PRE = false>
 __global__ void __launch_bounds__(kThreads, MB)
     binomial_hw(const float* __restrict__ rand, float* __restrict__ out, int steps, uint64_t first_opt,
-                uint64_t n_opt) {
+                uint64_t n_opt, const OptionRec* __restrict__ recs) {
   // per warp: the leaves of its two pairs (full 32 x 8 layout), then each
   // pair's window / repack buffer
   __shared__ float2 pair_buf[kThreads / 32][2][32 * kNodesPerLane];
@@ -406,7 +458,8 @@ __global__ void __launch_bounds__(kThreads, MB)
     const uint64_t left = first_opt + n_opt - o;  // options of this group that exist (>= 1)
     // Lanes 8q..8q+7 set up option o+q (missing options repeat option o).
     const unsigned q = lane >> 3;
-    const Option mine = option_params<32, kNodesPerLane>(rand[o + (q < left ? q : 0)], steps);
+    const Option mine = PRE ? load_option(recs, o + (q < left ? q : 0))
+                            : option_params<32, kNodesPerLane>(rand[o + (q < left ? q : 0)], steps);
     const int tw = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(mine.t0)));
     // Only the lattice's inputs stay in registers across it: the tails wait
     // in shared memory, each pair's (pu/pd, pd^32) is re-read from its lanes.
@@ -449,16 +502,26 @@ __global__ void __launch_bounds__(kThreads, MB)
   }
 }
 
-template <int MB, int U>
+template <int MB, int U, bool PRE = false>
 cudaError_t launch_hw(const KernelSpec& spec, const LaunchEnv& env, uint64_t first_opt, uint64_t n_opt) {
   const uint64_t warps_per_block = kThreads / 32;
   const uint64_t groups = (n_opt + 3) / 4;
   uint64_t blocks = (groups + warps_per_block - 1) / warps_per_block;
   const uint64_t cap = static_cast<uint64_t>(env.sms) * 8 * 16;  // measured: a persistent grid (1 wave) 13.3 ms vs 12.7
   if (blocks > cap) blocks = cap;
-  binomial_hw<MB, U><<<static_cast<unsigned>(blocks), kThreads, 0, env.stream>>>(
+  OptionRec* recs = nullptr;
+  if (PRE) {
+    recs = static_cast<OptionRec*>(env.scratch);
+    if (!recs) return cudaErrorInvalidValue;
+    const uint64_t sb = std::min<uint64_t>((n_opt + 255) / 256, static_cast<uint64_t>(env.sms) * 16);
+    binomial_setup<<<static_cast<unsigned>(sb), 256, 0, env.stream>>>(static_cast<const float*>(env.in[0]), recs,
+                                                                      static_cast<int>(spec.binom.steps), first_opt,
+                                                                      n_opt);
+    if (env.extra_launches) ++*env.extra_launches;
+  }
+  binomial_hw<MB, U, PRE><<<static_cast<unsigned>(blocks), kThreads, 0, env.stream>>>(
       static_cast<const float*>(env.in[0]), static_cast<float*>(env.out[0]), static_cast<int>(spec.binom.steps),
-      first_opt, n_opt);
+      first_opt, n_opt, recs);
   return cudaGetLastError();
 }
 
@@ -549,7 +612,9 @@ cudaError_t launch_binomial(const KernelSpec& spec, const LaunchEnv& env, uint64
     return v ? std::atoi(v) : 0;
   }();
   // Variants (all bit-identical; times at the 8M x 254 config, one launch):
-  //   0  binomial_hw: half-warp pairs + zero window      12.69 ms (MB 6, unroll 4)
+  //   0  binomial_setup + binomial_hw: option records     11.71 ms
+  //      computed ahead, one thread per option; half-warp pairs + zero window
+  //   5  binomial_hw with the option setup inside it      12.69 ms (MB 6, unroll 4)
   //   1  scalar full lattice, one option per warp         20.2 ms
   //   2  half-warp pairs, 16 nodes per lane, full lattice 18.8 ms
   //   3  packed pair per warp, full lattice (round 1)     17.5 ms
@@ -572,18 +637,22 @@ cudaError_t launch_binomial(const KernelSpec& spec, const LaunchEnv& env, uint64
       }
     case 3: return launch<2, 4, false>(spec, env, first_opt, n_opt);
     case 4: return launch<2, 4>(spec, env, first_opt, n_opt);
+    case 5: return launch_hw<6, 4, false>(spec, env, first_opt, n_opt);  // option setup inside the lattice kernel
     default:
-      // measured (MB, unroll): (4,2) 13.57, (4,4) 12.93, (5,2) 12.97,
-      // (5,4) 12.84, (6,2) 12.69, (6,4) 12.69 ms
+      // measured with the setup inside the lattice kernel (MB, unroll):
+      // (4,2) 13.57, (4,4) 12.93, (5,2) 12.97, (5,4) 12.84, (6,2) 12.69,
+      // (6,4) 12.69 ms; with the records computed ahead (default) 11.71 ms
       switch ((mb ? mb : 6) * 10 + hw_unroll) {
-        case 42: return launch_hw<4, 2>(spec, env, first_opt, n_opt);
-        case 44: return launch_hw<4, 4>(spec, env, first_opt, n_opt);
-        case 52: return launch_hw<5, 2>(spec, env, first_opt, n_opt);
-        case 54: return launch_hw<5, 4>(spec, env, first_opt, n_opt);
-        case 62: return launch_hw<6, 2>(spec, env, first_opt, n_opt);
-        default: return launch_hw<6, 4>(spec, env, first_opt, n_opt);
+        case 42: return launch_hw<4, 2, true>(spec, env, first_opt, n_opt);
+        case 44: return launch_hw<4, 4, true>(spec, env, first_opt, n_opt);
+        case 52: return launch_hw<5, 2, true>(spec, env, first_opt, n_opt);
+        case 54: return launch_hw<5, 4, true>(spec, env, first_opt, n_opt);
+        case 62: return launch_hw<6, 2, true>(spec, env, first_opt, n_opt);
+        default: return launch_hw<6, 4, true>(spec, env, first_opt, n_opt);
       }
   }
 }
+
+uint64_t binomial_scratch_bytes(const KernelSpec& spec) { return spec.binom.options * sizeof(OptionRec); }
 
 }  // namespace ecl

@@ -300,6 +300,7 @@ ecl::LaunchEnv env_of(const ecl_gpu* g, int lane) {
   env.scratch = g->scratch;
   env.device = g->ordinal;
   env.in_host = g->in_host_ptr.data();
+  env.extra_launches = const_cast<uint64_t*>(&g->launches);  // g itself is never a const object
   if (g->n_peers) {
     env.peer_out = g->peer_out.data();
     env.n_peers = g->n_peers;

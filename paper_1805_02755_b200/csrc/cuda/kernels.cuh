@@ -110,6 +110,9 @@ struct LaunchEnv {
   // there too, over NVLink, as it computes them.
   void* const* peer_out = nullptr;
   uint32_t n_peers = 0;
+  // The device's kernel-launch counter: the caller counts one launch per
+  // launch_kernel call, a launcher that issues more kernels adds the rest.
+  uint64_t* extra_launches = nullptr;
 };
 
 constexpr uint32_t kMaxPeerWrites = 8;  // peers a fused-exchange kernel writes to
@@ -134,6 +137,7 @@ inline CompactOut compact_of(const LaunchEnv& env) { return CompactOut{env.compa
 uint64_t scratch_bytes(const KernelSpec& spec);
 cudaError_t prepare_kernel(const KernelSpec& spec, const LaunchEnv& env);
 uint64_t mandelbrot_scratch_bytes(const KernelSpec& spec);
+uint64_t binomial_scratch_bytes(const KernelSpec& spec);
 cudaError_t prepare_mandelbrot(const KernelSpec& spec, const LaunchEnv& env);
 
 // Prefix of input `input` (bytes) the work-items [first, first+count) read:

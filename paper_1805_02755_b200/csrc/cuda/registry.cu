@@ -113,7 +113,7 @@ int resolve_kernel(KernelSpec& s, std::string* err) {
     switch (s.kind) {
       case KernelKind::Mandelbrot: max_variant = 15; break;
       case KernelKind::MandelbrotF32: max_variant = 2; break;
-      case KernelKind::Binomial: max_variant = 4; break;
+      case KernelKind::Binomial: max_variant = 5; break;
       case KernelKind::NBody: max_variant = 1; break;
       case KernelKind::Ray: max_variant = 2; break;
       case KernelKind::Gaussian: max_variant = 2; break;
@@ -250,6 +250,7 @@ uint64_t scratch_bytes(const KernelSpec& spec) {
   switch (spec.kind) {
     case KernelKind::Mandelbrot:
     case KernelKind::MandelbrotF32: return mandelbrot_scratch_bytes(spec);
+    case KernelKind::Binomial: return binomial_scratch_bytes(spec);  // option records (binomial@5)
     default: return 0;
   }
 }

@@ -72,7 +72,7 @@ def test_nbody_one_and_two_bodies(gpu_available, oracle):
         assert rel_ok(res.outputs[1].view(np.float32).reshape(-1, 4), nvel, 1e-4, atol=1e-6)
 
 
-@pytest.mark.parametrize("kernel", ["binomial", "binomial@1", "binomial@2", "binomial@3", "binomial@4"])
+@pytest.mark.parametrize("kernel", ["binomial", "binomial@1", "binomial@2", "binomial@3", "binomial@4", "binomial@5"])
 @pytest.mark.parametrize("steps", [1, 2, 15, 16, 17, 31, 32, 33, 63, 64, 127, 128, 129, 255])
 def test_binomial_depth_edges(gpu_available, oracle, steps, kernel):
     # phase boundaries of the lattices (multiples of 32 levels for the warp

@@ -127,7 +127,7 @@ def test_binomial_packed_lattice_is_bit_identical_to_scalar(gpu_available, tmp_p
     import subprocess
     import sys
     outs = []
-    for variant in ("1", "0", "3", "4"):
+    for variant in ("1", "0", "3", "4", "5"):
         f = tmp_path / f"v{variant}.npy"
         env = dict(os.environ, ECL_BINOMIAL_VARIANT=variant)
         r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, str(f)], env=env, capture_output=True,
