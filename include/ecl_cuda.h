@@ -248,9 +248,10 @@ int ecl_gpu_native_run_split(ecl_gpu* gpu, uint64_t items_per_launch, float* ker
  * first D2H of a package. */
 int ecl_gpu_set_copy_split(ecl_gpu* gpu, uint64_t items);
 /* For kernels whose outputs are replicated (Mandelbrot's 4 identical counts
- * per pixel): of every 8 pieces, `per_8` copy one value per item and are
- * widened by host threads, the others are copied whole.  Balances PCIe
- * bytes against host-DRAM traffic (default 8 = all widened). */
+ * per pixel): of every 8 pieces, `per_8` copy one value per item (uint16
+ * when the kernel's values fit 16 bits — Mandelbrot with max_iter < 65536 —
+ * else uint32) and are widened by host threads, the others are copied whole.
+ * Balances PCIe bytes against host-DRAM traffic (default 8 = all widened). */
 int ecl_gpu_set_widen_fraction(ecl_gpu* gpu, uint32_t per_8);
 
 /* Package kernel time (CUDA events, summed over packages) and the number of
