@@ -641,7 +641,8 @@ cudaError_t launch_binomial(const KernelSpec& spec, const LaunchEnv& env, uint64
     default:
       // measured with the setup inside the lattice kernel (MB, unroll):
       // (4,2) 13.57, (4,4) 12.93, (5,2) 12.97, (5,4) 12.84, (6,2) 12.69,
-      // (6,4) 12.69 ms; with the records computed ahead (default) 11.71 ms
+      // (6,4) 12.69 ms; with the records computed ahead (default): (6,4)
+      // 11.70, (5,4) 11.82, (4,4) 12.47, (6,2) 12.70, (6,3) 12.83, (6,8) 12.63
       switch ((mb ? mb : 6) * 10 + hw_unroll) {
         case 42: return launch_hw<4, 2, true>(spec, env, first_opt, n_opt);
         case 44: return launch_hw<4, 4, true>(spec, env, first_opt, n_opt);
