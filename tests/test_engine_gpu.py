@@ -389,17 +389,18 @@ def test_adaptive_hguided_learns_and_carries_powers(gpu_available, oracle):
     assert lp2[0] > lp2[1]  # the variant that skips periodic orbits is faster
 
 
+@pytest.mark.parametrize("kernel", ["mandelbrot", "mandelbrot_f32"])
 @pytest.mark.parametrize("max_iter", [65535, 65536, 70001])
-def test_compact_count_width_at_16_bit_boundary(gpu_available, oracle, max_iter):
+def test_compact_count_width_at_16_bit_boundary(gpu_available, oracle, max_iter, kernel):
     # Host-bound counts cross PCIe as uint16 when max_iter < 65536 (every
     # count fits) and as uint32 otherwise; interior pixels of this window
     # reach max_iter itself, so a truncated count would show.
     vp = (-0.9, -0.2, 0.5, 0.6)  # the main cardioid and its boundary: counts from 5 to max_iter
     w, h = 48, 32
-    prog = P.validate_program(W.mandelbrot_spec(w, h, max_iter, lws=32, viewport=vp))
+    prog = P.validate_program(W.mandelbrot_spec(w, h, max_iter, lws=32, viewport=vp, kernel=kernel))
     devs = [P.cuda_device(f"gpu{i}", 0, copy_split_items=256) for i in range(2)]
     with P.Engine(P.EngineConfig(devs, P.DynamicConfig(5)), prog) as e:
         got = e.run([]).outputs[0].view(np.uint32)
-    exp = oracle.mandelbrot(w, h, max_iter, viewport=vp)
+    exp = oracle.mandelbrot(w, h, max_iter, viewport=vp, f32=kernel == "mandelbrot_f32")
     assert int(exp.max()) == max_iter
     assert np.array_equal(got, expand_4to1(exp))
